@@ -17,9 +17,9 @@ def omega(n_b):
 
 
 def dft_matrix(n_b):
-    """F_{kt} = omega^{kt} (plain definition, k, t = 0..n_b-1)."""
+    """F_{kt} = omega^{kt} = exp(-2 pi i (k t mod n_b) / n_b) (plain definition, k, t = 0..n_b-1)."""
     k = np.arange(n_b)
-    return omega(n_b) ** np.outer(k, k)
+    return np.exp(-2j * np.pi * (np.outer(k, k) % n_b) / n_b)
 
 
 def circulant_C(n_b):
