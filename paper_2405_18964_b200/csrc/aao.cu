@@ -1,0 +1,1153 @@
+// C-ABI library: setup (step A9), KKT apply (A2), Algorithm-1 preconditioner (A3-A8)
+// and GMRES (A1) for the all-at-once Stokes/Oseen control system of arXiv 2405.18964.
+// See include/aao.h for the contract and DESIGN.md for the design.
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <chrono>
+#include <stdexcept>
+
+#include "aao_internal.h"
+
+using cplx = std::complex<double>;
+
+namespace aao {
+
+long& launch_counter() {
+  static long c = 0;
+  return c;
+}
+
+namespace {
+
+struct CudaError : std::runtime_error {
+  aao_status st;
+  CudaError(aao_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      throw CudaError(e_ == cudaErrorMemoryAllocation ? AAO_ERR_OOM : AAO_ERR_CUDA,           \
+                      std::string(#call) + ": " + cudaGetErrorString(e_));                    \
+  } while (0)
+
+template <class T>
+T* dalloc(Ctx& c, size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+  if (e != cudaSuccess) throw CudaError(AAO_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  c.allocs.push_back(p);
+  c.bytes += count * sizeof(T);
+  return static_cast<T*>(p);
+}
+
+template <class T>
+T* upload(Ctx& c, const std::vector<T>& h) {
+  T* d = dalloc<T>(c, h.size());
+  CK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+
+// ------------------------------------------------------------------ 1-D finite elements
+// 3-point Gauss-Legendre on [0,1]; quadratic (nodes 0, 1/2, 1) and linear Lagrange bases.
+struct Ref1D {
+  double gp[3], gw[3];
+  double phi[3][3], dphi[3][3];  // [basis][point]
+  double psi[2][3], dpsi[2][3];
+  double m2[3][3], k2[3][3], m1[2][2], k1[2][2], pm[2][3], gm[2][3];
+  Ref1D() {
+    const double s = std::sqrt(3.0 / 5.0);
+    const double xi[3] = {-s, 0.0, s}, w[3] = {5.0 / 9.0, 8.0 / 9.0, 5.0 / 9.0};
+    for (int q = 0; q < 3; ++q) {
+      gp[q] = 0.5 * (xi[q] + 1.0);
+      gw[q] = 0.5 * w[q];
+      const double x = gp[q];
+      phi[0][q] = 2 * (x - 0.5) * (x - 1);
+      phi[1][q] = 4 * x * (1 - x);
+      phi[2][q] = 2 * x * (x - 0.5);
+      dphi[0][q] = 4 * x - 3;
+      dphi[1][q] = 4 - 8 * x;
+      dphi[2][q] = 4 * x - 1;
+      psi[0][q] = 1 - x;
+      psi[1][q] = x;
+      dpsi[0][q] = -1;
+      dpsi[1][q] = 1;
+    }
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        m2[i][j] = k2[i][j] = 0;
+        for (int q = 0; q < 3; ++q) {
+          m2[i][j] += gw[q] * phi[i][q] * phi[j][q];
+          k2[i][j] += gw[q] * dphi[i][q] * dphi[j][q];
+        }
+      }
+    for (int i = 0; i < 2; ++i) {
+      for (int j = 0; j < 2; ++j) {
+        m1[i][j] = k1[i][j] = 0;
+        for (int q = 0; q < 3; ++q) {
+          m1[i][j] += gw[q] * psi[i][q] * psi[j][q];
+          k1[i][j] += gw[q] * dpsi[i][q] * dpsi[j][q];
+        }
+      }
+      for (int j = 0; j < 3; ++j) {
+        pm[i][j] = gm[i][j] = 0;
+        for (int q = 0; q < 3; ++q) {
+          pm[i][j] += gw[q] * psi[i][q] * phi[j][q];
+          gm[i][j] += gw[q] * psi[i][q] * dphi[j][q];
+        }
+      }
+    }
+  }
+};
+
+// assembled 1-D rows on N cells of width h
+struct Tables1D {
+  std::vector<double> M2, K2, M2full, M1, K1, Pm, Gm, PmT, GmT;
+};
+
+Tables1D tables_1d(const Ref1D& R, int N, double h) {
+  Tables1D T;
+  const int n1 = 2 * N + 1, m1 = N + 1;
+  T.M2.assign(n1 * 5, 0.0);
+  T.K2.assign(n1 * 5, 0.0);
+  for (int e = 0; e < N; ++e)
+    for (int li = 0; li < 3; ++li)
+      for (int lj = 0; lj < 3; ++lj) {
+        const int i = 2 * e + li, j = 2 * e + lj;
+        T.M2[i * 5 + (j - i + 2)] += h * R.m2[li][lj];
+        T.K2[i * 5 + (j - i + 2)] += R.k2[li][lj] / h;
+      }
+  T.M2full = T.M2;
+  for (int i = 0; i < n1; ++i)
+    for (int o = 0; o < 5; ++o) {
+      const int j = i + o - 2;
+      if (j <= 0 || j >= n1 - 1) {  // Dirichlet columns eliminated (and out of range)
+        T.M2[i * 5 + o] = 0.0;
+        T.K2[i * 5 + o] = 0.0;
+      }
+      if (j < 0 || j > n1 - 1) T.M2full[i * 5 + o] = 0.0;
+    }
+  T.M1.assign(m1 * 3, 0.0);
+  T.K1.assign(m1 * 3, 0.0);
+  for (int e = 0; e < N; ++e)
+    for (int li = 0; li < 2; ++li)
+      for (int lj = 0; lj < 2; ++lj) {
+        const int i = e + li, j = e + lj;
+        T.M1[i * 3 + (j - i + 1)] += h * R.m1[li][lj];
+        T.K1[i * 3 + (j - i + 1)] += R.k1[li][lj] / h;
+      }
+  // B rows: Q1 node I, Q2 columns 2I-2..2I+2
+  T.Pm.assign(m1 * 5, 0.0);
+  T.Gm.assign(m1 * 5, 0.0);
+  for (int e = 0; e < N; ++e)
+    for (int li = 0; li < 2; ++li)
+      for (int lj = 0; lj < 3; ++lj) {
+        const int I = e + li, j = 2 * e + lj;
+        T.Pm[I * 5 + (j - 2 * I + 2)] += h * R.pm[li][lj];
+        T.Gm[I * 5 + (j - 2 * I + 2)] += R.gm[li][lj];
+      }
+  for (int I = 0; I < m1; ++I)
+    for (int o = 0; o < 5; ++o) {
+      const int j = 2 * I + o - 2;
+      if (j <= 0 || j >= n1 - 1) T.Pm[I * 5 + o] = T.Gm[I * 5 + o] = 0.0;
+    }
+  T.PmT.assign(n1 * 3, 0.0);
+  T.GmT.assign(n1 * 3, 0.0);
+  for (int i = 0; i < n1; ++i) {
+    const int I0 = i >= 1 ? (i - 1) / 2 : -1;
+    for (int o = 0; o < 3; ++o) {
+      const int I = I0 + o;
+      if (I < 0 || I >= m1) continue;
+      const int off = i - 2 * I + 2;
+      if (off < 0 || off > 4) continue;
+      T.PmT[i * 3 + o] = T.Pm[I * 5 + off];
+      T.GmT[i * 3 + o] = T.Gm[I * 5 + off];
+    }
+  }
+  return T;
+}
+
+// prolongation tables, coarse N cells -> fine 2N cells (nodal interpolation; DESIGN.md reading)
+void transfer_1d(const Ref1D&, int Nc, int order, std::vector<double>& tP, std::vector<double>& tR) {
+  const int nf = order * 2 * Nc + 1, nc = order * Nc + 1;
+  std::vector<double> P((size_t)nf * nc, 0.0);
+  tP.assign((size_t)nf * 4, 0.0);
+  for (int f = 0; f < nf; ++f) {
+    const double x = f / (2.0 * order);
+    int e = (int)std::floor(x);
+    if (e > Nc - 1) e = Nc - 1;
+    const double xi = x - e;
+    double w[3];
+    if (order == 2) {
+      w[0] = 2 * (xi - 0.5) * (xi - 1);
+      w[1] = 4 * xi * (1 - xi);
+      w[2] = 2 * xi * (xi - 0.5);
+    } else {
+      w[0] = 1 - xi;
+      w[1] = xi;
+      w[2] = 0;
+    }
+    for (int a = 0; a < 3; ++a)
+      if (std::fabs(w[a]) < 1e-15) w[a] = 0.0;
+    tP[f * 4 + 0] = order * e;
+    for (int a = 0; a <= order; ++a) {
+      tP[f * 4 + 1 + a] = w[a];
+      P[(size_t)f * nc + order * e + a] += w[a];
+    }
+  }
+  tR.assign((size_t)nc * 7, 0.0);
+  for (int I = 0; I < nc; ++I)
+    for (int o = 0; o < 7; ++o) {
+      const int f = 2 * I + o - 3;
+      if (f < 0 || f >= nf) continue;
+      tR[I * 7 + o] = P[(size_t)f * nc + I];
+    }
+}
+
+// convection stencils N_ij = int phi_i (w_h . grad phi_j) by an element loop (3^d Gauss points)
+// on the Q2 space (order 2) or Q1 space (order 1) with the Q2 nodal wind of the level.
+void convection(const Ref1D& R, int dim, int N, double h, int order, const std::vector<double>& wind,
+                std::vector<double>& conv, std::vector<double>& convT) {
+  const int n1q2 = 2 * N + 1;
+  const long ns = (long)std::pow(n1q2, dim);
+  const int n1 = order * N + 1, W = 2 * order + 1, nl1 = order + 1;
+  const long n = (long)std::pow(n1, dim);
+  const int NS = (int)std::pow(W, dim);
+  const int nloc = (int)std::pow(nl1, dim), nq = (int)std::pow(3, dim), nw = (int)std::pow(3, dim);
+  // reference basis at tensor Gauss points
+  std::vector<double> bv(nloc * nq), bg(nloc * nq * dim), wv(nw * nq), wq(nq);
+  for (int q = 0; q < nq; ++q) {
+    int qa[3] = {q % 3, (q / 3) % 3, q / 9};
+    wq[q] = 1.0;
+    for (int a = 0; a < dim; ++a) wq[q] *= R.gw[qa[a]];
+    for (int l = 0; l < nloc; ++l) {
+      int la[3] = {l % nl1, (l / nl1) % nl1, l / (nl1 * nl1)};
+      double v = 1.0;
+      for (int a = 0; a < dim; ++a) v *= order == 2 ? R.phi[la[a]][qa[a]] : R.psi[la[a]][qa[a]];
+      bv[l * nq + q] = v;
+      for (int c = 0; c < dim; ++c) {
+        double g = 1.0;
+        for (int a = 0; a < dim; ++a) {
+          const double val = order == 2 ? (a == c ? R.dphi[la[a]][qa[a]] : R.phi[la[a]][qa[a]])
+                                        : (a == c ? R.dpsi[la[a]][qa[a]] : R.psi[la[a]][qa[a]]);
+          g *= val;
+        }
+        bg[(l * nq + q) * dim + c] = g;
+      }
+    }
+    for (int l = 0; l < nw; ++l) {
+      int la[3] = {l % 3, (l / 3) % 3, l / 9};
+      double v = 1.0;
+      for (int a = 0; a < dim; ++a) v *= R.phi[la[a]][qa[a]];
+      wv[l * nq + q] = v;
+    }
+  }
+  conv.assign((size_t)n * NS, 0.0);
+  const long E = (long)std::pow(N, dim);
+  const double scale = std::pow(h, dim - 1);
+  std::vector<double> wc(nq * dim);
+  for (long e = 0; e < E; ++e) {
+    int ec[3] = {(int)(e % N), (int)((e / N) % N), (int)(e / ((long)N * N))};
+    for (int q = 0; q < nq; ++q)
+      for (int c = 0; c < dim; ++c) {
+        double s = 0;
+        for (int l = 0; l < nw; ++l) {
+          int la[3] = {l % 3, (l / 3) % 3, l / 9};
+          long g = 0, st = 1;
+          for (int a = 0; a < dim; ++a) {
+            g += (2 * ec[a] + la[a]) * st;
+            st *= n1q2;
+          }
+          s += wind[(size_t)c * ns + g] * wv[l * nq + q];
+        }
+        wc[q * dim + c] = s;
+      }
+    for (int i = 0; i < nloc; ++i) {
+      int ia[3] = {i % nl1, (i / nl1) % nl1, i / (nl1 * nl1)};
+      long gi = 0, st = 1;
+      for (int a = 0; a < dim; ++a) {
+        gi += (order * ec[a] + ia[a]) * st;
+        st *= n1;
+      }
+      for (int j = 0; j < nloc; ++j) {
+        int ja[3] = {j % nl1, (j / nl1) % nl1, j / (nl1 * nl1)};
+        double val = 0;
+        for (int q = 0; q < nq; ++q) {
+          double adv = 0;
+          for (int c = 0; c < dim; ++c) adv += wc[q * dim + c] * bg[(j * nq + q) * dim + c];
+          val += wq[q] * bv[i * nq + q] * adv;
+        }
+        int off = 0, sw = 1;
+        for (int a = 0; a < dim; ++a) {
+          off += (ja[a] - ia[a] + order) * sw;
+          sw *= W;
+        }
+        conv[(size_t)gi * NS + off] += scale * val;
+      }
+    }
+  }
+  // eliminate: rows/columns of masked nodes (Dirichlet boundary for Q2, pinned node 0 for Q1)
+  auto is_masked = [&](long node) {
+    if (order == 1) return node == 0;
+    long t = node;
+    for (int a = 0; a < dim; ++a) {
+      const int ca = (int)(t % n1);
+      t /= n1;
+      if (ca == 0 || ca == n1 - 1) return true;
+    }
+    return false;
+  };
+  for (long i = 0; i < n; ++i) {
+    int ia[3] = {(int)(i % n1), (int)((i / n1) % n1), (int)(i / ((long)n1 * n1))};
+    const bool mi = is_masked(i);
+    for (int o = 0; o < NS; ++o) {
+      int oa[3] = {o % W, (o / W) % W, o / (W * W)};
+      long j = 0, st = 1;
+      bool inr = true;
+      for (int a = 0; a < dim; ++a) {
+        const int ja = ia[a] + oa[a] - order;
+        if (ja < 0 || ja >= n1) inr = false;
+        j += ja * st;
+        st *= n1;
+      }
+      if (mi || !inr || is_masked(j)) conv[(size_t)i * NS + o] = 0.0;
+    }
+  }
+  convT.assign((size_t)n * NS, 0.0);
+  for (long i = 0; i < n; ++i) {
+    int ia[3] = {(int)(i % n1), (int)((i / n1) % n1), (int)(i / ((long)n1 * n1))};
+    for (int o = 0; o < NS; ++o) {
+      int oa[3] = {o % W, (o / W) % W, o / (W * W)};
+      long j = 0, st = 1;
+      bool inr = true;
+      int oT = 0, sw = 1;
+      for (int a = 0; a < dim; ++a) {
+        const int ja = ia[a] + oa[a] - order;
+        if (ja < 0 || ja >= n1) inr = false;
+        j += ja * st;
+        st *= n1;
+        oT += (2 * order - oa[a]) * sw;
+        sw *= W;
+      }
+      if (inr) convT[(size_t)i * NS + o] = conv[(size_t)j * NS + oT];
+    }
+  }
+}
+
+// dense operator a M + b K + c C on the unknowns of a (small) grid, host evaluation of the stencil
+std::vector<cplx> dense_coarse(int dim, int order, int n1, const std::vector<double>& tM, const std::vector<double>& tK,
+                               const std::vector<double>* conv, cplx a, cplx b, cplx c, const std::vector<int>& unk) {
+  const int W = 2 * order + 1, NS = (int)std::pow(W, dim);
+  const int nu = (int)unk.size();
+  std::vector<cplx> A((size_t)nu * nu, 0.0);
+  for (int r = 0; r < nu; ++r) {
+    const int gi = unk[r];
+    int ia[3] = {gi % n1, (gi / n1) % n1, gi / (n1 * n1)};
+    for (int s = 0; s < nu; ++s) {
+      const int gj = unk[s];
+      int ja[3] = {gj % n1, (gj / n1) % n1, gj / (n1 * n1)};
+      bool ok = true;
+      int oa[3];
+      for (int x = 0; x < dim; ++x) {
+        oa[x] = ja[x] - ia[x] + order;
+        if (oa[x] < 0 || oa[x] >= W) ok = false;
+      }
+      if (!ok) continue;
+      double m = 1.0, k = 0.0;
+      for (int x = 0; x < dim; ++x) m *= tM[ia[x] * W + oa[x]];
+      for (int x = 0; x < dim; ++x) {
+        double t = tK[ia[x] * W + oa[x]];
+        for (int y = 0; y < dim; ++y)
+          if (y != x) t *= tM[ia[y] * W + oa[y]];
+        k += t;
+      }
+      cplx v = a * m + b * k;
+      if (conv) {
+        int off = 0, sw = 1;
+        for (int x = 0; x < dim; ++x) {
+          off += oa[x] * sw;
+          sw *= W;
+        }
+        v += c * (*conv)[(size_t)gi * NS + off];
+      }
+      A[(size_t)r * nu + s] = v;
+    }
+  }
+  return A;
+}
+
+// Gauss-Jordan inverse with partial pivoting
+bool invert(std::vector<cplx>& A, int n) {
+  std::vector<cplx> I((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) I[(size_t)i * n + i] = 1.0;
+  double amax = 0;
+  for (auto& v : A) amax = std::max(amax, std::abs(v));
+  for (int col = 0; col < n; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < n; ++r)
+      if (std::abs(A[(size_t)r * n + col]) > std::abs(A[(size_t)piv * n + col])) piv = r;
+    if (std::abs(A[(size_t)piv * n + col]) <= 1e-14 * amax) return false;
+    if (piv != col)
+      for (int j = 0; j < n; ++j) {
+        std::swap(A[(size_t)piv * n + j], A[(size_t)col * n + j]);
+        std::swap(I[(size_t)piv * n + j], I[(size_t)col * n + j]);
+      }
+    const cplx p = A[(size_t)col * n + col];
+    for (int j = 0; j < n; ++j) {
+      A[(size_t)col * n + j] /= p;
+      I[(size_t)col * n + j] /= p;
+    }
+    for (int r = 0; r < n; ++r) {
+      if (r == col) continue;
+      const cplx f = A[(size_t)r * n + col];
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) {
+        A[(size_t)r * n + j] -= f * A[(size_t)col * n + j];
+        I[(size_t)r * n + j] -= f * I[(size_t)col * n + j];
+      }
+    }
+  }
+  A = I;
+  return true;
+}
+
+inline double2 d2(cplx z) { return make_double2(z.real(), z.imag()); }
+inline Coef coef(cplx a, cplx b, cplx c) { return Coef{d2(a), d2(b), d2(c)}; }
+
+struct HostLevel {
+  int N;
+  double h;
+  Tables1D t;
+  std::vector<double> wind, conv, convT;    // Q2 (Oseen)
+};
+
+// ------------------------------------------------------------------ setup
+void setup(Ctx& c, const aao_config& cfg) {
+  c.cfg = cfg;
+  c.dim = cfg.dim;
+  c.Nc = cfg.n_cells;
+  c.n_t = cfg.n_t;
+  c.n_b = cfg.n_t - 1;
+  c.n_f = c.n_b / 2 + 1;
+  c.tau = cfg.T / cfg.n_t;
+  c.beta = cfg.beta;
+  c.nu = cfg.nu;
+  c.oseen = cfg.problem == AAO_OSEEN;
+  c.n1q2 = 2 * c.Nc + 1;
+  c.n1q1 = c.Nc + 1;
+  c.n_s = (long)std::pow(c.n1q2, c.dim);
+  c.n_p = (long)std::pow(c.n1q1, c.dim);
+  c.n_v = c.dim * c.n_s;
+  c.nblk = c.n_v + c.n_p;
+  c.N = 2L * c.n_b * c.nblk;
+  const int dim = c.dim;
+  const Ref1D R;
+
+  // levels N_c, N_c/2, ..., 2 (reading C.2 #12)
+  std::vector<HostLevel> L;
+  for (int N = c.Nc; N >= 2; N /= 2) {
+    HostLevel hl;
+    hl.N = N;
+    hl.h = (cfg.x_hi - cfg.x_lo) / N;
+    hl.t = tables_1d(R, N, hl.h);
+    L.push_back(std::move(hl));
+  }
+  const int nlev = (int)L.size();
+  if (c.oseen) {
+    L[0].wind.assign(cfg.wind_q2, cfg.wind_q2 + (size_t)dim * c.n_s);
+    for (int l = 1; l < nlev; ++l) {  // injection: coarse node I <-> fine node 2I
+      const int nf1 = 2 * L[l - 1].N + 1, nc1 = 2 * L[l].N + 1;
+      const long ncn = (long)std::pow(nc1, dim), nfn = (long)std::pow(nf1, dim);
+      L[l].wind.assign((size_t)dim * ncn, 0.0);
+      for (long I = 0; I < ncn; ++I) {
+        long f = 0, st = 1, t = I;
+        for (int a = 0; a < dim; ++a) {
+          f += 2 * (t % nc1) * st;
+          t /= nc1;
+          st *= nf1;
+        }
+        for (int comp = 0; comp < dim; ++comp) L[l].wind[(size_t)comp * ncn + I] = L[l - 1].wind[(size_t)comp * nfn + f];
+      }
+    }
+    for (int l = 0; l < nlev; ++l) convection(R, dim, L[l].N, L[l].h, 2, L[l].wind, L[l].conv, L[l].convT);
+  }
+
+  // MG spaces
+  for (int sp = 0; sp < 2; ++sp) {
+    MGSpace& S = sp == 0 ? c.vel : c.pres;
+    const int order = sp == 0 ? 2 : 1;
+    S.order = order;
+    S.nlev = nlev;
+    S.grids.resize(nlev);
+    S.transfers.resize(nlev);
+    for (int l = 0; l < nlev; ++l) {
+      Grid& g = S.grids[l];
+      g.dim = dim;
+      g.order = order;
+      g.n1 = order * L[l].N + 1;
+      g.n = (long)std::pow(g.n1, dim);
+      g.tM = upload(c, order == 2 ? L[l].t.M2 : L[l].t.M1);
+      g.tK = upload(c, order == 2 ? L[l].t.K2 : L[l].t.K1);
+      g.conv = g.convT = nullptr;
+      if (order == 2 && c.oseen) {
+        g.conv = upload(c, L[l].conv);
+        g.convT = upload(c, L[l].convT);
+      }
+      if (l + 1 < nlev) {
+        std::vector<double> tP, tR;
+        transfer_1d(R, L[l + 1].N, order, tP, tR);
+        S.transfers[l].tP = upload(c, tP);
+        S.transfers[l].tR = upload(c, tR);
+      }
+    }
+    // coarsest-level unknowns
+    const Grid& gc = S.grids[nlev - 1];
+    std::vector<int> unk;
+    for (long i = 0; i < gc.n; ++i) {
+      bool m;
+      if (order == 1) {
+        m = i == 0;
+      } else {
+        m = false;
+        long t = i;
+        for (int a = 0; a < dim; ++a) {
+          const int ca = (int)(t % gc.n1);
+          t /= gc.n1;
+          m = m || ca == 0 || ca == gc.n1 - 1;
+        }
+      }
+      if (!m) unk.push_back((int)i);
+    }
+    S.ncoarse_unk = (int)unk.size();
+    S.coarse_unk = upload(c, unk);
+  }
+  // fine pressure convection (Oseen Schur complement)
+  if (c.oseen) {
+    std::vector<double> cp, cpT;
+    convection(R, dim, c.Nc, L[0].h, 1, L[0].wind, cp, cpT);
+    c.pres.grids[0].conv = upload(c, cp);
+    c.pres.grids[0].convT = upload(c, cpT);
+  }
+  c.tPm = upload(c, L[0].t.Pm);
+  c.tGm = upload(c, L[0].t.Gm);
+  c.tPmT = upload(c, L[0].t.PmT);
+  c.tGmT = upload(c, L[0].t.GmT);
+  c.tMfull = upload(c, L[0].t.M2full);
+
+  // frequency constants: d_k = 1 - exp(-2 pi i k / n_b) (reading C.2 #2)
+  const int n_f = c.n_f, n_b = c.n_b;
+  const double tau = c.tau, beta = c.beta, nu = c.nu;
+  std::vector<cplx> d(n_f);
+  c.fch.resize(n_f);
+  for (int k = 0; k < n_f; ++k) {
+    const double th = 2.0 * M_PI * (double)k / n_b;
+    d[k] = cplx(1.0 - std::cos(th), std::sin(th));
+    FreqConst& f = c.fch[k];
+    f.dr = d[k].real();
+    f.dc = d[k].imag();
+    f.c1 = f.dr / std::sqrt(tau * tau / beta + f.dc * f.dc);       // squared reading (C.2 #1)
+    f.c2 = 1.0 / std::sqrt(1.0 / beta + f.dc * f.dc / (tau * tau));
+  }
+  c.fc = upload(c, c.fch);
+  std::vector<double2> tw(n_b);
+  for (int m = 0; m < n_b; ++m) {
+    const double th = 2.0 * M_PI * (double)m / n_b;
+    tw[m] = make_double2(std::cos(th), std::sin(th));
+  }
+  c.tw = upload(c, tw);
+
+  // coefficient tables and coarse inverses
+  const Grid& gv = c.vel.grids[nlev - 1];
+  const Grid& gp = c.pres.grids[nlev - 1];
+  std::vector<int> unk_v(c.vel.ncoarse_unk), unk_p(c.pres.ncoarse_unk);
+  CK(cudaMemcpy(unk_v.data(), c.vel.coarse_unk, unk_v.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(unk_p.data(), c.pres.coarse_unk, unk_p.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  const HostLevel& LC = L[nlev - 1];
+  auto inv_of = [&](int order, cplx a, cplx b, cplx cc, const std::vector<double>* conv, const std::vector<int>& unk) {
+    const Tables1D& t = LC.t;
+    std::vector<cplx> A = dense_coarse(dim, order, order == 2 ? gv.n1 : gp.n1, order == 2 ? t.M2 : t.M1,
+                                       order == 2 ? t.K2 : t.K1, conv, a, b, cc, unk);
+    if (!invert(A, (int)unk.size())) throw CudaError(AAO_ERR_NUMERIC, "singular coarse-grid matrix");
+    std::vector<double2> out(A.size());
+    for (size_t i = 0; i < A.size(); ++i) out[i] = d2(A[i]);
+    return out;
+  };
+  auto append = [](std::vector<double2>& dst, const std::vector<double2>& src) {
+    dst.insert(dst.end(), src.begin(), src.end());
+  };
+  c.coefKp = upload(c, std::vector<Coef>{coef(0.0, 1.0, 0.0)});
+  c.coefMass = upload(c, std::vector<Coef>{coef(1.0, 0.0, 0.0)});
+  c.invKp = upload(c, inv_of(1, 0.0, 1.0, 0.0, nullptr, unk_p));
+  if (!c.oseen) {
+    std::vector<Coef> cw(n_f);
+    std::vector<double2> iw;
+    for (int k = 0; k < n_f; ++k) {
+      // W_k = (1 + c_{k,1}) M + c_{k,2} L, L = nu K
+      const cplx a = 1.0 + c.fch[k].c1, b = c.fch[k].c2 * nu;
+      cw[k] = coef(a, b, 0.0);
+      append(iw, inv_of(2, a, b, 0.0, nullptr, unk_v));
+    }
+    c.coefW = upload(c, cw);
+    c.invW = upload(c, iw);
+  } else {
+    // Q_k = d_k M + tau L + (tau/sqrt(beta)) M, L = nu K + N; Q_k^H uses N^T
+    std::vector<Coef> cq(n_f), cqh(n_f), u2(n_f), u3(n_f), s2(n_f), s3(n_f);
+    std::vector<double2> iq, iqh;
+    const double sb = tau / std::sqrt(beta);
+    for (int k = 0; k < n_f; ++k) {
+      const cplx sh = d[k] + sb;
+      cq[k] = coef(sh, tau * nu, tau);
+      cqh[k] = coef(std::conj(sh), tau * nu, tau);
+      append(iq, inv_of(2, sh, tau * nu, tau, &LC.conv, unk_v));
+      append(iqh, inv_of(2, std::conj(sh), tau * nu, tau, &LC.convT, unk_v));
+      u2[k] = coef(-std::conj(d[k]), -tau * nu, -tau);   // -(d^* M + tau L^T)       (Uzawa x1 update)
+      u3[k] = coef(-d[k], -tau * nu, -tau);              // -(d M + tau L)           (Uzawa x2 update)
+      s2[k] = coef(std::conj(d[k]), tau * nu, tau);      // d^* M_p + tau L_p^T      (Schur middle block)
+      s3[k] = coef(d[k], tau * nu, tau);                 // d M_p + tau L_p
+    }
+    c.coefQ = upload(c, cq);
+    c.coefQH = upload(c, cqh);
+    c.invQ = upload(c, iq);
+    c.invQH = upload(c, iqh);
+    c.coefU1 = upload(c, std::vector<Coef>{coef(-tau, 0.0, 0.0)});
+    c.coefU2 = upload(c, u2);
+    c.coefU3 = upload(c, u3);
+    c.coefU4 = upload(c, std::vector<Coef>{coef(tau / beta, 0.0, 0.0)});
+    c.coefS1 = upload(c, std::vector<Coef>{coef(tau, 0.0, 0.0)});
+    c.coefS2 = upload(c, s2);
+    c.coefS3 = upload(c, s3);
+    c.coefS4 = upload(c, std::vector<Coef>{coef(-tau / beta, 0.0, 0.0)});
+  }
+
+  // frequency-domain arrays and workspaces
+  const long fv = (long)n_f * 2 * dim * c.n_s, fp = (long)n_f * 2 * c.n_p;
+  c.Fv = dalloc<double2>(c, fv);
+  c.Fp = dalloc<double2>(c, fp);
+  c.XpA = dalloc<double2>(c, fp);
+  const int nprob_v = c.oseen ? n_f * dim : n_f * 2 * dim;
+  const int nprob_p = 2 * n_f;
+  long cheb_len = (long)nprob_p * c.n_p;
+  if (c.oseen) {
+    const long vv = (long)n_f * dim * c.n_s;
+    c.X1 = dalloc<double2>(c, vv);
+    c.X2 = dalloc<double2>(c, vv);
+    c.T1 = dalloc<double2>(c, vv);
+    c.T2 = dalloc<double2>(c, vv);
+    c.T3 = dalloc<double2>(c, vv);
+    c.Qp = dalloc<double2>(c, fp);
+    c.Sp = dalloc<double2>(c, fp);
+    c.Tp = dalloc<double2>(c, fp);
+    cheb_len = std::max(cheb_len, vv);
+  } else {
+    c.Xv = dalloc<double2>(c, fv);
+    c.XpB = dalloc<double2>(c, fp);
+  }
+  c.Cr = dalloc<double2>(c, cheb_len);
+  c.Cd0 = dalloc<double2>(c, cheb_len);
+  c.Cd1 = dalloc<double2>(c, cheb_len);
+  for (int sp = 0; sp < 2; ++sp) {
+    MGSpace& S = sp == 0 ? c.vel : c.pres;
+    const int np = sp == 0 ? nprob_v : nprob_p;
+    S.nprob_max = np;
+    S.x.assign(nlev, nullptr);
+    S.b.assign(nlev, nullptr);
+    S.r.assign(nlev, nullptr);
+    for (int l = 0; l < nlev; ++l) {
+      const long n = S.grids[l].n * (long)np;
+      S.r[l] = dalloc<double2>(c, n);
+      if (l > 0) {
+        S.x[l] = dalloc<double2>(c, n);
+        S.b[l] = dalloc<double2>(c, n);
+      }
+    }
+  }
+  CK(cudaMemset(c.Fv, 0, fv * sizeof(double2)));
+  CK(cudaMemset(c.Fp, 0, fp * sizeof(double2)));
+  CK(cudaMemset(c.XpA, 0, fp * sizeof(double2)));
+  if (c.Xv) CK(cudaMemset(c.Xv, 0, fv * sizeof(double2)));
+  if (c.XpB) CK(cudaMemset(c.XpB, 0, fp * sizeof(double2)));
+  if (c.X1) {
+    CK(cudaMemset(c.X1, 0, (size_t)n_f * dim * c.n_s * sizeof(double2)));
+    CK(cudaMemset(c.X2, 0, (size_t)n_f * dim * c.n_s * sizeof(double2)));
+  }
+  CK(cudaDeviceSynchronize());
+}
+
+// ------------------------------------------------------------------ block solvers
+inline View contig(double2* p, long n) { return View{p, 1, n}; }
+
+void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, int inv_pg, View x, View b, int nprob,
+               cudaStream_t s) {
+  const Grid& g = S.grids[l];
+  auto& cnt = launch_counter();
+  if (l == S.nlev - 1) {
+    launch_coarse(g, inv, inv_pg, S.coarse_unk, S.ncoarse_unk, b, x, nprob, s);
+    ++cnt;
+    return;
+  }
+  const int C = S.order == 2 ? (c.dim == 2 ? 9 : 27) : (c.dim == 2 ? 4 : 8);
+  for (int sw = 0; sw < c.cfg.pre_sweeps; ++sw)
+    for (int col = 0; col < C; ++col) {
+      launch_gs(g, op, x, b, nprob, col, c.cfg.omega, s);
+      ++cnt;
+    }
+  View r = contig(S.r[l], g.n);
+  launch_residual(g, op, x, b, r, nprob, s);
+  const Grid& gc = S.grids[l + 1];
+  View bc = contig(S.b[l + 1], gc.n), xc = contig(S.x[l + 1], gc.n);
+  launch_restrict(g, gc, S.transfers[l], r, bc, nprob, s);
+  launch_zero(xc, gc.n, nprob, s);
+  cnt += 3;
+  mg_vcycle(c, S, l + 1, op, inv, inv_pg, xc, bc, nprob, s);
+  launch_prolong(g, gc, S.transfers[l], xc, x, nprob, s);
+  ++cnt;
+  for (int sw = 0; sw < c.cfg.post_sweeps; ++sw)
+    for (int col = C - 1; col >= 0; --col) {
+      launch_gs(g, op, x, b, nprob, col, c.cfg.omega, s);
+      ++cnt;
+    }
+}
+
+// x = MG(A; b): mg_cycles V-cycles from x = 0
+void mg_solve(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, int inv_pg, View x, View b, int nprob,
+              cudaStream_t s) {
+  launch_zero(x, S.grids[0].n, nprob, s);
+  ++launch_counter();
+  for (int cyc = 0; cyc < c.cfg.mg_cycles; ++cyc) mg_vcycle(c, S, 0, op, inv, inv_pg, x, b, nprob, s);
+}
+
+// x = scale * Chebyshev(M; b), Jacobi-preconditioned, Wathen bounds
+void cheb_solve(Ctx& c, const Grid& g, View b, View x, int nprob, double scale, cudaStream_t s) {
+  const double lo1 = 0.5, hi1 = g.order == 2 ? 1.25 : 1.5;
+  const double lo = std::pow(lo1, c.dim), hi = std::pow(hi1, c.dim);
+  const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+  View r = contig(c.Cr, g.n), d0 = contig(c.Cd0, g.n), d1 = contig(c.Cd1, g.n);
+  launch_cheb_init(g, b, x, r, d0, 1.0 / theta, nprob, s);
+  double rho = 1.0 / sigma;
+  for (int k = 0; k < c.cfg.cheb_iters - 1; ++k) {
+    const double rho1 = 1.0 / (2.0 * sigma - rho);
+    launch_cheb_step(g, x, r, d0, d1, rho1 * rho, 2.0 * rho1 / delta, nprob, s);
+    std::swap(d0, d1);
+    rho = rho1;
+  }
+  launch_cheb_final(g, x, d0, scale, nprob, s);
+  launch_counter() += c.cfg.cheb_iters + 1;
+}
+
+void precond_stokes(Ctx& c, cudaStream_t s) {
+  const int dim = c.dim, n_f = c.n_f;
+  const Grid& gv = c.vel.grids[0];
+  const Grid& gp = c.pres.grids[0];
+  // x1 = MG(W; s1), x2 = MG(W; s2) per velocity component
+  OpSel opW{c.coefW, 2 * dim, 0};
+  mg_solve(c, c.vel, opW, c.invW, 2 * dim, contig(c.Xv, gv.n), contig(c.Fv, gv.n), n_f * 2 * dim, s);
+  if (c.timing) cudaEventRecord(c.ev[2], s);
+  // pressure slots: K_p^{-1} by MG and M_p^{-1} by Chebyshev, combined in the inverse transform
+  OpSel opKp{c.coefKp, 1 << 30, 0};
+  mg_solve(c, c.pres, opKp, c.invKp, 1 << 30, contig(c.XpA, gp.n), contig(c.Fp, gp.n), 2 * n_f, s);
+  cheb_solve(c, gp, contig(c.Fp, gp.n), contig(c.XpB, gp.n), 2 * n_f, 1.0, s);
+}
+
+void precond_oseen(Ctx& c, cudaStream_t s) {
+  const int dim = c.dim, n_f = c.n_f;
+  const Grid& gv = c.vel.grids[0];
+  const Grid& gp = c.pres.grids[0];
+  const long nv = gv.n, np = gp.n;
+  const int nprob = n_f * dim;
+  const double tau = c.tau, mu = c.cfg.uzawa_mu;
+  View B1{c.Fv, dim, 2L * dim * nv}, B2{c.Fv + (long)dim * nv, dim, 2L * dim * nv};
+  View X1 = contig(c.X1, nv), X2 = contig(c.X2, nv), T1 = contig(c.T1, nv), T2 = contig(c.T2, nv),
+       T3 = contig(c.T3, nv);
+  OpSel U1{c.coefU1, 1 << 30, 0}, U2{c.coefU2, dim, 2}, U3{c.coefU3, dim, 1}, U4{c.coefU4, 1 << 30, 0};
+  OpSel Mass{c.coefMass, 1 << 30, 0};
+  OpSel opQ{c.coefQ, dim, 1}, opQH{c.coefQH, dim, 2};
+  auto& cnt = launch_counter();
+  launch_zero(X1, nv, nprob, s);
+  launch_zero(X2, nv, nprob, s);
+  cnt += 2;
+  for (int it = 0; it < c.cfg.uzawa_iters; ++it) {
+    // x1 <- x1 + (1/tau) Mhat^{-1}(b1 - tau M x1 - (d M + tau L)^H x2)     (eq. Uzawa11)
+    launch_lincomb(gv, T1, 1.0, B1, U1, X1, U2, X2, nprob, s);
+    cheb_solve(c, gv, T1, T2, nprob, 1.0, s);
+    launch_axpby(gv, X1, make_double2(1, 0), T2, make_double2(1.0 / tau, 0), nprob, s);
+    // x2 <- x2 - (1/mu) S^{-1}(b2 - (d M + tau L) x1 + (tau/beta) M x2),  S^{-1} = tau Q^{-H} M Q^{-1}
+    launch_lincomb(gv, T1, 1.0, B2, U3, X1, U4, X2, nprob, s);
+    cnt += 3;
+    mg_solve(c, c.vel, opQ, c.invQ, dim, T2, T1, nprob, s);
+    launch_lincomb(gv, T3, 0.0, T1, Mass, T2, Mass, View{nullptr, 1, 0}, nprob, s);
+    ++cnt;
+    mg_solve(c, c.vel, opQH, c.invQH, dim, T2, T3, nprob, s);
+    launch_axpby(gv, X2, make_double2(1, 0), T2, make_double2(-tau / mu, 0), nprob, s);
+    ++cnt;
+  }
+  if (c.timing) cudaEventRecord(c.ev[2], s);
+  // (y3, y4) = -S_hat^{-1}((r3, r4) - tau (B y2, B y1))   (Algorithm 3)
+  View Xv2{c.X2, dim, (long)dim * nv}, Xv1{c.X1, dim, (long)dim * nv};
+  View P3{c.Fp, 1, 2 * np}, P4{c.Fp + np, 1, 2 * np};
+  View Q3{c.Qp, 1, 2 * np}, Q4{c.Qp + np, 1, 2 * np};
+  launch_Bv(gv, gp, c.tPm, c.tGm, Xv2, P3, Q3, 1.0, -tau, n_f, s);
+  launch_Bv(gv, gp, c.tPm, c.tGm, Xv1, P4, Q4, 1.0, -tau, n_f, s);
+  // S_hat^{-1}: [[0,tau M_p],[tau M_p,0]]^{-1} -> Sp[k][0] = s2 = M_p^{-1} q3 / tau, Sp[k][1] = s1 = M_p^{-1} q4 / tau
+  cheb_solve(c, gp, contig(c.Qp, np), contig(c.Sp, np), 2 * n_f, 1.0 / tau, s);
+  View s2v{c.Sp, 1, 2 * np}, s1v{c.Sp + np, 1, 2 * np};
+  View t2v{c.Tp, 1, 2 * np}, t1v{c.Tp + np, 1, 2 * np};
+  OpSel S1{c.coefS1, 1 << 30, 0}, S2{c.coefS2, 1, 2}, S3{c.coefS3, 1, 1}, S4{c.coefS4, 1 << 30, 0};
+  // t1 = tau M_p s1 + (d^* M_p + tau L_p^T) s2 ;  t2 = (d M_p + tau L_p) s1 - (tau/beta) M_p s2
+  launch_lincomb(gp, t1v, 0.0, t1v, S1, s1v, S2, s2v, n_f, s);
+  launch_lincomb(gp, t2v, 0.0, t2v, S3, s1v, S4, s2v, n_f, s);
+  cnt += 4;
+  // [[0,tau K_p],[tau K_p,0]]^{-1}: XpA[k][0] = K_p^{-1} t2, XpA[k][1] = K_p^{-1} t1 (scaled by -1/tau on output)
+  OpSel opKp{c.coefKp, 1 << 30, 0};
+  mg_solve(c, c.pres, opKp, c.invKp, 1 << 30, contig(c.XpA, np), contig(c.Tp, np), 2 * n_f, s);
+}
+
+void precond_apply(Ctx& c, const double* r, double* z, cudaStream_t s) {
+  if (c.timing) cudaEventRecord(c.ev[0], s);
+  launch_fft_fwd(c, r, s);
+  ++launch_counter();
+  if (c.timing) cudaEventRecord(c.ev[1], s);
+  if (c.oseen)
+    precond_oseen(c, s);
+  else
+    precond_stokes(c, s);
+  if (c.timing) cudaEventRecord(c.ev[3], s);
+  launch_fft_inv(c, z, s);
+  ++launch_counter();
+  if (c.timing) cudaEventRecord(c.ev[4], s);
+}
+
+void kkt_apply(Ctx& c, const double* x, double* y, cudaStream_t s) {
+  launch_kkt(c, x, y, s);
+  launch_counter() += 2;
+}
+
+// ------------------------------------------------------------------ GMRES
+void gmres_alloc(Ctx& c, int m) {
+  if (c.gm_m >= m) return;
+  if (c.gm_m > 0) throw CudaError(AAO_ERR_CONFIG, "GMRES restart larger than the first solve's is not supported");
+  const long N = c.N;
+  c.gV = dalloc<double>(c, (size_t)(m + 1) * N);
+  c.gz = dalloc<double>(c, N);
+  c.gu = dalloc<double>(c, N);
+  c.gr = dalloc<double>(c, N);
+  c.gH = dalloc<double>(c, (size_t)(m + 2) * (m + 1));
+  c.gpart = dalloc<double>(c, dot_blocks());
+  c.gscal = dalloc<double>(c, 4 * (m + 2));
+  std::vector<double*> ptr(m + 1);
+  for (int i = 0; i <= m; ++i) ptr[i] = c.gV + (size_t)i * N;
+  c.gVptr = upload(c, ptr);
+  CK(cudaMallocHost(&c.hostH, sizeof(double) * (m + 2) * 2));
+  c.gm_m = m;
+}
+
+double dot_host(Ctx& c, const double* x, const double* y, int mode, cudaStream_t s) {
+  launch_dot(x, y, c.N, c.gpart, dot_blocks(), c.gscal, mode, s);
+  launch_counter() += 2;
+  CK(cudaMemcpyAsync(c.hostH, c.gscal, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return c.hostH[0];
+}
+
+aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_info* info, double* hist, int hist_cap,
+                 cudaStream_t s) {
+  const int m = kry.restart;
+  gmres_alloc(c, m);
+  const long N = c.N;
+  auto t0 = std::chrono::steady_clock::now();
+  aao_info inf;
+  std::memset(&inf, 0, sizeof(inf));
+  const double bnorm = dot_host(c, b, b, 1, s);
+  int nh = 0;
+  if (bnorm == 0.0) {
+    CK(cudaMemsetAsync(x, 0, N * sizeof(double), s));
+    CK(cudaStreamSynchronize(s));
+    inf.converged = 1;
+    if (info) *info = inf;
+    return AAO_OK;
+  }
+  // r = b - A x0
+  kkt_apply(c, x, c.gz, s);
+  launch_copy_sub(c.gr, b, c.gz, N, s);
+  ++launch_counter();
+  int it = 0;
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
+  bool stop = false;
+  for (;;) {
+    const double beta0 = dot_host(c, c.gr, c.gr, 1, s);
+    double* V0 = c.gV;
+    launch_scale_dev(V0, c.gr, c.gscal, N, s);
+    ++launch_counter();
+    std::fill(H.begin(), H.end(), 0.0);
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta0;
+    int kdone = 0;
+    for (int k = 0; k < m; ++k) {
+      double* Vk = c.gV + (size_t)k * N;
+      double* w = c.gV + (size_t)(k + 1) * N;
+      precond_apply(c, Vk, c.gz, s);
+      kkt_apply(c, c.gz, w, s);
+      inf.precond_applies++;
+      // modified Gram-Schmidt with device-resident coefficients
+      double* hcol = c.gH + (size_t)k * (m + 1);
+      for (int i = 0; i <= k; ++i) {
+        launch_dot(w, c.gV + (size_t)i * N, N, c.gpart, dot_blocks(), hcol + i, 0, s);
+        launch_axpy_dev(w, c.gV + (size_t)i * N, hcol + i, -1.0, N, s);
+        launch_counter() += 3;
+      }
+      launch_dot(w, w, N, c.gpart, dot_blocks(), hcol + k + 1, 1, s);
+      launch_counter() += 2;
+      CK(cudaMemcpyAsync(c.hostH, hcol, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int i = 0; i <= k + 1; ++i) H[(size_t)i * m + k] = c.hostH[i];
+      // Givens rotations (same arithmetic as oracle/gmres.py)
+      for (int i = 0; i < k; ++i) {
+        const double t = cs[i] * H[(size_t)i * m + k] + sn[i] * H[(size_t)(i + 1) * m + k];
+        H[(size_t)(i + 1) * m + k] = -sn[i] * H[(size_t)i * m + k] + cs[i] * H[(size_t)(i + 1) * m + k];
+        H[(size_t)i * m + k] = t;
+      }
+      const double hkk = H[(size_t)k * m + k], hk1 = H[(size_t)(k + 1) * m + k];
+      const double den = std::hypot(hkk, hk1);
+      cs[k] = hkk / den;
+      sn[k] = hk1 / den;
+      H[(size_t)k * m + k] = den;
+      H[(size_t)(k + 1) * m + k] = 0.0;
+      g[k + 1] = -sn[k] * g[k];
+      g[k] = cs[k] * g[k];
+      ++it;
+      kdone = k + 1;
+      const double rel = std::fabs(g[k + 1]) / bnorm;
+      if (hist && nh < hist_cap) hist[nh++] = rel;
+      inf.final_relres = rel;
+      if (!std::isfinite(rel)) throw CudaError(AAO_ERR_NUMERIC, "NaN/Inf in GMRES");
+      if (std::fabs(g[k + 1]) <= kry.tol * bnorm) {
+        inf.converged = 1;
+        stop = true;
+        break;
+      }
+      if (hk1 < 1e-14 * bnorm) {
+        inf.breakdown = 1;
+        stop = true;
+        break;
+      }
+      if (it >= kry.max_iters) {
+        stop = true;
+        break;
+      }
+      launch_scale_dev(w, w, hcol + k + 1, N, s);
+      ++launch_counter();
+    }
+    // x += P^{-1}(V_k y), H_k y = g_k
+    for (int i = kdone - 1; i >= 0; --i) {
+      double acc = g[i];
+      for (int j = i + 1; j < kdone; ++j) acc -= H[(size_t)i * m + j] * y[j];
+      y[i] = acc / H[(size_t)i * m + i];
+    }
+    CK(cudaMemcpyAsync(c.gscal + 8, y.data(), sizeof(double) * kdone, cudaMemcpyHostToDevice, s));
+    launch_multi_axpy(c.gu, (const double* const*)c.gVptr, c.gscal + 8, kdone, N, s);
+    ++launch_counter();
+    precond_apply(c, c.gu, c.gz, s);
+    inf.precond_applies++;
+    launch_axpy(x, c.gz, 1.0, N, s);
+    kkt_apply(c, x, c.gz, s);
+    launch_copy_sub(c.gr, b, c.gz, N, s);
+    launch_counter() += 2;
+    inf.true_relres = dot_host(c, c.gr, c.gr, 1, s) / bnorm;
+    if (stop) break;
+    inf.restarts++;
+  }
+  inf.iterations = it;
+  inf.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (info) *info = inf;
+  return inf.converged ? AAO_OK : AAO_NOT_CONVERGED;
+}
+
+}  // namespace
+}  // namespace aao
+
+// ====================================================================== C ABI
+struct aao_ctx {
+  aao::Ctx c;
+  long launches_last = 0;
+};
+
+using aao::CudaError;
+
+static aao_status fail(aao_ctx* ctx, aao_status st, const std::string& msg) {
+  if (ctx) ctx->c.err = msg;
+  return st;
+}
+
+#define ABI_GUARD(ctx, body)                                         \
+  try {                                                              \
+    ctx->c.err.clear();                                              \
+    const long l0_ = aao::launch_counter();                          \
+    body;                                                            \
+    ctx->launches_last = aao::launch_counter() - l0_;                \
+    cudaError_t e_ = cudaGetLastError();                             \
+    if (e_ != cudaSuccess) return fail(ctx, AAO_ERR_CUDA, cudaGetErrorString(e_)); \
+  } catch (const CudaError& e) {                                     \
+    return fail(ctx, e.st, e.what());                                \
+  } catch (const std::exception& e) {                                \
+    return fail(ctx, AAO_ERR_CUDA, e.what());                        \
+  }
+
+extern "C" {
+
+void aao_config_defaults(aao_config* cfg) {
+  if (!cfg) return;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->dim = 2;
+  cfg->n_cells = 8;
+  cfg->x_lo = 0.0;
+  cfg->x_hi = 1.0;
+  cfg->n_t = 16;
+  cfg->T = 1.0;
+  cfg->beta = 1e-2;
+  cfg->nu = 1e-2;
+  cfg->problem = AAO_STOKES;
+  cfg->wind_q2 = nullptr;
+  cfg->mg_cycles = 4;
+  cfg->pre_sweeps = 2;
+  cfg->post_sweeps = 2;
+  cfg->omega = 1.0;
+  cfg->cheb_iters = 10;
+  cfg->uzawa_iters = 6;
+  cfg->uzawa_mu = 0.75;
+}
+
+aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
+  if (!cfg || !out) return AAO_ERR_SHAPE;
+  *out = nullptr;
+  const int N = cfg->n_cells;
+  const bool pow2 = N >= 4 && (N & (N - 1)) == 0;
+  if ((cfg->dim != 2 && cfg->dim != 3) || !pow2 || cfg->n_t < 3 || !(cfg->T > 0) || !(cfg->beta > 0) ||
+      !(cfg->nu > 0) || !(cfg->x_hi > cfg->x_lo) || (cfg->problem != AAO_STOKES && cfg->problem != AAO_OSEEN) ||
+      (cfg->problem == AAO_OSEEN && cfg->wind_q2 == nullptr) || cfg->mg_cycles < 1 || cfg->cheb_iters < 1 ||
+      cfg->uzawa_iters < 1 || !(cfg->uzawa_mu > 0) || cfg->pre_sweeps < 0 || cfg->post_sweeps < 0)
+    return AAO_ERR_CONFIG;
+  aao_ctx* ctx = new aao_ctx();
+  try {
+    aao::setup(ctx->c, *cfg);
+    for (auto& e : ctx->c.ev) cudaEventCreate(&e);
+  } catch (const CudaError& e) {
+    std::fprintf(stderr, "aao_create: %s\n", e.what());
+    aao_status st = e.st;
+    aao_destroy(ctx);
+    return st;
+  }
+  *out = ctx;
+  return AAO_OK;
+}
+
+void aao_destroy(aao_ctx* ctx) {
+  if (!ctx) return;
+  for (void* p : ctx->c.allocs) cudaFree(p);
+  if (ctx->c.hostH) cudaFreeHost(ctx->c.hostH);
+  for (auto& e : ctx->c.ev)
+    if (e) cudaEventDestroy(e);
+  delete ctx;
+}
+
+const char* aao_last_error(const aao_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "null context"; }
+size_t aao_vector_len(const aao_ctx* ctx) { return ctx ? (size_t)ctx->c.N : 0; }
+size_t aao_device_bytes(const aao_ctx* ctx) { return ctx ? ctx->c.bytes : 0; }
+long aao_last_launch_count(const aao_ctx* ctx) { return ctx ? ctx->launches_last : 0; }
+
+aao_status aao_pack(aao_ctx* ctx, const double* in, double* out, void* stream) {
+  if (!ctx || !in || !out) return AAO_ERR_SHAPE;
+  ABI_GUARD(ctx, { aao::launch_mask_copy(ctx->c, in, out, (cudaStream_t)stream); ++aao::launch_counter(); });
+  return AAO_OK;
+}
+
+aao_status aao_build_rhs(aao_ctx* ctx, const double* vd, double* b, void* stream) {
+  if (!ctx || !vd || !b) return AAO_ERR_SHAPE;
+  ABI_GUARD(ctx, { aao::launch_rhs(ctx->c, vd, b, (cudaStream_t)stream); ++aao::launch_counter(); });
+  return AAO_OK;
+}
+
+aao_status aao_kkt_apply(aao_ctx* ctx, const double* x, double* y, void* stream) {
+  if (!ctx || !x || !y || x == y) return AAO_ERR_SHAPE;
+  ABI_GUARD(ctx, { aao::kkt_apply(ctx->c, x, y, (cudaStream_t)stream); });
+  return AAO_OK;
+}
+
+aao_status aao_precond_apply(aao_ctx* ctx, const double* r, double* z, void* stream) {
+  if (!ctx || !r || !z || r == z) return AAO_ERR_SHAPE;
+  ABI_GUARD(ctx, { aao::precond_apply(ctx->c, r, z, (cudaStream_t)stream); });
+  return AAO_OK;
+}
+
+aao_status aao_gmres_solve(aao_ctx* ctx, const double* b, double* x, const aao_krylov* kry, aao_info* info,
+                           double* hist, int hist_cap, void* stream) {
+  if (!ctx || !b || !x || !kry || kry->restart < 1 || kry->restart > 64 || !(kry->tol > 0) || kry->max_iters < 1)
+    return AAO_ERR_SHAPE;
+  aao_status st = AAO_OK;
+  ABI_GUARD(ctx, { st = aao::gmres(ctx->c, b, x, *kry, info, hist, hist_cap, (cudaStream_t)stream); });
+  return st;
+}
+
+aao_status aao_gmres_solve_host(aao_ctx* ctx, const double* b_host, double* x_host, const aao_krylov* kry,
+                                aao_info* info, double* hist, int hist_cap, void* stream) {
+  if (!ctx || !b_host || !x_host || !kry) return AAO_ERR_SHAPE;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = ctx->c.N * sizeof(double);
+  double *db = nullptr, *dx = nullptr;
+  aao_status st = AAO_OK;
+  try {
+    if (!ctx->c.gr) aao::gmres_alloc(ctx->c, kry->restart);
+  } catch (const CudaError& e) {
+    return fail(ctx, e.st, e.what());
+  }
+  if (cudaMalloc(&db, bytes) != cudaSuccess || cudaMalloc(&dx, bytes) != cudaSuccess) {
+    if (db) cudaFree(db);
+    return fail(ctx, AAO_ERR_OOM, "aao_gmres_solve_host: cudaMalloc");
+  }
+  cudaMemcpyAsync(db, b_host, bytes, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(dx, x_host, bytes, cudaMemcpyHostToDevice, s);
+  st = aao_gmres_solve(ctx, db, dx, kry, info, hist, hist_cap, stream);
+  cudaMemcpyAsync(x_host, dx, bytes, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  cudaFree(db);
+  cudaFree(dx);
+  return st;
+}
+
+aao_status aao_debug_freq_block(aao_ctx* ctx, int k, double* out, void* stream) {
+  if (!ctx || !out || k < 0 || k >= ctx->c.n_f) return AAO_ERR_SHAPE;
+  ABI_GUARD(ctx, {
+    cudaStream_t s = (cudaStream_t)stream;
+    double2* tmp = nullptr;
+    if (cudaMalloc(&tmp, 2 * ctx->c.nblk * sizeof(double2)) != cudaSuccess)
+      throw CudaError(AAO_ERR_OOM, "debug block alloc");
+    aao::launch_debug_block(ctx->c, k, tmp, s);
+    cudaMemcpyAsync(out, tmp, 2 * ctx->c.nblk * sizeof(double2), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFree(tmp);
+  });
+  return AAO_OK;
+}
+
+aao_status aao_set_timing(aao_ctx* ctx, int on) {
+  if (!ctx) return AAO_ERR_SHAPE;
+  ctx->c.timing = on != 0;
+  return AAO_OK;
+}
+
+aao_status aao_last_phase_ms(aao_ctx* ctx, double* ms4) {
+  if (!ctx || !ms4) return AAO_ERR_SHAPE;
+  if (!ctx->c.timing) return fail(ctx, AAO_ERR_CONFIG, "timing not enabled");
+  cudaEventSynchronize(ctx->c.ev[4]);
+  float t[4];
+  cudaEventElapsedTime(&t[0], ctx->c.ev[0], ctx->c.ev[1]);
+  cudaEventElapsedTime(&t[1], ctx->c.ev[1], ctx->c.ev[2]);
+  cudaEventElapsedTime(&t[2], ctx->c.ev[2], ctx->c.ev[3]);
+  cudaEventElapsedTime(&t[3], ctx->c.ev[3], ctx->c.ev[4]);
+  for (int i = 0; i < 4; ++i) ms4[i] = t[i];
+  return AAO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,166 @@
+// Internal declarations of the B200 all-at-once library (not part of the C ABI).
+// Device descriptors are passed to kernels by value.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/aao.h"
+
+namespace aao {
+
+// One multigrid level of one scalar finite-element space on the full node grid.
+//   order 2: Q2 velocity component, 5-point 1-D rows, Dirichlet boundary nodes masked;
+//   order 1: Q1 pressure, 3-point 1-D rows, corner node 0 pinned.
+// Constant-coefficient operators are Kronecker sums of 1-D assembled rows:
+//   M = M_z (x) M_y (x) M_x,  K = sum_a (K_a (x) prod_{b!=a} M_b)     (x fastest)
+// tM/tK rows are indexed by the 1-D node index i, entry o is the coupling to
+// node i + o - order; entries to eliminated (boundary) columns are 0.
+struct Grid {
+  int dim;
+  int order;
+  int n1;
+  long n;
+  const double* tM;     // [n1][2*order+1]
+  const double* tK;     // [n1][2*order+1]
+  const double* conv;   // [n][(2*order+1)^dim] convection N (Oseen) or nullptr
+  const double* convT;  // its transpose N^T, same layout, or nullptr
+};
+
+// A = a*M + b*K + c*C, C = conv (sel 1) or convT (sel 2); coefficients per group.
+struct Coef { double2 a, b, c; };
+struct OpSel {
+  const Coef* coef;    // device, [n_groups]
+  int per_group;       // problems per coefficient group
+  int conv_sel;        // 0: none, 1: N, 2: N^T
+};
+
+// A batch of complex vectors of length n: problem p lives at
+//   p + (p / per_group) * gstride + (p % per_group) * n   (in double2 units)
+struct View {
+  double2* p;
+  int per_group;
+  long gstride;
+};
+
+// MG transfer tables between a fine level f and the coarse level c = f+1 (1-D).
+struct Transfer {
+  const double* tP;    // [n1_fine][4]: base coarse index, 3 weights (Q1: 2 used)
+  const double* tR;    // [n1_coarse][7]: weights on fine nodes 2I-3..2I+3 (Q1: 2I-1..2I+1 in [2..4])
+};
+
+// per-frequency constants for the time kernels (k < n_f)
+struct FreqConst {
+  double c1, c2;       // c_{k,1}, c_{k,2} (squared reading)
+  double dr, dc;       // Re d_k, Im d_k
+};
+
+struct MGLevel {       // device storage of one level of one space in a batch workspace
+  Grid g;
+  Transfer tr;         // to the next coarser level (unused on the coarsest)
+  double2* x;          // [nprob_max][n] (level 0: supplied by the caller)
+  double2* b;
+  double2* r;
+};
+
+struct MGSpace {       // an MG hierarchy for one space, with batch workspace
+  int order;
+  int nlev;
+  std::vector<Grid> grids;
+  std::vector<Transfer> transfers;
+  std::vector<double2*> x, b, r;     // per level (level 0 x/b external)
+  int ncoarse_unk;                   // unknowns on the coarsest grid
+  int* coarse_unk;                   // device, node indices
+  int nprob_max;
+};
+
+// The context: configuration, device operators, per-frequency data, workspace.
+struct Ctx {
+  aao_config cfg;
+  int dim = 2, Nc = 0, n_t = 0, n_b = 0, n_f = 0;
+  double tau = 0, beta = 0, nu = 0;
+  bool oseen = false;
+  int n1q2 = 0, n1q1 = 0;
+  long n_s = 0, n_p = 0, n_v = 0, nblk = 0, N = 0;
+  MGSpace vel, pres;             // MG hierarchies (Q2 velocity component, Q1 pressure)
+  double *tPm = nullptr, *tGm = nullptr;    // [n1q1][5] B rows: int psi_I phi_j, int psi_I phi_j'
+  double *tPmT = nullptr, *tGmT = nullptr;  // [n1q2][3] B^T rows, Q1 cols floor((i-1)/2)+o
+  double* tMfull = nullptr;                 // [n1q2][5] un-eliminated Q2 mass rows (RHS)
+  FreqConst* fc = nullptr;                  // device [n_f]
+  std::vector<FreqConst> fch;
+  double2* tw = nullptr;                    // [n_b] (cos, sin)(2 pi m / n_b)
+  // frequency-domain arrays: Fv [n_f][2][d][n_s], Fp [n_f][2][n_p]
+  double2 *Fv = nullptr, *Fp = nullptr, *Xv = nullptr, *XpA = nullptr, *XpB = nullptr;
+  // Oseen work arrays (velocity [n_f][d][n_s], pressure [n_f][2][n_p])
+  double2 *X1 = nullptr, *X2 = nullptr, *T1 = nullptr, *T2 = nullptr, *T3 = nullptr;
+  double2 *Qp = nullptr, *Sp = nullptr, *Tp = nullptr;
+  // Chebyshev work (r, d_old, d_new) sized for the largest batch
+  double2 *Cr = nullptr, *Cd0 = nullptr, *Cd1 = nullptr;
+  // operator coefficient tables (device)
+  Coef *coefW = nullptr, *coefKp = nullptr, *coefMass = nullptr;
+  Coef *coefQ = nullptr, *coefQH = nullptr;        // MG operators Q_k, Q_k^H (per k)
+  Coef *coefU1 = nullptr, *coefU2 = nullptr, *coefU3 = nullptr, *coefU4 = nullptr;  // Uzawa combos
+  Coef *coefS1 = nullptr, *coefS2 = nullptr, *coefS3 = nullptr, *coefS4 = nullptr;  // Schur combos
+  // coarse-grid inverses
+  double2 *invW = nullptr, *invKp = nullptr, *invQ = nullptr, *invQH = nullptr;
+  // GMRES workspace (allocated on first solve)
+  int gm_m = 0;
+  double *gV = nullptr, *gz = nullptr, *gw = nullptr, *gu = nullptr, *gr = nullptr;
+  double *gH = nullptr, *gpart = nullptr, *gscal = nullptr;
+  double **gVptr = nullptr;
+  double* hostH = nullptr;   // pinned
+  // bookkeeping
+  std::vector<void*> allocs;
+  size_t bytes = 0;
+  std::string err;
+  long launches = 0;
+  bool timing = false;
+  cudaEvent_t ev[5] = {};
+  double phase_ms[4] = {0, 0, 0, 0};
+};
+
+// ---- kernel launchers (kernels_*.cu) --------------------------------------
+void launch_gs(const Grid& g, const OpSel& op, View x, View b, int nprob, int colour, double omega,
+               cudaStream_t s);
+void launch_residual(const Grid& g, const OpSel& op, View x, View b, View r, int nprob, cudaStream_t s);
+void launch_restrict(const Grid& gf, const Grid& gc, const Transfer& t, View rf, View bc, int nprob,
+                     cudaStream_t s);
+void launch_prolong(const Grid& gf, const Grid& gc, const Transfer& t, View xc, View xf, int nprob,
+                    cudaStream_t s);
+void launch_coarse(const Grid& gc, const double2* inv, int inv_per_group, const int* unk, int nu,
+                   View b, View x, int nprob, cudaStream_t s);
+void launch_zero(View x, long n, int nprob, cudaStream_t s);
+void launch_cheb_init(const Grid& g, View b, View x, View r, View d, double inv_theta, int nprob,
+                      cudaStream_t s);
+void launch_cheb_step(const Grid& g, View x, View r, View dold, View dnew, double c1, double c2,
+                      int nprob, cudaStream_t s);
+void launch_cheb_final(const Grid& g, View x, View d, double scale, int nprob, cudaStream_t s);
+// out = cb*b + A1 x1 + A2 x2  (A2 optional: x2.p == nullptr)
+void launch_lincomb(const Grid& g, View out, double cb, View b, const OpSel& A1, View x1,
+                    const OpSel& A2, View x2, int nprob, cudaStream_t s);
+// y = a*y + bcoef*x  (pointwise, masked entries stay 0)
+void launch_axpby(const Grid& g, View y, double2 a, View x, double2 bcoef, int nprob, cudaStream_t s);
+// pressure: out = sb*bp + sB * sum_c B_c v_c (v: d components per problem group)
+void launch_Bv(const Grid& g2, const Grid& g1, const double* tPm, const double* tGm, View v, View bp,
+               View out, double sb, double sB, int nprob, cudaStream_t s);
+
+// time transforms and KKT (kernels_time.cu)
+void launch_fft_fwd(const Ctx& c, const double* r, cudaStream_t s);
+void launch_fft_inv(const Ctx& c, double* z, cudaStream_t s);
+void launch_kkt(const Ctx& c, const double* x, double* y, cudaStream_t s);
+void launch_mask_copy(const Ctx& c, const double* in, double* out, cudaStream_t s);
+void launch_rhs(const Ctx& c, const double* vd, double* b, cudaStream_t s);
+void launch_debug_block(const Ctx& c, int k, double2* out, cudaStream_t s);
+
+// blas (kernels_blas.cu): deterministic two-stage reductions
+void launch_dot(const double* x, const double* y, long n, double* partial, int nblk, double* out,
+                int mode, cudaStream_t s);   // mode 0: out = dot; 1: out = sqrt(dot)
+void launch_axpy_dev(double* y, const double* x, const double* alpha, double sign, long n, cudaStream_t s);
+void launch_scale_dev(double* y, const double* x, const double* denom, long n, cudaStream_t s);
+void launch_axpy(double* y, const double* x, double alpha, long n, cudaStream_t s);
+void launch_copy_sub(double* y, const double* b, const double* ax, long n, cudaStream_t s);  // y = b - ax
+void launch_multi_axpy(double* u, const double* const* V, const double* coef, int k, long n, cudaStream_t s);
+int dot_blocks();
+
+}  // namespace aao

@@ -1,0 +1,105 @@
+// GMRES vector kernels (step A1): deterministic two-stage reductions with warp
+// shuffles (fixed grid, fixed order -> bitwise reproducible), device-scalar axpys
+// so Gram-Schmidt coefficients never round-trip through the host.
+#include "aao_internal.h"
+
+namespace aao {
+
+constexpr int DOT_BLOCKS = 4 * 148;
+constexpr int DOT_THREADS = 256;
+int dot_blocks() { return DOT_BLOCKS; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double ws[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum(v);
+  if (lane == 0) ws[wid] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  v = threadIdx.x < nw ? ws[threadIdx.x] : 0.0;
+  if (wid == 0) v = warp_sum(v);
+  return v;  // valid in thread 0
+}
+
+__global__ void k_dot_partial(const double* __restrict__ x, const double* __restrict__ y, long n,
+                              double* __restrict__ partial) {
+  double acc = 0.0;
+  const long stride = (long)gridDim.x * blockDim.x;
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  // 2-way unrolled grid-stride loop with vectorised loads when aligned
+  for (; i < n; i += stride) acc = fma(__ldg(x + i), __ldg(y + i), acc);
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+}
+
+__global__ void k_dot_final(const double* __restrict__ partial, int nb, double* out, int mode) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) acc += partial[i];
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) *out = mode == 1 ? sqrt(acc) : acc;
+}
+
+void launch_dot(const double* x, const double* y, long n, double* partial, int nblk, double* out, int mode,
+                cudaStream_t s) {
+  k_dot_partial<<<nblk, DOT_THREADS, 0, s>>>(x, y, n, partial);
+  k_dot_final<<<1, 1024, 0, s>>>(partial, nblk, out, mode);
+}
+
+__global__ void k_axpy_dev(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ alpha,
+                           double sign, long n) {
+  const double a = sign * *alpha;
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) y[i] = fma(a, x[i], y[i]);
+}
+void launch_axpy_dev(double* y, const double* x, const double* alpha, double sign, long n, cudaStream_t s) {
+  k_axpy_dev<<<DOT_BLOCKS, 256, 0, s>>>(y, x, alpha, sign, n);
+}
+
+__global__ void k_scale_dev(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ den,
+                            long n) {
+  const double a = 1.0 / *den;
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) y[i] = x[i] * a;
+}
+void launch_scale_dev(double* y, const double* x, const double* denom, long n, cudaStream_t s) {
+  k_scale_dev<<<DOT_BLOCKS, 256, 0, s>>>(y, x, denom, n);
+}
+
+__global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double a, long n) {
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) y[i] = fma(a, x[i], y[i]);
+}
+void launch_axpy(double* y, const double* x, double alpha, long n, cudaStream_t s) {
+  k_axpy<<<DOT_BLOCKS, 256, 0, s>>>(y, x, alpha, n);
+}
+
+__global__ void k_copy_sub(double* __restrict__ y, const double* __restrict__ b, const double* __restrict__ ax,
+                           long n) {
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) y[i] = b[i] - ax[i];
+}
+void launch_copy_sub(double* y, const double* b, const double* ax, long n, cudaStream_t s) {
+  k_copy_sub<<<DOT_BLOCKS, 256, 0, s>>>(y, b, ax, n);
+}
+
+// u = sum_{i<k} coef[i] * V_i, V_i = V[i]
+__global__ void k_multi_axpy(double* __restrict__ u, const double* const* __restrict__ V,
+                             const double* __restrict__ coef, int k, long n) {
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long j = (long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+    double acc = 0.0;
+    for (int i = 0; i < k; ++i) acc = fma(coef[i], V[i][j], acc);
+    u[j] = acc;
+  }
+}
+void launch_multi_axpy(double* u, const double* const* V, const double* coef, int k, long n, cudaStream_t s) {
+  k_multi_axpy<<<DOT_BLOCKS, 256, 0, s>>>(u, V, coef, k, n);
+}
+
+}  // namespace aao

@@ -1,0 +1,602 @@
+// Batched-over-frequency stencil kernels for the per-frequency block solves
+// (SURVEY 8(a) A4-A7): operator application, multicolour SOR, residual,
+// restriction / prolongation, coarsest-level dense solve, Chebyshev steps,
+// fused linear combinations.  sm_100a, fp64 / complex128.
+//
+// Every constant-coefficient operator is evaluated from 1-D assembled rows
+// (Kronecker structure of Q2/Q1 on a uniform box mesh), so no matrix is
+// stored except the convection N of the Oseen problem (per-node stencil).
+// All problems of a batch share the real stencil; per-frequency complex scalars
+// (alpha M + beta K + gamma N) come from a small coefficient table.
+#include "aao_internal.h"
+
+namespace aao {
+
+// ---------------------------------------------------------------- complex helpers
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+__device__ __forceinline__ double2 cfma(double s, double2 a, double2 acc) {
+  return make_double2(fma(s, a.x, acc.x), fma(s, a.y, acc.y));
+}
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  double den = b.x * b.x + b.y * b.y;
+  return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
+}
+
+__device__ __forceinline__ long voff(const View& v, int p, long n) {
+  return (long)(p / v.per_group) * v.gstride + (long)(p % v.per_group) * n;
+}
+
+template <int DIM>
+__device__ __forceinline__ void coords(long idx, int n1, int* c) {
+  c[0] = (int)(idx % n1);
+  c[1] = (int)((idx / n1) % n1);
+  if (DIM == 3) c[2] = (int)(idx / ((long)n1 * n1));
+}
+
+template <int DIM, int ORD>
+__device__ __forceinline__ bool masked(const int* c, long idx, int n1) {
+  if (ORD == 1) return idx == 0;  // pinned pressure node
+  bool m = false;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) m |= (c[a] == 0) | (c[a] == n1 - 1);  // Dirichlet velocity
+  return m;
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// Mx = (M x)_i, Kx = (K x)_i, Cx = (C x)_i at one node; dM, dK, dC = diagonal entries.
+template <int DIM, int ORD, bool CONV>
+__device__ __forceinline__ void apply_MKC(const Grid& g, const double* __restrict__ cv,
+                                          const double2* __restrict__ x, const int* c, long idx,
+                                          double2& Mx, double2& Kx, double2& Cx, double& dM, double& dK,
+                                          double& dC) {
+  constexpr int W = 2 * ORD + 1;
+  double m[DIM][W], k[DIM][W];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int o = 0; o < W; ++o) {
+      m[a][o] = __ldg(g.tM + c[a] * W + o);
+      k[a][o] = __ldg(g.tK + c[a] * W + o);
+    }
+  const int n1 = g.n1;
+  Mx = Kx = Cx = make_double2(0.0, 0.0);
+  const double* cvr = CONV ? cv + idx * (DIM == 2 ? W * W : W * W * W) : nullptr;
+  if constexpr (DIM == 2) {
+#pragma unroll
+    for (int ob = 0; ob < W; ++ob) {
+      const int jj = clampi(c[1] + ob - ORD, 0, n1 - 1);
+#pragma unroll
+      for (int oa = 0; oa < W; ++oa) {
+        const int ii = clampi(c[0] + oa - ORD, 0, n1 - 1);
+        const double2 v = __ldg(x + (long)jj * n1 + ii);
+        const double mm = m[1][ob] * m[0][oa];
+        const double kk = k[1][ob] * m[0][oa] + m[1][ob] * k[0][oa];
+        Mx = cfma(mm, v, Mx);
+        Kx = cfma(kk, v, Kx);
+        if (CONV) Cx = cfma(__ldg(cvr + ob * W + oa), v, Cx);
+      }
+    }
+    dM = m[1][ORD] * m[0][ORD];
+    dK = k[1][ORD] * m[0][ORD] + m[1][ORD] * k[0][ORD];
+    dC = CONV ? __ldg(cvr + ORD * W + ORD) : 0.0;
+  } else {
+#pragma unroll 1
+    for (int oc = 0; oc < W; ++oc) {
+      const int kk3 = clampi(c[2] + oc - ORD, 0, n1 - 1);
+#pragma unroll
+      for (int ob = 0; ob < W; ++ob) {
+        const int jj = clampi(c[1] + ob - ORD, 0, n1 - 1);
+        const double mzy = m[2][oc] * m[1][ob];
+        const double kzy = k[2][oc] * m[1][ob] + m[2][oc] * k[1][ob];
+#pragma unroll
+        for (int oa = 0; oa < W; ++oa) {
+          const int ii = clampi(c[0] + oa - ORD, 0, n1 - 1);
+          const double2 v = __ldg(x + ((long)kk3 * n1 + jj) * n1 + ii);
+          const double mm = mzy * m[0][oa];
+          const double kk = kzy * m[0][oa] + mzy * k[0][oa];
+          Mx = cfma(mm, v, Mx);
+          Kx = cfma(kk, v, Kx);
+          if (CONV) Cx = cfma(__ldg(cvr + (oc * W + ob) * W + oa), v, Cx);
+        }
+      }
+    }
+    dM = m[2][ORD] * m[1][ORD] * m[0][ORD];
+    dK = k[2][ORD] * m[1][ORD] * m[0][ORD] + m[2][ORD] * k[1][ORD] * m[0][ORD] +
+         m[2][ORD] * m[1][ORD] * k[0][ORD];
+    dC = CONV ? __ldg(cvr + (ORD * W + ORD) * W + ORD) : 0.0;
+  }
+}
+
+// (A x)_i and A_ii for A = a M + b K + c C
+template <int DIM, int ORD>
+__device__ __forceinline__ void apply_op(const Grid& g, const OpSel& op, int p, const double2* __restrict__ x,
+                                         const int* c, long idx, double2& Ax, double2& D) {
+  const Coef cf = op.coef[p / op.per_group];
+  double2 Mx, Kx, Cx;
+  double dM, dK, dC;
+  if (op.conv_sel == 0) {
+    apply_MKC<DIM, ORD, false>(g, nullptr, x, c, idx, Mx, Kx, Cx, dM, dK, dC);
+  } else {
+    apply_MKC<DIM, ORD, true>(g, op.conv_sel == 1 ? g.conv : g.convT, x, c, idx, Mx, Kx, Cx, dM, dK, dC);
+  }
+  Ax = cadd(cadd(cmul(cf.a, Mx), cmul(cf.b, Kx)), cmul(cf.c, Cx));
+  D = cadd(cadd(cscale(dM, cf.a), cscale(dK, cf.b)), cscale(dC, cf.c));
+}
+
+// ---------------------------------------------------------------- multicolour SOR
+// x_i <- x_i + omega (b_i - (A x)_i) / A_ii for the nodes of one colour (DESIGN.md reading:
+// colour = sum_a (c_a mod C1) C1^a, C1 = 3 for Q2, 2 for Q1; no same-colour couplings).
+template <int DIM, int ORD>
+__global__ void k_gs(Grid g, OpSel op, View xv, View bv, int colour, double omega) {
+  constexpr int C1 = ORD == 2 ? 3 : 2;
+  const int p = blockIdx.y;
+  int res[DIM], cnt[DIM];
+  int cc = colour;
+  long total = 1;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    res[a] = cc % C1;
+    cc /= C1;
+    cnt[a] = (g.n1 - res[a] + C1 - 1) / C1;
+    total *= cnt[a];
+  }
+  long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  int c[DIM];
+  long idx = 0, stride = 1;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    c[a] = res[a] + C1 * (int)(t % cnt[a]);
+    t /= cnt[a];
+    idx += c[a] * stride;
+    stride *= g.n1;
+  }
+  if (masked<DIM, ORD>(c, idx, g.n1)) return;
+  double2* x = xv.p + voff(xv, p, g.n);
+  const double2* b = bv.p + voff(bv, p, g.n);
+  double2 Ax, D;
+  apply_op<DIM, ORD>(g, op, p, x, c, idx, Ax, D);
+  const double2 upd = cdiv(csub(b[idx], Ax), D);
+  x[idx] = cadd(x[idx], cscale(omega, upd));
+}
+
+// r = b - A x  (masked entries -> 0)
+template <int DIM, int ORD>
+__global__ void k_residual(Grid g, OpSel op, View xv, View bv, View rv) {
+  const int p = blockIdx.y;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.n) return;
+  int c[DIM];
+  coords<DIM>(idx, g.n1, c);
+  double2* r = rv.p + voff(rv, p, g.n);
+  if (masked<DIM, ORD>(c, idx, g.n1)) {
+    r[idx] = make_double2(0.0, 0.0);
+    return;
+  }
+  const double2* x = xv.p + voff(xv, p, g.n);
+  const double2* b = bv.p + voff(bv, p, g.n);
+  double2 Ax, D;
+  apply_op<DIM, ORD>(g, op, p, x, c, idx, Ax, D);
+  r[idx] = csub(b[idx], Ax);
+}
+
+// ---------------------------------------------------------------- transfers
+// restriction b_c = P^T r_f: coarse node I gathers fine nodes 2I-R..2I+R per axis (R = 3 Q2, 1 Q1)
+template <int DIM, int ORD>
+__global__ void k_restrict(Grid gf, Grid gc, Transfer t, View rv, View bv) {
+  constexpr int R = ORD == 2 ? 3 : 1;
+  constexpr int WR = 2 * R + 1;
+  const int p = blockIdx.y;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= gc.n) return;
+  int c[DIM];
+  coords<DIM>(idx, gc.n1, c);
+  double2* b = bv.p + voff(bv, p, gc.n);
+  if (masked<DIM, ORD>(c, idx, gc.n1)) {
+    b[idx] = make_double2(0.0, 0.0);
+    return;
+  }
+  const double2* r = rv.p + voff(rv, p, gf.n);
+  const int o7 = ORD == 2 ? 0 : 2;  // Q1 rows use entries [2..4] of the 7-wide table
+  double w[DIM][WR];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int o = 0; o < WR; ++o) w[a][o] = __ldg(t.tR + c[a] * 7 + o7 + o);
+  double2 acc = make_double2(0.0, 0.0);
+  const int n1 = gf.n1;
+  if constexpr (DIM == 2) {
+#pragma unroll
+    for (int ob = 0; ob < WR; ++ob) {
+      if (w[1][ob] == 0.0) continue;
+      const int jj = 2 * c[1] + ob - R;
+#pragma unroll
+      for (int oa = 0; oa < WR; ++oa) {
+        if (w[0][oa] == 0.0) continue;
+        const int ii = 2 * c[0] + oa - R;
+        acc = cfma(w[1][ob] * w[0][oa], r[(long)jj * n1 + ii], acc);
+      }
+    }
+  } else {
+    for (int oc = 0; oc < WR; ++oc) {
+      if (w[2][oc] == 0.0) continue;
+      const int kk = 2 * c[2] + oc - R;
+      for (int ob = 0; ob < WR; ++ob) {
+        if (w[1][ob] == 0.0) continue;
+        const int jj = 2 * c[1] + ob - R;
+#pragma unroll
+        for (int oa = 0; oa < WR; ++oa) {
+          if (w[0][oa] == 0.0) continue;
+          const int ii = 2 * c[0] + oa - R;
+          acc = cfma(w[2][oc] * w[1][ob] * w[0][oa], r[((long)kk * n1 + jj) * n1 + ii], acc);
+        }
+      }
+    }
+  }
+  b[idx] = acc;
+}
+
+// prolongation + correction x_f += P x_c (nodal interpolation; masked fine nodes untouched)
+template <int DIM, int ORD>
+__global__ void k_prolong(Grid gf, Grid gc, Transfer t, View xcv, View xfv) {
+  constexpr int NW = ORD == 2 ? 3 : 2;
+  const int p = blockIdx.y;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= gf.n) return;
+  int c[DIM];
+  coords<DIM>(idx, gf.n1, c);
+  if (masked<DIM, ORD>(c, idx, gf.n1)) return;
+  const double2* xc = xcv.p + voff(xcv, p, gc.n);
+  double2* xf = xfv.p + voff(xfv, p, gf.n);
+  int base[DIM];
+  double w[DIM][NW];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    base[a] = (int)__ldg(t.tP + c[a] * 4);
+#pragma unroll
+    for (int o = 0; o < NW; ++o) w[a][o] = __ldg(t.tP + c[a] * 4 + 1 + o);
+  }
+  const int n1 = gc.n1;
+  double2 acc = make_double2(0.0, 0.0);
+  if constexpr (DIM == 2) {
+#pragma unroll
+    for (int ob = 0; ob < NW; ++ob) {
+      if (w[1][ob] == 0.0) continue;
+#pragma unroll
+      for (int oa = 0; oa < NW; ++oa) {
+        if (w[0][oa] == 0.0) continue;
+        acc = cfma(w[1][ob] * w[0][oa], xc[(long)(base[1] + ob) * n1 + base[0] + oa], acc);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int oc = 0; oc < NW; ++oc) {
+      if (w[2][oc] == 0.0) continue;
+#pragma unroll
+      for (int ob = 0; ob < NW; ++ob) {
+        if (w[1][ob] == 0.0) continue;
+#pragma unroll
+        for (int oa = 0; oa < NW; ++oa) {
+          if (w[0][oa] == 0.0) continue;
+          acc = cfma(w[2][oc] * w[1][ob] * w[0][oa],
+                     xc[((long)(base[2] + oc) * n1 + base[1] + ob) * n1 + base[0] + oa], acc);
+        }
+      }
+    }
+  }
+  xf[idx] = cadd(xf[idx], acc);
+}
+
+// coarsest level: x[unk] = inv_g * b[unk] (dense inverse per coefficient group)
+__global__ void k_coarse(long nc, const double2* __restrict__ inv, int inv_per_group, const int* __restrict__ unk,
+                         int nu, View bv, View xv) {
+  const int p = blockIdx.x;
+  const double2* b = bv.p + voff(bv, p, nc);
+  double2* x = xv.p + voff(xv, p, nc);
+  const double2* A = inv + (long)(p / inv_per_group) * nu * nu;
+  extern __shared__ double2 sb[];
+  for (int i = threadIdx.x; i < nu; i += blockDim.x) sb[i] = b[unk[i]];
+  __syncthreads();
+  for (int i = threadIdx.x; i < nu; i += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int j = 0; j < nu; ++j) acc = cadd(acc, cmul(A[(long)i * nu + j], sb[j]));
+    x[unk[i]] = acc;
+  }
+}
+
+__global__ void k_zero(View xv, long n) {
+  const int p = blockIdx.y;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  xv.p[voff(xv, p, n) + idx] = make_double2(0.0, 0.0);
+}
+
+// ---------------------------------------------------------------- Chebyshev on a mass matrix
+// x0 = 0, r0 = f, d0 = D^-1 r0 / theta; per step x += d; r -= M d; d' = c1 d + c2 D^-1 r.
+template <int DIM, int ORD>
+__device__ __forceinline__ double mass_diag(const Grid& g, const int* c) {
+  constexpr int W = 2 * ORD + 1;
+  double d = 1.0;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) d *= __ldg(g.tM + c[a] * W + ORD);
+  return d;
+}
+
+template <int DIM, int ORD>
+__global__ void k_cheb_init(Grid g, View bv, View xv, View rv, View dv, double inv_theta) {
+  const int p = blockIdx.y;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.n) return;
+  int c[DIM];
+  coords<DIM>(idx, g.n1, c);
+  const long o = voff(bv, p, g.n) + idx;
+  double2 bb = bv.p[o];
+  double2 z = make_double2(0.0, 0.0);
+  double2 dd = z;
+  if (masked<DIM, ORD>(c, idx, g.n1)) {
+    bb = z;
+  } else {
+    dd = cscale(1.0 / mass_diag<DIM, ORD>(g, c), bb);
+    dd = cscale(inv_theta, dd);
+  }
+  xv.p[voff(xv, p, g.n) + idx] = z;
+  rv.p[voff(rv, p, g.n) + idx] = bb;
+  dv.p[voff(dv, p, g.n) + idx] = dd;
+}
+
+template <int DIM, int ORD>
+__global__ void k_cheb_step(Grid g, View xv, View rv, View dov, View dnv, double c1, double c2) {
+  const int p = blockIdx.y;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.n) return;
+  int c[DIM];
+  coords<DIM>(idx, g.n1, c);
+  const long oo = voff(dnv, p, g.n) + idx;
+  if (masked<DIM, ORD>(c, idx, g.n1)) {
+    dnv.p[oo] = make_double2(0.0, 0.0);
+    return;
+  }
+  const double2* dold = dov.p + voff(dov, p, g.n);
+  double2 Mx, Kx, Cx;
+  double dM, dK, dC;
+  apply_MKC<DIM, ORD, false>(g, nullptr, dold, c, idx, Mx, Kx, Cx, dM, dK, dC);
+  const long ox = voff(xv, p, g.n) + idx, orr = voff(rv, p, g.n) + idx;
+  const double2 d = dold[idx];
+  xv.p[ox] = cadd(xv.p[ox], d);
+  const double2 r = csub(rv.p[orr], Mx);
+  rv.p[orr] = r;
+  dnv.p[oo] = cadd(cscale(c1, d), cscale(c2, cscale(1.0 / dM, r)));
+}
+
+template <int DIM, int ORD>
+__global__ void k_cheb_final(Grid g, View xv, View dv, double scale) {
+  const int p = blockIdx.y;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.n) return;
+  const long ox = voff(xv, p, g.n) + idx;
+  xv.p[ox] = cscale(scale, cadd(xv.p[ox], dv.p[voff(dv, p, g.n) + idx]));
+}
+
+// ---------------------------------------------------------------- fused linear combinations
+template <int DIM, int ORD>
+__global__ void k_lincomb(Grid g, View ov, double cb, View bv, OpSel A1, View x1, OpSel A2, View x2, int two) {
+  const int p = blockIdx.y;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.n) return;
+  int c[DIM];
+  coords<DIM>(idx, g.n1, c);
+  double2* out = ov.p + voff(ov, p, g.n);
+  if (masked<DIM, ORD>(c, idx, g.n1)) {
+    out[idx] = make_double2(0.0, 0.0);
+    return;
+  }
+  double2 acc = make_double2(0.0, 0.0);
+  if (cb != 0.0) acc = cscale(cb, bv.p[voff(bv, p, g.n) + idx]);
+  double2 Ax, D;
+  apply_op<DIM, ORD>(g, A1, p, x1.p + voff(x1, p, g.n), c, idx, Ax, D);
+  acc = cadd(acc, Ax);
+  if (two) {
+    apply_op<DIM, ORD>(g, A2, p, x2.p + voff(x2, p, g.n), c, idx, Ax, D);
+    acc = cadd(acc, Ax);
+  }
+  out[idx] = acc;
+}
+
+template <int DIM, int ORD>
+__global__ void k_axpby(Grid g, View yv, double2 a, View xv, double2 bc) {
+  const int p = blockIdx.y;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.n) return;
+  const long oy = voff(yv, p, g.n) + idx;
+  yv.p[oy] = cadd(cmul(a, yv.p[oy]), cmul(bc, xv.p[voff(xv, p, g.n) + idx]));
+}
+
+// pressure out_q = sb * bp_q + sB * sum_c (B_c v_c)_q, B = -[int psi d_c phi]
+// tPm/tGm: [n1q1][5] 1-D rows int psi_I phi_j, int psi_I phi_j' for j = 2I-2..2I+2 (Dirichlet cols 0)
+// v view: problem p (pressure problem) -> velocity components at p*DIMgroups (see launcher)
+template <int DIM>
+__global__ void k_Bv(Grid g2, Grid g1, const double* __restrict__ tPm, const double* __restrict__ tGm, View vv,
+                     View bpv, View ov, double sb, double sB) {
+  const int p = blockIdx.y;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g1.n) return;
+  int c[DIM];
+  coords<DIM>(idx, g1.n1, c);
+  double2* out = ov.p + voff(ov, p, g1.n);
+  if (idx == 0) {
+    out[0] = make_double2(0.0, 0.0);
+    return;
+  }
+  double Pm[DIM][5], Gm[DIM][5];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int o = 0; o < 5; ++o) {
+      Pm[a][o] = __ldg(tPm + c[a] * 5 + o);
+      Gm[a][o] = __ldg(tGm + c[a] * 5 + o);
+    }
+  double2 acc = make_double2(0.0, 0.0);
+  const int n1 = g2.n1;
+  for (int comp = 0; comp < DIM; ++comp) {
+    const double2* v = vv.p + voff(vv, p * DIM + comp, g2.n);
+    if constexpr (DIM == 2) {
+#pragma unroll
+      for (int ob = 0; ob < 5; ++ob) {
+        const int jj = clampi(2 * c[1] + ob - 2, 0, n1 - 1);
+        const double fy = comp == 1 ? Gm[1][ob] : Pm[1][ob];
+#pragma unroll
+        for (int oa = 0; oa < 5; ++oa) {
+          const int ii = clampi(2 * c[0] + oa - 2, 0, n1 - 1);
+          const double fx = comp == 0 ? Gm[0][oa] : Pm[0][oa];
+          acc = cfma(-fy * fx, v[(long)jj * n1 + ii], acc);
+        }
+      }
+    } else {
+      for (int oc = 0; oc < 5; ++oc) {
+        const int kk = clampi(2 * c[2] + oc - 2, 0, n1 - 1);
+        const double fz = comp == 2 ? Gm[2][oc] : Pm[2][oc];
+#pragma unroll
+        for (int ob = 0; ob < 5; ++ob) {
+          const int jj = clampi(2 * c[1] + ob - 2, 0, n1 - 1);
+          const double fy = comp == 1 ? Gm[1][ob] : Pm[1][ob];
+#pragma unroll
+          for (int oa = 0; oa < 5; ++oa) {
+            const int ii = clampi(2 * c[0] + oa - 2, 0, n1 - 1);
+            const double fx = comp == 0 ? Gm[0][oa] : Pm[0][oa];
+            acc = cfma(-fz * fy * fx, v[((long)kk * n1 + jj) * n1 + ii], acc);
+          }
+        }
+      }
+    }
+  }
+  double2 res = cscale(sB, acc);
+  if (sb != 0.0) res = cadd(res, cscale(sb, bpv.p[voff(bpv, p, g1.n) + idx]));
+  out[idx] = res;
+}
+
+// ---------------------------------------------------------------- launchers
+static inline dim3 grid1(long n, int nprob, int bs) { return dim3((unsigned)((n + bs - 1) / bs), nprob); }
+constexpr int BS = 128;
+
+template <int DIM, int ORD>
+static void gs_t(const Grid& g, const OpSel& op, View x, View b, int nprob, int colour, double omega,
+                 cudaStream_t s) {
+  constexpr int C1 = ORD == 2 ? 3 : 2;
+  long total = 1;
+  int cc = colour;
+  for (int a = 0; a < DIM; ++a) {
+    int r = cc % C1;
+    cc /= C1;
+    total *= (g.n1 - r + C1 - 1) / C1;
+  }
+  k_gs<DIM, ORD><<<grid1(total, nprob, BS), BS, 0, s>>>(g, op, x, b, colour, omega);
+}
+
+#define SWITCH_DO(g, FN, ...)                         \
+  switch ((g).dim * 10 + (g).order) {                 \
+    case 22: FN<2, 2>(__VA_ARGS__); break;            \
+    case 21: FN<2, 1>(__VA_ARGS__); break;            \
+    case 32: FN<3, 2>(__VA_ARGS__); break;            \
+    case 31: FN<3, 1>(__VA_ARGS__); break;            \
+  }
+
+void launch_gs(const Grid& g, const OpSel& op, View x, View b, int nprob, int colour, double omega,
+               cudaStream_t s) {
+  SWITCH_DO(g, gs_t, g, op, x, b, nprob, colour, omega, s);
+}
+
+template <int DIM, int ORD>
+static void res_t(const Grid& g, const OpSel& op, View x, View b, View r, int nprob, cudaStream_t s) {
+  k_residual<DIM, ORD><<<grid1(g.n, nprob, BS), BS, 0, s>>>(g, op, x, b, r);
+}
+void launch_residual(const Grid& g, const OpSel& op, View x, View b, View r, int nprob, cudaStream_t s) {
+  SWITCH_DO(g, res_t, g, op, x, b, r, nprob, s);
+}
+
+template <int DIM, int ORD>
+static void restr_t(const Grid& gf, const Grid& gc, const Transfer& t, View rf, View bc, int nprob,
+                    cudaStream_t s) {
+  k_restrict<DIM, ORD><<<grid1(gc.n, nprob, BS), BS, 0, s>>>(gf, gc, t, rf, bc);
+}
+void launch_restrict(const Grid& gf, const Grid& gc, const Transfer& t, View rf, View bc, int nprob,
+                     cudaStream_t s) {
+  SWITCH_DO(gf, restr_t, gf, gc, t, rf, bc, nprob, s);
+}
+
+template <int DIM, int ORD>
+static void prol_t(const Grid& gf, const Grid& gc, const Transfer& t, View xc, View xf, int nprob,
+                   cudaStream_t s) {
+  k_prolong<DIM, ORD><<<grid1(gf.n, nprob, BS), BS, 0, s>>>(gf, gc, t, xc, xf);
+}
+void launch_prolong(const Grid& gf, const Grid& gc, const Transfer& t, View xc, View xf, int nprob,
+                    cudaStream_t s) {
+  SWITCH_DO(gf, prol_t, gf, gc, t, xc, xf, nprob, s);
+}
+
+void launch_coarse(const Grid& gc, const double2* inv, int inv_per_group, const int* unk, int nu, View b,
+                   View x, int nprob, cudaStream_t s) {
+  k_coarse<<<nprob, 32, nu * sizeof(double2), s>>>(gc.n, inv, inv_per_group, unk, nu, b, x);
+}
+
+void launch_zero(View x, long n, int nprob, cudaStream_t s) {
+  k_zero<<<grid1(n, nprob, 256), 256, 0, s>>>(x, n);
+}
+
+template <int DIM, int ORD>
+static void chi_t(const Grid& g, View b, View x, View r, View d, double it, int nprob, cudaStream_t s) {
+  k_cheb_init<DIM, ORD><<<grid1(g.n, nprob, BS), BS, 0, s>>>(g, b, x, r, d, it);
+}
+void launch_cheb_init(const Grid& g, View b, View x, View r, View d, double inv_theta, int nprob,
+                      cudaStream_t s) {
+  SWITCH_DO(g, chi_t, g, b, x, r, d, inv_theta, nprob, s);
+}
+template <int DIM, int ORD>
+static void chs_t(const Grid& g, View x, View r, View dold, View dnew, double c1, double c2, int nprob,
+                  cudaStream_t s) {
+  k_cheb_step<DIM, ORD><<<grid1(g.n, nprob, BS), BS, 0, s>>>(g, x, r, dold, dnew, c1, c2);
+}
+void launch_cheb_step(const Grid& g, View x, View r, View dold, View dnew, double c1, double c2, int nprob,
+                      cudaStream_t s) {
+  SWITCH_DO(g, chs_t, g, x, r, dold, dnew, c1, c2, nprob, s);
+}
+template <int DIM, int ORD>
+static void chf_t(const Grid& g, View x, View d, double scale, int nprob, cudaStream_t s) {
+  k_cheb_final<DIM, ORD><<<grid1(g.n, nprob, 256), 256, 0, s>>>(g, x, d, scale);
+}
+void launch_cheb_final(const Grid& g, View x, View d, double scale, int nprob, cudaStream_t s) {
+  SWITCH_DO(g, chf_t, g, x, d, scale, nprob, s);
+}
+
+template <int DIM, int ORD>
+static void lc_t(const Grid& g, View out, double cb, View b, const OpSel& A1, View x1, const OpSel& A2, View x2,
+                 int nprob, cudaStream_t s) {
+  k_lincomb<DIM, ORD><<<grid1(g.n, nprob, BS), BS, 0, s>>>(g, out, cb, b, A1, x1, A2, x2, x2.p != nullptr);
+}
+void launch_lincomb(const Grid& g, View out, double cb, View b, const OpSel& A1, View x1, const OpSel& A2,
+                    View x2, int nprob, cudaStream_t s) {
+  SWITCH_DO(g, lc_t, g, out, cb, b, A1, x1, A2, x2, nprob, s);
+}
+
+template <int DIM, int ORD>
+static void ax_t(const Grid& g, View y, double2 a, View x, double2 bc, int nprob, cudaStream_t s) {
+  k_axpby<DIM, ORD><<<grid1(g.n, nprob, 256), 256, 0, s>>>(g, y, a, x, bc);
+}
+void launch_axpby(const Grid& g, View y, double2 a, View x, double2 bcoef, int nprob, cudaStream_t s) {
+  SWITCH_DO(g, ax_t, g, y, a, x, bcoef, nprob, s);
+}
+
+void launch_Bv(const Grid& g2, const Grid& g1, const double* tPm, const double* tGm, View v, View bp, View out,
+               double sb, double sB, int nprob, cudaStream_t s) {
+  if (g1.dim == 2)
+    k_Bv<2><<<grid1(g1.n, nprob, BS), BS, 0, s>>>(g2, g1, tPm, tGm, v, bp, out, sb, sB);
+  else
+    k_Bv<3><<<grid1(g1.n, nprob, BS), BS, 0, s>>>(g2, g1, tPm, tGm, v, bp, out, sb, sB);
+}
+
+}  // namespace aao

@@ -1,0 +1,526 @@
+// Time-axis transforms fused with the T-transforms, and the all-at-once KKT matvec.
+//
+//  k_fft_fwd : r (paper order, real) -> T_l^{-1} F r  in the frequency layout
+//              (steps A3; Oseen: no T transform)
+//  k_fft_inv : T_r^{-1} x  -> F^{-1} (...) (paper order, real)  (step A8)
+//  k_kkt_*   : y = A x of eq. (FinalA) (step A2)
+//
+// Layout choice: the Krylov vectors keep the paper's
+// order [half][t][field][node] -- SPACE is contiguous.  A CTA owns a tile of TD
+// consecutive spatial columns for all n_b time rows of both halves: every global
+// load/store is a coalesced row segment, the time DFT runs along the tile in
+// shared memory, and the frequency layout [k][half][field][node] (space
+// contiguous again) falls out of the same tile.  No separate transpose pass.
+#include "aao_internal.h"
+
+namespace aao {
+
+namespace {
+
+struct InvSrc {
+  const double2* v1;   // slot 1 (x1) velocity, element (k, comp, node) at k*vstride + comp*n_s + node
+  const double2* v2;   // slot 2 (x2)
+  long vstride;
+  const double2* pA;   // pressure, (k, h, node) at k*pstride + h*phoff + node
+  const double2* pB;   // Stokes only: Chebyshev(M_p) part
+  long pstride, phoff;
+  int stokes;
+  double pscale;       // Oseen: slots 3/4 = pscale * pA
+};
+
+__device__ __forceinline__ bool q2_interior(long node, int n1, int dim) {
+  int i = (int)(node % n1), j = (int)((node / n1) % n1);
+  bool in = i > 0 && i < n1 - 1 && j > 0 && j < n1 - 1;
+  if (dim == 3) {
+    int k = (int)(node / ((long)n1 * n1));
+    in = in && k > 0 && k < n1 - 1;
+  }
+  return in;
+}
+
+struct Geo {
+  int dim, n1q2, n1q1, n_b, n_f;
+  long n_s, n_v, n_p, nblk;
+  double tau, nu, beta;
+};
+
+// slot values y_h0, y_h1 of column `col` at frequency k (after T_r^{-1} for Stokes)
+__device__ __forceinline__ void slot_values(const Geo& G, const InvSrc& S, const FreqConst& f, int k, long col,
+                                            double2& y0, double2& y1) {
+  const double st = sqrt(G.tau);
+  if (col < G.n_v) {
+    const long comp = col / G.n_s, node = col % G.n_s;
+    const double2 x1 = S.v1[k * S.vstride + comp * G.n_s + node];
+    const double2 x2 = S.v2[k * S.vstride + comp * G.n_s + node];
+    if (S.stokes) {
+      // T_r^{-1}: y2 = x2 c2 / sqrt(tau); y1 = (x1 + i (dc/sqrt(tau)) y2) / sqrt(tau)
+      const double2 yy2 = make_double2(x2.x * f.c2 / st, x2.y * f.c2 / st);
+      const double a = f.dc / st;
+      y0 = make_double2((x1.x - a * yy2.y) / st, (x1.y + a * yy2.x) / st);
+      y1 = yy2;
+    } else {
+      y0 = x1;
+      y1 = x2;
+    }
+  } else {
+    const long node = col - G.n_v;
+    const double2 a0 = S.pA[k * S.pstride + node];
+    const double2 a1 = S.pA[k * S.pstride + S.phoff + node];
+    if (S.stokes) {
+      // x3 = (1+c1) K_p^{-1} s3 + nu c2 M_p^{-1} s3, same for x4
+      const double2 b0 = S.pB[k * S.pstride + node];
+      const double2 b1 = S.pB[k * S.pstride + S.phoff + node];
+      const double ca = 1.0 + f.c1, cb = G.nu * f.c2;
+      const double2 x3 = make_double2(ca * a0.x + cb * b0.x, ca * a0.y + cb * b0.y);
+      const double2 x4 = make_double2(ca * a1.x + cb * b1.x, ca * a1.y + cb * b1.y);
+      // T_r^{-1}: y4 = x4 / sqrt(tau); y3 = (x3 + i (dc c2 / sqrt(tau)) y4) / (sqrt(tau) c2)
+      const double2 yy4 = make_double2(x4.x / st, x4.y / st);
+      const double a = f.dc * f.c2 / st, den = st * f.c2;
+      y0 = make_double2((x3.x - a * yy4.y) / den, (x3.y + a * yy4.x) / den);
+      y1 = yy4;
+    } else {
+      y0 = make_double2(S.pscale * a0.x, S.pscale * a0.y);
+      y1 = make_double2(S.pscale * a1.x, S.pscale * a1.y);
+    }
+  }
+}
+
+__device__ __forceinline__ bool col_masked(const Geo& G, long col) {
+  if (col < G.n_v) return !q2_interior(col % G.n_s, G.n1q2, G.dim);
+  return (col - G.n_v) == 0;
+}
+
+// ------------------------------------------------------------------ forward transform
+__global__ void k_fft_fwd(Geo G, const double* __restrict__ r, double2* __restrict__ Fv, double2* __restrict__ Fp,
+                          const FreqConst* __restrict__ fc, const double2* __restrict__ tw, int TD, int stokes) {
+  extern __shared__ double sm[];
+  const int n_b = G.n_b;
+  double2* stw = reinterpret_cast<double2*>(sm);
+  double* xs = sm + 2 * n_b;  // [2 n_b][TD]
+  const int tx = threadIdx.x, ty = threadIdx.y, KY = blockDim.y;
+  const int tid = ty * blockDim.x + tx;
+  for (int m = tid; m < n_b; m += blockDim.x * KY) stw[m] = tw[m];
+  const long col = (long)blockIdx.x * TD + tx;
+  const bool valid = col < G.nblk;
+  const bool msk = !valid || col_masked(G, col);
+  for (int row = ty; row < 2 * n_b; row += KY)
+    xs[row * TD + tx] = msk ? 0.0 : __ldg(r + (long)row * G.nblk + col);
+  __syncthreads();
+  if (!valid) return;
+  const double st = sqrt(G.tau);
+  for (int k = ty; k < G.n_f; k += KY) {
+    // r_hat_k = sum_t r_{t} omega^{k t}, omega = exp(-2 pi i / n_b)   (reading C.2 #2)
+    double a0r = 0, a0i = 0, a1r = 0, a1i = 0;
+    int m = 0;
+    for (int t = 0; t < n_b; ++t) {
+      const double2 w = stw[m];
+      const double x0 = xs[t * TD + tx], x1 = xs[(n_b + t) * TD + tx];
+      a0r = fma(x0, w.x, a0r);
+      a0i = fma(-x0, w.y, a0i);
+      a1r = fma(x1, w.x, a1r);
+      a1i = fma(-x1, w.y, a1i);
+      m += k;
+      if (m >= n_b) m -= n_b;
+    }
+    double2 s0 = make_double2(a0r, a0i), s1 = make_double2(a1r, a1i);
+    const FreqConst f = fc[k];
+    if (col < G.n_v) {
+      if (stokes) {
+        // T_l^{-1}: s1 = r1/sqrt(tau); s2 = (r2 - i (dc/sqrt(tau)) s1) c2 / sqrt(tau)
+        const double2 q1 = make_double2(s0.x / st, s0.y / st);
+        const double a = f.dc / st, g = f.c2 / st;
+        s1 = make_double2((s1.x + a * q1.y) * g, (s1.y - a * q1.x) * g);
+        s0 = q1;
+      }
+      const long comp = col / G.n_s, node = col % G.n_s;
+      Fv[(((long)k * 2 + 0) * G.dim + comp) * G.n_s + node] = s0;
+      Fv[(((long)k * 2 + 1) * G.dim + comp) * G.n_s + node] = s1;
+    } else {
+      if (stokes) {
+        // s3 = r3 / (sqrt(tau) c2); s4 = (r4 - i (dc c2 / sqrt(tau)) s3) / sqrt(tau)
+        const double den = st * f.c2;
+        const double2 q3 = make_double2(s0.x / den, s0.y / den);
+        const double a = f.dc * f.c2 / st;
+        s1 = make_double2((s1.x + a * q3.y) / st, (s1.y - a * q3.x) / st);
+        s0 = q3;
+      }
+      const long node = col - G.n_v;
+      Fp[((long)k * 2 + 0) * G.n_p + node] = s0;
+      Fp[((long)k * 2 + 1) * G.n_p + node] = s1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ inverse transform
+__global__ void k_fft_inv(Geo G, InvSrc S, double* __restrict__ z, const FreqConst* __restrict__ fc,
+                          const double2* __restrict__ tw, int TD) {
+  extern __shared__ double sm[];
+  const int n_b = G.n_b, n_f = G.n_f;
+  double2* stw = reinterpret_cast<double2*>(sm);
+  double2* ys = stw + n_b;  // [2][n_f][TD]
+  const int tx = threadIdx.x, ty = threadIdx.y, KY = blockDim.y;
+  const int tid = ty * blockDim.x + tx;
+  for (int m = tid; m < n_b; m += blockDim.x * KY) stw[m] = tw[m];
+  const long col = (long)blockIdx.x * TD + tx;
+  const bool valid = col < G.nblk;
+  const bool msk = !valid || col_masked(G, col);
+  for (int k = ty; k < n_f; k += KY) {
+    double2 y0 = make_double2(0, 0), y1 = y0;
+    if (!msk) slot_values(G, S, fc[k], k, col, y0, y1);
+    ys[(0 * n_f + k) * TD + tx] = y0;
+    ys[(1 * n_f + k) * TD + tx] = y1;
+  }
+  __syncthreads();
+  if (!valid) return;
+  const bool even = (n_b % 2) == 0;
+  const double inv_n = 1.0 / n_b;
+  for (int t = ty; t < n_b; t += KY) {
+    // y_t = (1/n_b) sum_k y_hat_k omega^{-k t}, using y_hat_{n_b-k} = conj(y_hat_k)
+    double acc0 = ys[(0 * n_f) * TD + tx].x, acc1 = ys[(1 * n_f) * TD + tx].x;
+    int m = 0;
+    for (int k = 1; k < n_f; ++k) {
+      m += t;
+      if (m >= n_b) m -= n_b;
+      const double2 w = stw[m];
+      const double wk = (even && 2 * k == n_b) ? 1.0 : 2.0;
+      const double2 a = ys[(0 * n_f + k) * TD + tx], b = ys[(1 * n_f + k) * TD + tx];
+      acc0 = fma(wk, a.x * w.x - a.y * w.y, acc0);
+      acc1 = fma(wk, b.x * w.x - b.y * w.y, acc1);
+    }
+    z[(long)t * G.nblk + col] = msk ? 0.0 : acc0 * inv_n;
+    z[(long)(n_b + t) * G.nblk + col] = msk ? 0.0 : acc1 * inv_n;
+  }
+}
+
+__global__ void k_debug_block(Geo G, InvSrc S, const FreqConst* __restrict__ fc, int k, double2* out) {
+  const long col = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= G.nblk) return;
+  double2 y0 = make_double2(0, 0), y1 = y0;
+  if (!col_masked(G, col)) slot_values(G, S, fc[k], k, col, y0, y1);
+  out[col] = y0;
+  out[G.nblk + col] = y1;
+}
+
+// ------------------------------------------------------------------ KKT matvec (real)
+struct KKTTab {
+  const double *tM, *tK, *conv, *convT;   // fine Q2 (eliminated columns zero)
+  const double *tPmT, *tGmT;              // B^T rows [n1q2][3]
+  const double *tPm, *tGm;                // B rows [n1q1][5]
+};
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// velocity rows: half 0  y1v_t = M(tau v_t + lam_t - lam_{t+1}) + tau L^T lam_t + tau B^T mu_t
+//                half 1  y2v_t = M(v_t - v_{t-1} - tau/beta lam_t) + tau L v_t + tau B^T p_t
+// (eq. FinalA expanded block-row by block-row, with E (x) M = backward-Euler difference)
+template <int DIM>
+__global__ void k_kkt_vel(Geo G, KKTTab T, const double* __restrict__ x, double* __restrict__ y, int oseen) {
+  const long col = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= G.n_v) return;
+  const int row = blockIdx.y;  // h * n_b + t
+  const int h = row / G.n_b, t = row % G.n_b;
+  const long comp = col / G.n_s, node = col % G.n_s;
+  const int n1 = G.n1q2;
+  int c[3];
+  c[0] = (int)(node % n1);
+  c[1] = (int)((node / n1) % n1);
+  c[2] = DIM == 3 ? (int)(node / ((long)n1 * n1)) : 0;
+  double* yo = y + (long)row * G.nblk + col;
+  bool interior = true;
+  for (int a = 0; a < DIM; ++a) interior = interior && c[a] > 0 && c[a] < n1 - 1;
+  if (!interior) {
+    *yo = 0.0;
+    return;
+  }
+  const long nblk = G.nblk, n_b = G.n_b;
+  const double tau = G.tau;
+  // slices (all at component comp): A = the M-combined input, Bk = the L-input
+  const double* xv = x + (long)t * nblk + comp * G.n_s;                    // v_t
+  const double* xl = x + (long)(n_b + t) * nblk + comp * G.n_s;            // lam_t
+  const double* xo = nullptr;                                              // lam_{t+1} or v_{t-1}
+  double cA, cB, cO;  // w = cA*v_t + cB*lam_t + cO*other
+  const double* xL;   // operand of L (or L^T)
+  if (h == 0) {
+    cA = tau; cB = 1.0; cO = -1.0;
+    if (t + 1 < n_b) xo = x + (long)(n_b + t + 1) * nblk + comp * G.n_s;
+    xL = xl;
+  } else {
+    cA = 1.0; cB = -tau / G.beta; cO = -1.0;
+    if (t >= 1) xo = x + (long)(t - 1) * nblk + comp * G.n_s;
+    xL = xv;
+  }
+  double m[DIM][5], k[DIM][5];
+  for (int a = 0; a < DIM; ++a)
+    for (int o = 0; o < 5; ++o) {
+      m[a][o] = __ldg(T.tM + c[a] * 5 + o);
+      k[a][o] = __ldg(T.tK + c[a] * 5 + o);
+    }
+  const double* cv = oseen ? ((h == 0 ? T.convT : T.conv) + node * (DIM == 2 ? 25 : 125)) : nullptr;
+  double Mw = 0, KL = 0, CL = 0;
+  const int nz = DIM == 3 ? 5 : 1;
+  for (int oc = 0; oc < nz; ++oc) {
+    const int kk = DIM == 3 ? clampi(c[2] + oc - 2, 0, n1 - 1) : 0;
+    const double mz = DIM == 3 ? m[DIM == 3 ? 2 : 0][oc] : 1.0;
+    const double kz = DIM == 3 ? k[DIM == 3 ? 2 : 0][oc] : 0.0;
+    for (int ob = 0; ob < 5; ++ob) {
+      const int jj = clampi(c[1] + ob - 2, 0, n1 - 1);
+      const double mzy = mz * m[1][ob];
+      const double kzy = kz * m[1][ob] + mz * k[1][ob];
+#pragma unroll
+      for (int oa = 0; oa < 5; ++oa) {
+        const int ii = clampi(c[0] + oa - 2, 0, n1 - 1);
+        const long nb = ((long)kk * n1 + jj) * n1 + ii;
+        const double mm = mzy * m[0][oa];
+        const double kc = kzy * m[0][oa] + mzy * k[0][oa];
+        double w = cA * __ldg(xv + nb) + cB * __ldg(xl + nb);
+        if (xo) w += cO * __ldg(xo + nb);
+        Mw = fma(mm, w, Mw);
+        const double uL = __ldg(xL + nb);
+        KL = fma(kc, uL, KL);
+        if (oseen) CL = fma(__ldg(cv + (oc * 5 + ob) * 5 + oa), uL, CL);
+      }
+    }
+  }
+  // B^T q: q = mu_t (half 0) or p_t (half 1); B_c = -(prod of Pm, with Gm on axis c), pinned node skipped
+  const double* q = x + (long)(h == 0 ? (n_b + t) : t) * nblk + G.n_v;
+  double P[DIM][3], Gd[DIM][3];
+  int I0[DIM];
+  for (int a = 0; a < DIM; ++a) {
+    I0[a] = (c[a] - 1 >= 0) ? (c[a] - 1) / 2 : -1;
+    for (int o = 0; o < 3; ++o) {
+      P[a][o] = __ldg(T.tPmT + c[a] * 3 + o);
+      Gd[a][o] = __ldg(T.tGmT + c[a] * 3 + o);
+    }
+  }
+  const int m1 = G.n1q1;
+  double BTq = 0;
+  for (int oc = 0; oc < (DIM == 3 ? 3 : 1); ++oc) {
+    double fz = 1.0;
+    int Kz = 0;
+    if (DIM == 3) {
+      fz = (comp == 2 ? Gd[2][oc] : P[2][oc]);
+      Kz = I0[2] + oc;
+      if (fz == 0.0 || Kz < 0 || Kz >= m1) continue;
+    }
+    for (int ob = 0; ob < 3; ++ob) {
+      const double fy = (comp == 1 ? Gd[1][ob] : P[1][ob]);
+      const int J = I0[1] + ob;
+      if (fy == 0.0 || J < 0 || J >= m1) continue;
+      for (int oa = 0; oa < 3; ++oa) {
+        const double fx = (comp == 0 ? Gd[0][oa] : P[0][oa]);
+        const int I = I0[0] + oa;
+        if (fx == 0.0 || I < 0 || I >= m1) continue;
+        const long pn = ((long)Kz * m1 + J) * m1 + I;
+        if (pn == 0) continue;  // pinned pressure node: eliminated column
+        BTq = fma(-fz * fy * fx, __ldg(q + pn), BTq);
+      }
+    }
+  }
+  *yo = Mw + tau * (G.nu * KL + CL) + tau * BTq;
+}
+
+// pressure rows: half 0 y1p_t = tau B lam_t ; half 1 y2p_t = tau B v_t
+template <int DIM>
+__global__ void k_kkt_pres(Geo G, KKTTab T, const double* __restrict__ x, double* __restrict__ y) {
+  const long node = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= G.n_p) return;
+  const int row = blockIdx.y;
+  const int h = row / G.n_b, t = row % G.n_b;
+  double* yo = y + (long)row * G.nblk + G.n_v + node;
+  if (node == 0) {
+    *yo = 0.0;
+    return;
+  }
+  const int m1 = G.n1q1, n1 = G.n1q2;
+  int c[3];
+  c[0] = (int)(node % m1);
+  c[1] = (int)((node / m1) % m1);
+  c[2] = DIM == 3 ? (int)(node / ((long)m1 * m1)) : 0;
+  const double* u = x + (long)(h == 0 ? (G.n_b + t) : t) * G.nblk;
+  double Pm[DIM][5], Gm[DIM][5];
+  for (int a = 0; a < DIM; ++a)
+    for (int o = 0; o < 5; ++o) {
+      Pm[a][o] = __ldg(T.tPm + c[a] * 5 + o);
+      Gm[a][o] = __ldg(T.tGm + c[a] * 5 + o);
+    }
+  double acc = 0;
+  for (int comp = 0; comp < DIM; ++comp) {
+    const double* uc = u + comp * G.n_s;
+    for (int oc = 0; oc < (DIM == 3 ? 5 : 1); ++oc) {
+      double fz = 1.0;
+      int kk = 0;
+      if (DIM == 3) {
+        fz = comp == 2 ? Gm[2][oc] : Pm[2][oc];
+        kk = clampi(2 * c[2] + oc - 2, 0, n1 - 1);
+      }
+      for (int ob = 0; ob < 5; ++ob) {
+        const double fy = comp == 1 ? Gm[1][ob] : Pm[1][ob];
+        const int jj = clampi(2 * c[1] + ob - 2, 0, n1 - 1);
+#pragma unroll
+        for (int oa = 0; oa < 5; ++oa) {
+          const double fx = comp == 0 ? Gm[0][oa] : Pm[0][oa];
+          const int ii = clampi(2 * c[0] + oa - 2, 0, n1 - 1);
+          acc = fma(-fz * fy * fx, __ldg(uc + ((long)kk * n1 + jj) * n1 + ii), acc);
+        }
+      }
+    }
+  }
+  *yo = G.tau * acc;
+}
+
+__global__ void k_mask_copy(Geo G, const double* __restrict__ in, double* __restrict__ out, long N) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const long col = i % G.nblk;
+  out[i] = col_masked(G, col) ? 0.0 : in[i];
+}
+
+// b = tau (M_full v_d)|_interior in the adjoint-velocity rows (half 0), 0 elsewhere
+template <int DIM>
+__global__ void k_rhs(Geo G, const double* __restrict__ tMf, const double* __restrict__ vd, double* __restrict__ b) {
+  const long col = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= G.nblk) return;
+  const int row = blockIdx.y;
+  double* bo = b + (long)row * G.nblk + col;
+  if (row >= G.n_b || col >= G.n_v || col_masked(G, col)) {
+    *bo = 0.0;
+    return;
+  }
+  const long comp = col / G.n_s, node = col % G.n_s;
+  const int n1 = G.n1q2;
+  int c[3];
+  c[0] = (int)(node % n1);
+  c[1] = (int)((node / n1) % n1);
+  c[2] = DIM == 3 ? (int)(node / ((long)n1 * n1)) : 0;
+  const double* v = vd + comp * G.n_s;
+  double acc = 0;
+  for (int oc = 0; oc < (DIM == 3 ? 5 : 1); ++oc) {
+    const double fz = DIM == 3 ? tMf[c[2] * 5 + oc] : 1.0;
+    const int kk = DIM == 3 ? clampi(c[2] + oc - 2, 0, n1 - 1) : 0;
+    for (int ob = 0; ob < 5; ++ob) {
+      const double fy = tMf[c[1] * 5 + ob];
+      const int jj = clampi(c[1] + ob - 2, 0, n1 - 1);
+      for (int oa = 0; oa < 5; ++oa) {
+        const double fx = tMf[c[0] * 5 + oa];
+        const int ii = clampi(c[0] + oa - 2, 0, n1 - 1);
+        acc = fma(fz * fy * fx, v[((long)kk * n1 + jj) * n1 + ii], acc);
+      }
+    }
+  }
+  *bo = G.tau * acc;
+}
+
+Geo geo_of(const Ctx& c) {
+  Geo g;
+  g.dim = c.dim;
+  g.n1q2 = c.n1q2;
+  g.n1q1 = c.n1q1;
+  g.n_b = c.n_b;
+  g.n_f = c.n_f;
+  g.n_s = c.n_s;
+  g.n_v = c.n_v;
+  g.n_p = c.n_p;
+  g.nblk = c.nblk;
+  g.tau = c.tau;
+  g.nu = c.nu;
+  g.beta = c.beta;
+  return g;
+}
+
+InvSrc src_of(const Ctx& c) {
+  InvSrc S;
+  if (!c.oseen) {
+    S.v1 = c.Xv;
+    S.v2 = c.Xv + (long)c.dim * c.n_s;
+    S.vstride = 2L * c.dim * c.n_s;
+    S.pA = c.XpA;
+    S.pB = c.XpB;
+    S.stokes = 1;
+    S.pscale = 0.0;
+  } else {
+    S.v1 = c.X1;
+    S.v2 = c.X2;
+    S.vstride = (long)c.dim * c.n_s;
+    S.pA = c.XpA;
+    S.pB = nullptr;
+    S.stokes = 0;
+    S.pscale = -1.0 / c.tau;   // (y3, y4) = -S_hat^{-1}(...), with the 1/tau of [[0,tau K_p],[tau K_p,0]]^{-1}
+  }
+  S.pstride = 2L * c.n_p;
+  S.phoff = c.n_p;
+  return S;
+}
+
+int tile_width(int n_b, int n_f, size_t* smem_fwd, size_t* smem_inv) {
+  int TD = 32;
+  for (;;) {
+    size_t f = (size_t)n_b * 16 + 2ull * n_b * TD * 8;
+    size_t i = (size_t)n_b * 16 + 2ull * n_f * TD * 16;
+    if ((f <= 160 * 1024 && i <= 160 * 1024) || TD == 8) {
+      *smem_fwd = f;
+      *smem_inv = i;
+      return TD;
+    }
+    TD /= 2;
+  }
+}
+
+}  // namespace
+
+void launch_fft_fwd(const Ctx& c, const double* r, cudaStream_t s) {
+  size_t sf, si;
+  const int TD = tile_width(c.n_b, c.n_f, &sf, &si);
+  cudaFuncSetAttribute(k_fft_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
+  dim3 blk(TD, 256 / TD);
+  dim3 grd((unsigned)((c.nblk + TD - 1) / TD));
+  k_fft_fwd<<<grd, blk, sf, s>>>(geo_of(c), r, c.Fv, c.Fp, c.fc, c.tw, TD, c.oseen ? 0 : 1);
+}
+
+void launch_fft_inv(const Ctx& c, double* z, cudaStream_t s) {
+  size_t sf, si;
+  const int TD = tile_width(c.n_b, c.n_f, &sf, &si);
+  cudaFuncSetAttribute(k_fft_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)si);
+  dim3 blk(TD, 256 / TD);
+  dim3 grd((unsigned)((c.nblk + TD - 1) / TD));
+  k_fft_inv<<<grd, blk, si, s>>>(geo_of(c), src_of(c), z, c.fc, c.tw, TD);
+}
+
+void launch_debug_block(const Ctx& c, int k, double2* out, cudaStream_t s) {
+  k_debug_block<<<(unsigned)((c.nblk + 255) / 256), 256, 0, s>>>(geo_of(c), src_of(c), c.fc, k, out);
+}
+
+void launch_kkt(const Ctx& c, const double* x, double* y, cudaStream_t s) {
+  KKTTab T;
+  T.tM = c.vel.grids[0].tM;
+  T.tK = c.vel.grids[0].tK;
+  T.conv = c.vel.grids[0].conv;
+  T.convT = c.vel.grids[0].convT;
+  T.tPmT = c.tPmT;
+  T.tGmT = c.tGmT;
+  T.tPm = c.tPm;
+  T.tGm = c.tGm;
+  const Geo G = geo_of(c);
+  dim3 gv((unsigned)((c.n_v + 127) / 128), 2 * c.n_b);
+  dim3 gp((unsigned)((c.n_p + 127) / 128), 2 * c.n_b);
+  if (c.dim == 2) {
+    k_kkt_vel<2><<<gv, 128, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0);
+    k_kkt_pres<2><<<gp, 128, 0, s>>>(G, T, x, y);
+  } else {
+    k_kkt_vel<3><<<gv, 128, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0);
+    k_kkt_pres<3><<<gp, 128, 0, s>>>(G, T, x, y);
+  }
+}
+
+void launch_mask_copy(const Ctx& c, const double* in, double* out, cudaStream_t s) {
+  k_mask_copy<<<(unsigned)((c.N + 255) / 256), 256, 0, s>>>(geo_of(c), in, out, c.N);
+}
+
+void launch_rhs(const Ctx& c, const double* vd, double* b, cudaStream_t s) {
+  dim3 g((unsigned)((c.nblk + 127) / 128), 2 * c.n_b);
+  if (c.dim == 2)
+    k_rhs<2><<<g, 128, 0, s>>>(geo_of(c), c.tMfull, vd, b);
+  else
+    k_rhs<3><<<g, 128, 0, s>>>(geo_of(c), c.tMfull, vd, b);
+}
+
+}  // namespace aao

@@ -1,0 +1,51 @@
+"""Write oracle GMRES reference histories to tests/golden/gmres_<case>.json.
+
+Calls ONLY oracle/ and synth/ (never the CUDA path).  The stored values are the
+oracle's residual histories |g_{k+1}|/||b|| and iteration counts for GMRES(30),
+tol 1e-6, x0 = 0, used by tests/test_gpu_parity.py for the
+"KKT residual histories agreeing to 1e-8, iteration counts within +-1" bar.
+
+usage: python tests/golden/gen_oracle_refs.py c1 oseen_small [c2 c2b ...]
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+from oracle import gmres, kkt, precond  # noqa: E402
+from oracle.problem import Problem  # noqa: E402
+
+CASES = {
+    "c1": synth.CONFIGS["c1"],
+    "c2": synth.CONFIGS["c2"],
+    "c2b": synth.CONFIGS["c2b"],
+    "oseen_small": synth.small_config("oseen_small", 2, 8, 8, problem="oseen", lo=-1.0, hi=1.0,
+                                      beta=1e-3, nu=1.0 / 20.0, index=3),
+    "stokes3d_small": synth.small_config("stokes3d_small", 3, 4, 6, beta=1e-3, nu=1e-2, index=5),
+}
+
+
+def run(name):
+    cfg = CASES[name]
+    t0 = time.time()
+    prob = Problem(cfg, synth.wind(cfg))
+    pc = precond.OraclePreconditioner(prob)
+    b = kkt.build_rhs(prob, synth.desired_state(cfg))
+    x, hist, info = gmres.gmres(lambda v: kkt.kkt_apply(prob, v), pc.apply, b, tol=1e-6, restart=30)
+    out = dict(case=name, config=cfg.__dict__, iterations=info["iterations"], restarts=info["restarts"],
+               converged=info["converged"], true_relres=[float(v) for v in info["true_relres"]],
+               hist=[float(h) for h in hist], oracle_seconds=time.time() - t0,
+               generator="tests/golden/gen_oracle_refs.py (oracle only)")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"gmres_{name}.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print(name, info["iterations"], info["true_relres"][-1], f"{time.time() - t0:.1f}s", flush=True)
+
+
+if __name__ == "__main__":
+    for n in sys.argv[1:]:
+        run(n)

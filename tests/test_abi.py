@@ -1,0 +1,104 @@
+"""CPU-side checks of the C-ABI boundary (no GPU needed): the library builds, loads and exports
+every symbol declared in include/aao.h; the ctypes structs match the C layout; config
+validation rejects invalid inputs before touching the device."""
+import ctypes
+import os
+import re
+import subprocess
+import tempfile
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "aao.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2405_18964_b200 import build, aao
+    build.build()
+    return aao.load()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(aao_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_the_survey_boundary():
+    names = declared_functions()
+    for required in ("aao_create", "aao_destroy", "aao_kkt_apply", "aao_precond_apply", "aao_gmres_solve",
+                     "aao_build_rhs", "aao_pack", "aao_debug_freq_block", "aao_last_error", "aao_vector_len"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2405_18964_b200 import aao
+    out = subprocess.run(["nm", "-D", "--defined-only", aao.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (aao_[a-z_0-9]+)\b", out))
+    missing = [n for n in declared_functions() if n not in exported]
+    assert not missing, missing
+    assert set(aao.EXPORTS) <= exported
+    for n in declared_functions():
+        getattr(lib, n)
+
+
+def test_ctypes_layout_matches_c(lib):
+    """Compile a probe against aao.h with gcc and compare sizes / offsets with the ctypes mirror."""
+    from paper_2405_18964_b200 import aao
+    probe = r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "aao.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu\n", sizeof(aao_config), offsetof(aao_config, wind_q2),
+         offsetof(aao_config, uzawa_mu), sizeof(aao_krylov), sizeof(aao_info));
+  printf("%zu %zu\n", offsetof(aao_info, final_relres), offsetof(aao_info, ms_total));
+  return 0;
+}'''
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "p.c")
+        open(c, "w").write(probe)
+        exe = os.path.join(d, "p")
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe], check=True)
+        vals = list(map(int, subprocess.run([exe], capture_output=True, text=True).stdout.split()))
+    C, K, I = aao.Config, aao.Krylov, aao.Info
+    assert vals == [ctypes.sizeof(C), C.wind_q2.offset, C.uzawa_mu.offset, ctypes.sizeof(K), ctypes.sizeof(I),
+                    I.final_relres.offset, I.ms_total.offset]
+
+
+def test_config_defaults_are_the_papers(lib):
+    from paper_2405_18964_b200 import aao
+    cfg = aao.Config()
+    lib.aao_config_defaults(ctypes.byref(cfg))
+    assert (cfg.mg_cycles, cfg.cheb_iters, cfg.uzawa_iters, cfg.uzawa_mu) == (4, 10, 6, 0.75)
+    assert (cfg.pre_sweeps, cfg.post_sweeps, cfg.omega) == (2, 2, 1.0)
+
+
+@pytest.mark.parametrize("field,value", [("beta", 0.0), ("nu", -1.0), ("T", 0.0), ("n_t", 2), ("dim", 4),
+                                         ("n_cells", 6), ("n_cells", 2), ("mg_cycles", 0), ("problem", 1)])
+def test_invalid_configs_rejected_before_device_work(lib, field, value):
+    from paper_2405_18964_b200 import aao
+    cfg = aao.Config()
+    lib.aao_config_defaults(ctypes.byref(cfg))
+    setattr(cfg, field, value)        # problem=1 (Oseen) without wind_q2 is invalid too
+    h = ctypes.c_void_p()
+    assert lib.aao_create(ctypes.byref(cfg), ctypes.byref(h)) == -1      # AAO_ERR_CONFIG
+    assert not h.value
+
+
+def test_null_arguments_rejected(lib):
+    assert lib.aao_create(None, None) == -2
+    assert lib.aao_kkt_apply(None, None, None, None) == -2
+    assert lib.aao_precond_apply(None, None, None, None) == -2
+    assert lib.aao_last_error(None) == b"null context"
+
+
+def test_binding_refuses_without_cuda():
+    import torch
+    from paper_2405_18964_b200 import AAOError, Context
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(AAOError):
+        Context(2, 4, 0.0, 1.0, 4, 1.0, 1e-2, 1e-2)

@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): precond_apply relative 2-norm error <= 1e-10 (fp64);
+kkt_apply <= 1e-12; GMRES residual histories within 1e-8 (relative, per entry) and
+iteration counts within +-1 of the oracle (tests/golden/gmres_*.json, written by
+tests/golden/gen_oracle_refs.py which calls only oracle/).
+Sizes: reduced configs that span several tiles and ragged tails (odd and even n_b,
+2-D and 3-D, Stokes and Oseen), the BASELINE configs where the oracle is affordable
+(c1, c2 full), and frequency-sampled blocks at full size (c3, c5, c4).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+PRECOND_TOL = 1e-10
+KKT_TOL = 1e-12
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    return torch
+
+
+_oracle_cache = {}
+
+
+def oracle_for(cfg):
+    from oracle import precond
+    from oracle.problem import Problem
+    if cfg.name not in _oracle_cache or _oracle_cache[cfg.name][0] is not cfg:
+        prob = Problem(cfg, synth.wind(cfg))
+        _oracle_cache[cfg.name] = (cfg, prob, precond.OraclePreconditioner(prob, cache_blocks=False))
+    return _oracle_cache[cfg.name][1:]
+
+
+def gpu_ctx(cfg):
+    from paper_2405_18964_b200 import Context
+    return Context.from_config(cfg, synth.wind(cfg))
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+SMALL = [
+    synth.small_config("s2d_odd", 2, 16, 10, beta=1e-2, nu=1e-2),           # n_b = 9 (odd), 5 MG levels
+    synth.small_config("s2d_even", 2, 8, 11, beta=1e-4, nu=1e-2),           # n_b = 10 (even: Nyquist term)
+    synth.small_config("s2d_nt3", 2, 4, 3, beta=1e-2, nu=1e-2),             # n_b = 2, minimal
+    synth.small_config("o2d", 2, 8, 8, problem="oseen", lo=-1.0, hi=1.0, beta=1e-3, nu=1 / 20, index=3),
+    synth.small_config("o2d_even", 2, 16, 7, problem="oseen", lo=-1.0, hi=1.0, beta=1e-2, nu=1 / 20, index=3),
+    synth.small_config("s3d", 3, 4, 6, beta=1e-3, nu=1e-2, index=5),
+    synth.small_config("s3d_even", 3, 8, 5, beta=1e-2, nu=1e-2, index=5),
+]
+
+
+@pytest.mark.parametrize("cfg", SMALL + [synth.CONFIGS["c1"]], ids=lambda c: c.name)
+def test_kkt_parity(cfg):
+    torch = _torch()
+    from oracle import kkt
+    prob, _ = oracle_for(cfg)
+    ctx = gpu_ctx(cfg)
+    x = synth.probe_vector(cfg)
+    y = ctx.kkt_apply(torch.from_numpy(x).cuda()).cpu().numpy()
+    yo = kkt.kkt_apply(prob, x)
+    assert rel(y, yo) <= KKT_TOL
+    assert np.all(y[~synth.full_mask(cfg)] == 0.0)
+
+
+@pytest.mark.parametrize("cfg", SMALL + [synth.CONFIGS["c1"]], ids=lambda c: c.name)
+def test_precond_parity(cfg):
+    torch = _torch()
+    _, pc = oracle_for(cfg)
+    ctx = gpu_ctx(cfg)
+    r = synth.probe_vector(cfg)
+    z = ctx.precond_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    zo = pc.apply(r)
+    assert rel(z, zo) <= PRECOND_TOL, rel(z, zo)
+    assert np.all(z[~synth.full_mask(cfg)] == 0.0)
+    # frequency blocks of the same application (debug entry) against the oracle's block solve
+    for k in sorted({0, 1, cfg.n_f - 1}):
+        Y, Q = pc.freq_block(r, k)
+        blk = ctx.debug_freq_block(k)
+        for h in range(2):
+            ref = prob_block(cfg, Y[h], Q[h])
+            assert rel(blk[h], ref) <= PRECOND_TOL
+
+
+def prob_block(cfg, Yh, Qh):
+    """Scatter the oracle's reduced block (d, nI) + (npu,) into the full-grid field order."""
+    prob, _ = oracle_for(cfg)
+    out = np.zeros(prob.n_block, dtype=complex)
+    f = prob.fine
+    for c in range(cfg.dim):
+        out[c * prob.n_s + f.Iv] = Yh[c]
+    out[cfg.dim * prob.n_s + f.Ip] = Qh
+    return out
+
+
+def test_masked_inputs_ignored_and_linearity_and_determinism():
+    torch = _torch()
+    cfg = SMALL[0]
+    ctx = gpu_ctx(cfg)
+    rng = np.random.default_rng(11)
+    r = synth.probe_vector(cfg)
+    g = r.copy()
+    g[~synth.full_mask(cfg)] = rng.standard_normal(int((~synth.full_mask(cfg)).sum())) * 1e3
+    for op in (ctx.precond_apply, ctx.kkt_apply):
+        a = op(torch.from_numpy(r).cuda()).cpu().numpy()
+        b = op(torch.from_numpy(g).cuda()).cpu().numpy()
+        assert rel(b, a) <= 1e-14
+        c2 = op(torch.from_numpy(r).cuda()).cpu().numpy()
+        assert np.array_equal(a, c2)                                   # bitwise deterministic
+        r2 = synth.probe_vector(cfg, seed_offset=5)
+        lin = op(torch.from_numpy(2.5 * r + r2).cuda()).cpu().numpy()
+        ref = 2.5 * a + op(torch.from_numpy(r2).cuda()).cpu().numpy()
+        assert rel(lin, ref) <= 1e-12
+        zero = op(torch.zeros(ctx.N, dtype=torch.float64, device="cuda")).cpu().numpy()
+        assert np.all(zero == 0.0)
+
+
+def test_rhs_parity():
+    torch = _torch()
+    from oracle import kkt
+    for cfg in (synth.CONFIGS["c1"], SMALL[3], SMALL[5]):
+        prob, _ = oracle_for(cfg)
+        ctx = gpu_ctx(cfg)
+        vd = synth.desired_state(cfg)
+        b = ctx.build_rhs(vd).cpu().numpy()
+        assert rel(b, kkt.build_rhs(prob, vd)) <= 1e-13
+
+
+def _golden(name):
+    path = os.path.join(GOLDEN, f"gmres_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    return json.load(open(path))
+
+
+GMRES_CASES = {"c1": synth.CONFIGS["c1"], "c2": synth.CONFIGS["c2"],
+               "oseen_small": synth.small_config("oseen_small", 2, 8, 8, problem="oseen", lo=-1.0, hi=1.0,
+                                                 beta=1e-3, nu=1.0 / 20.0, index=3),
+               "stokes3d_small": synth.small_config("stokes3d_small", 3, 4, 6, beta=1e-3, nu=1e-2, index=5)}
+
+
+@pytest.mark.parametrize("name", list(GMRES_CASES))
+def test_gmres_history_parity(name):
+    torch = _torch()
+    ref = _golden(name)
+    cfg = GMRES_CASES[name]
+    ctx = gpu_ctx(cfg)
+    b = ctx.build_rhs(synth.desired_state(cfg))
+    x, info, hist, rc = ctx.gmres_solve(b, tol=1e-6, restart=30)
+    assert abs(info["iterations"] - ref["iterations"]) <= 1
+    assert info["converged"] == 1 and info["true_relres"] <= 2e-6
+    n = min(len(hist), len(ref["hist"]))
+    h, hr = np.array(hist[:n]), np.array(ref["hist"][:n])
+    assert np.max(np.abs(h - hr) / hr) <= 1e-8
+
+
+def test_gmres_host_entry_matches_device_entry():
+    torch = _torch()
+    cfg = synth.CONFIGS["c1"]
+    ctx = gpu_ctx(cfg)
+    b = ctx.build_rhs(synth.desired_state(cfg))
+    x, info, hist, _ = ctx.gmres_solve(b)
+    xh, info_h, hist_h, _ = ctx.gmres_solve_host(b.cpu().numpy())
+    assert info_h["iterations"] == info["iterations"]
+    np.testing.assert_array_equal(xh, x.cpu().numpy())
+
+
+def test_c2_full_precond_and_kkt_parity():
+    """BASELINE configs[1] (the bench workload) at full size: the oracle applies all 63 frequencies."""
+    torch = _torch()
+    from oracle import kkt
+    cfg = synth.CONFIGS["c2"]
+    prob, pc = oracle_for(cfg)
+    ctx = gpu_ctx(cfg)
+    r = synth.probe_vector(cfg)
+    rd = torch.from_numpy(r).cuda()
+    assert rel(ctx.kkt_apply(rd).cpu().numpy(), kkt.kkt_apply(prob, r)) <= KKT_TOL
+    assert rel(ctx.precond_apply(rd).cpu().numpy(), pc.apply(r)) <= PRECOND_TOL
+
+
+@pytest.mark.parametrize("name", ["c3", "c5", "c4_64"])
+def test_full_size_frequency_sampled_parity(name):
+    """Full-size configs: full kkt_apply; precond_apply checked on sampled frequency blocks."""
+    torch = _torch()
+    from oracle import kkt
+    cfg = synth.CONFIGS[name]
+    prob, pc = oracle_for(cfg)
+    ctx = gpu_ctx(cfg)
+    r = synth.probe_vector(cfg)
+    rd = torch.from_numpy(r).cuda()
+    assert rel(ctx.kkt_apply(rd).cpu().numpy(), kkt.kkt_apply(prob, r)) <= KKT_TOL
+    ctx.precond_apply(rd)
+    torch.cuda.synchronize()
+    for k in (0, cfg.n_f - 1):
+        Y, Q = pc.freq_block(r, k)
+        blk = ctx.debug_freq_block(k)
+        for h in range(2):
+            assert rel(blk[h], prob_block(cfg, Y[h], Q[h])) <= PRECOND_TOL
