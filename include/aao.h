@@ -147,6 +147,14 @@ aao_status aao_debug_freq_block(aao_ctx* ctx, int k, double* out, void* stream);
 aao_status aao_set_timing(aao_ctx* ctx, int on);
 aao_status aao_last_phase_ms(aao_ctx* ctx, double* ms4);
 
+/* Live timing of the dominant kernel class, the finest-level multicolour SOR sweeps of the
+   velocity multigrid (CUDA events on the launching stream around each run of sweeps).
+   aao_profile_smoother(ctx, 1) resets and enables; aao_profile_read synchronises and returns
+   out3 = {milliseconds, algorithmic bytes (48 B per unknown per sweep: x and b read, x written,
+   complex128), number of kernel launches} accumulated since, then resets. */
+aao_status aao_profile_smoother(aao_ctx* ctx, int on);
+aao_status aao_profile_read(aao_ctx* ctx, double* out3);
+
 /* Number of kernel launches issued by the last aao_precond_apply / aao_kkt_apply /
    aao_gmres_solve (counted on the host as they are enqueued). */
 long aao_last_launch_count(const aao_ctx* ctx);

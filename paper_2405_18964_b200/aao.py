@@ -46,7 +46,7 @@ class Info(ctypes.Structure):
 EXPORTS = ["aao_config_defaults", "aao_create", "aao_destroy", "aao_last_error", "aao_vector_len",
            "aao_device_bytes", "aao_pack", "aao_build_rhs", "aao_kkt_apply", "aao_precond_apply",
            "aao_gmres_solve", "aao_gmres_solve_host", "aao_debug_freq_block", "aao_set_timing",
-           "aao_last_phase_ms", "aao_last_launch_count"]
+           "aao_last_phase_ms", "aao_last_launch_count", "aao_profile_smoother", "aao_profile_read"]
 
 
 def load(path: str = LIB_PATH):
@@ -83,6 +83,10 @@ def load(path: str = LIB_PATH):
     L.aao_set_timing.restype = st
     L.aao_last_phase_ms.argtypes = [vp, dp]
     L.aao_last_phase_ms.restype = st
+    L.aao_profile_smoother.argtypes = [vp, i]
+    L.aao_profile_smoother.restype = st
+    L.aao_profile_read.argtypes = [vp, dp]
+    L.aao_profile_read.restype = st
     L.aao_last_launch_count.argtypes = [vp]
     L.aao_last_launch_count.restype = ctypes.c_long
     _lib = L
@@ -237,6 +241,15 @@ class Context:
         out = (ctypes.c_double * 4)()
         self._check(self.L.aao_last_phase_ms(self.h, out), "phase_ms")
         return list(out)
+
+    def profile_smoother(self, on=True):
+        self._check(self.L.aao_profile_smoother(self.h, 1 if on else 0), "profile_smoother")
+
+    def profile_read(self):
+        """(ms, algorithmic bytes, launches) of the finest-level SOR sweeps since profile_smoother(True)."""
+        out = (ctypes.c_double * 3)()
+        self._check(self.L.aao_profile_read(self.h, out), "profile_read")
+        return out[0], out[1], int(out[2])
 
     def last_launch_count(self):
         return int(self.L.aao_last_launch_count(self.h))

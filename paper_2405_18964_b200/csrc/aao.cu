@@ -680,6 +680,36 @@ void setup(Ctx& c, const aao_config& cfg) {
 // ------------------------------------------------------------------ block solvers
 inline View contig(double2* p, long n) { return View{p, 1, n}; }
 
+// brackets a run of finest-level smoother launches with events when profiling is on
+struct SweepTimer {
+  Ctx& c;
+  bool on;
+  cudaStream_t s;
+  SweepTimer(Ctx& c_, bool fine, cudaStream_t s_, const Grid& g, int nprob, int sweeps) : c(c_), on(c_.prof && fine && sweeps > 0), s(s_) {
+    if (!on) return;
+    if (c.prof_used + 2 > c.prof_ev.size()) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c.prof_ev.push_back(e);
+      }
+    }
+    cudaEventRecord(c.prof_ev[c.prof_used], s);
+    // algorithmic bytes of one sweep: read x, b and write x once per unknown (complex128)
+    long unknowns = 1;
+    for (int a = 0; a < g.dim; ++a) unknowns *= (g.order == 2 ? g.n1 - 2 : g.n1);
+    if (g.order == 1) unknowns -= 1;
+    const int C = g.order == 2 ? (g.dim == 2 ? 9 : 27) : (g.dim == 2 ? 4 : 8);
+    c.prof_bytes += 48.0 * unknowns * nprob * sweeps;
+    c.prof_launches += (long)C * sweeps;
+  }
+  ~SweepTimer() {
+    if (!on) return;
+    cudaEventRecord(c.prof_ev[c.prof_used + 1], s);
+    c.prof_used += 2;
+  }
+};
+
 void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, int inv_pg, View x, View b, int nprob,
                cudaStream_t s) {
   const Grid& g = S.grids[l];
@@ -690,11 +720,14 @@ void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, i
     return;
   }
   const int C = S.order == 2 ? (c.dim == 2 ? 9 : 27) : (c.dim == 2 ? 4 : 8);
-  for (int sw = 0; sw < c.cfg.pre_sweeps; ++sw)
-    for (int col = 0; col < C; ++col) {
-      launch_gs(g, op, x, b, nprob, col, c.cfg.omega, s);
-      ++cnt;
-    }
+  {
+    SweepTimer tm(c, l == 0 && S.order == 2, s, g, nprob, c.cfg.pre_sweeps);
+    for (int sw = 0; sw < c.cfg.pre_sweeps; ++sw)
+      for (int col = 0; col < C; ++col) {
+        launch_gs(g, op, x, b, nprob, col, c.cfg.omega, s);
+        ++cnt;
+      }
+  }
   View r = contig(S.r[l], g.n);
   launch_residual(g, op, x, b, r, nprob, s);
   const Grid& gc = S.grids[l + 1];
@@ -705,6 +738,7 @@ void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, i
   mg_vcycle(c, S, l + 1, op, inv, inv_pg, xc, bc, nprob, s);
   launch_prolong(g, gc, S.transfers[l], xc, x, nprob, s);
   ++cnt;
+  SweepTimer tm(c, l == 0 && S.order == 2, s, g, nprob, c.cfg.post_sweeps);
   for (int sw = 0; sw < c.cfg.post_sweeps; ++sw)
     for (int col = C - 1; col >= 0; --col) {
       launch_gs(g, op, x, b, nprob, col, c.cfg.omega, s);
@@ -1049,6 +1083,7 @@ void aao_destroy(aao_ctx* ctx) {
   if (ctx->c.hostH) cudaFreeHost(ctx->c.hostH);
   for (auto& e : ctx->c.ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->c.prof_ev) cudaEventDestroy(e);
   delete ctx;
 }
 
@@ -1134,6 +1169,34 @@ aao_status aao_debug_freq_block(aao_ctx* ctx, int k, double* out, void* stream) 
 aao_status aao_set_timing(aao_ctx* ctx, int on) {
   if (!ctx) return AAO_ERR_SHAPE;
   ctx->c.timing = on != 0;
+  return AAO_OK;
+}
+
+aao_status aao_profile_smoother(aao_ctx* ctx, int on) {
+  if (!ctx) return AAO_ERR_SHAPE;
+  ctx->c.prof = on != 0;
+  ctx->c.prof_used = 0;
+  ctx->c.prof_bytes = 0;
+  ctx->c.prof_launches = 0;
+  return AAO_OK;
+}
+
+aao_status aao_profile_read(aao_ctx* ctx, double* out3) {
+  if (!ctx || !out3) return AAO_ERR_SHAPE;
+  auto& c = ctx->c;
+  double ms = 0;
+  if (c.prof_used) cudaEventSynchronize(c.prof_ev[c.prof_used - 1]);
+  for (size_t i = 0; i + 1 < c.prof_used; i += 2) {
+    float t = 0;
+    cudaEventElapsedTime(&t, c.prof_ev[i], c.prof_ev[i + 1]);
+    ms += t;
+  }
+  out3[0] = ms;
+  out3[1] = c.prof_bytes;
+  out3[2] = (double)c.prof_launches;
+  c.prof_used = 0;
+  c.prof_bytes = 0;
+  c.prof_launches = 0;
   return AAO_OK;
 }
 

@@ -118,6 +118,12 @@ struct Ctx {
   bool timing = false;
   cudaEvent_t ev[5] = {};
   double phase_ms[4] = {0, 0, 0, 0};
+  // live timing of the dominant kernel class (finest-level multicolour SOR sweeps)
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;   // pairs (start, end)
+  size_t prof_used = 0;
+  double prof_bytes = 0;
+  long prof_launches = 0;
 };
 
 // ---- kernel launchers (kernels_*.cu) --------------------------------------
