@@ -244,7 +244,7 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": "k_gs<2,2> finest-level multicolour SOR sweep (velocity MG)",
+    roofline = {"bound": "hbm", "kernel": "k_mg_cta<2,2>: CTA-resident velocity multigrid solve (4 V-cycles, all levels)" if os.environ.get("AAO_MG_MODE", "0") != "1" else "k_gs<2,2> finest-level multicolour SOR sweeps",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "fallback (B200_PROFILING.md)",
                 "traffic": traffic, "algorithmic_bytes_per_launch": sm_bytes / max(sm_launches, 1),

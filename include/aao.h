@@ -147,11 +147,14 @@ aao_status aao_debug_freq_block(aao_ctx* ctx, int k, double* out, void* stream);
 aao_status aao_set_timing(aao_ctx* ctx, int on);
 aao_status aao_last_phase_ms(aao_ctx* ctx, double* ms4);
 
-/* Live timing of the dominant kernel class, the finest-level multicolour SOR sweeps of the
-   velocity multigrid (CUDA events on the launching stream around each run of sweeps).
+/* Live timing of the dominant kernel class -- the velocity multigrid: in the default CTA-resident
+   mode the k_mg_cta solve launches, in the per-level mode (env AAO_MG_MODE=1) the finest-level
+   multicolour SOR sweeps -- with CUDA events on the launching stream around each launch (run).
    aao_profile_smoother(ctx, 1) resets and enables; aao_profile_read synchronises and returns
-   out3 = {milliseconds, algorithmic bytes (48 B per unknown per sweep: x and b read, x written,
-   complex128), number of kernel launches} accumulated since, then resets. */
+   out3 = {milliseconds, algorithmic bytes, number of kernel launches} accumulated since, then
+   resets.  Algorithmic bytes: a sweep reads x, b and writes x once per unknown (48 B, complex128);
+   a whole MG solve adds residual (48), restriction (16 + 16/coarse unknown), prolongation (32 +
+   16/coarse unknown) per level and V-cycle and the coarsest solve (32) -- DESIGN.md "Roofline". */
 aao_status aao_profile_smoother(aao_ctx* ctx, int on);
 aao_status aao_profile_read(aao_ctx* ctx, double* out3);
 

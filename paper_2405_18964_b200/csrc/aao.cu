@@ -4,6 +4,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <chrono>
 #include <stdexcept>
@@ -659,9 +660,12 @@ void setup(Ctx& c, const aao_config& cfg) {
     for (int l = 0; l < nlev; ++l) {
       const long n = S.grids[l].n * (long)np;
       S.r[l] = dalloc<double2>(c, n);
+      CK(cudaMemset(S.r[l], 0, n * sizeof(double2)));
       if (l > 0) {
         S.x[l] = dalloc<double2>(c, n);
         S.b[l] = dalloc<double2>(c, n);
+        CK(cudaMemset(S.x[l], 0, n * sizeof(double2)));
+        CK(cudaMemset(S.b[l], 0, n * sizeof(double2)));
       }
     }
   }
@@ -680,12 +684,13 @@ void setup(Ctx& c, const aao_config& cfg) {
 // ------------------------------------------------------------------ block solvers
 inline View contig(double2* p, long n) { return View{p, 1, n}; }
 
-// brackets a run of finest-level smoother launches with events when profiling is on
+// brackets a run of launches of the dominant kernel class with events when profiling is on
 struct SweepTimer {
   Ctx& c;
   bool on;
   cudaStream_t s;
-  SweepTimer(Ctx& c_, bool fine, cudaStream_t s_, const Grid& g, int nprob, int sweeps) : c(c_), on(c_.prof && fine && sweeps > 0), s(s_) {
+  SweepTimer(Ctx& c_, bool active, cudaStream_t s_, double bytes, long launches)
+      : c(c_), on(c_.prof && active), s(s_) {
     if (!on) return;
     if (c.prof_used + 2 > c.prof_ev.size()) {
       for (int i = 0; i < 64; ++i) {
@@ -695,13 +700,8 @@ struct SweepTimer {
       }
     }
     cudaEventRecord(c.prof_ev[c.prof_used], s);
-    // algorithmic bytes of one sweep: read x, b and write x once per unknown (complex128)
-    long unknowns = 1;
-    for (int a = 0; a < g.dim; ++a) unknowns *= (g.order == 2 ? g.n1 - 2 : g.n1);
-    if (g.order == 1) unknowns -= 1;
-    const int C = g.order == 2 ? (g.dim == 2 ? 9 : 27) : (g.dim == 2 ? 4 : 8);
-    c.prof_bytes += 48.0 * unknowns * nprob * sweeps;
-    c.prof_launches += (long)C * sweeps;
+    c.prof_bytes += bytes;
+    c.prof_launches += launches;
   }
   ~SweepTimer() {
     if (!on) return;
@@ -709,6 +709,29 @@ struct SweepTimer {
     c.prof_used += 2;
   }
 };
+
+long unknowns(const Grid& g) {
+  long u = 1;
+  for (int a = 0; a < g.dim; ++a) u *= (g.order == 2 ? g.n1 - 2 : g.n1);
+  return g.order == 1 ? u - 1 : u;
+}
+
+// algorithmic bytes of `sweeps` multicolour SOR sweeps on one level: x, b read and x written once per
+// unknown (complex128)
+double sweep_bytes(const Grid& g, int nprob, int sweeps) { return 48.0 * unknowns(g) * nprob * sweeps; }
+
+// algorithmic bytes of one MG solve (all cycles): per level and V-cycle, sweeps 48 B/unknown each,
+// residual 48, restriction 16 (+16 per coarse unknown), prolongation + correction 32 (+16 per coarse
+// unknown), coarsest solve 32 (~1579 B per fine unknown in 2-D)
+double mg_bytes(const Ctx& c, const MGSpace& S, int nprob) {
+  double b = 0;
+  for (int l = 0; l + 1 < S.nlev; ++l) {
+    const double u = unknowns(S.grids[l]), uc = unknowns(S.grids[l + 1]);
+    b += u * (48.0 * (c.cfg.pre_sweeps + c.cfg.post_sweeps) + 48 + 16 + 32) + uc * 32.0;
+  }
+  b += 32.0 * unknowns(S.grids[S.nlev - 1]);
+  return b * c.cfg.mg_cycles * nprob;
+}
 
 void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, int inv_pg, View x, View b, int nprob,
                cudaStream_t s) {
@@ -721,7 +744,8 @@ void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, i
   }
   const int C = S.order == 2 ? (c.dim == 2 ? 9 : 27) : (c.dim == 2 ? 4 : 8);
   {
-    SweepTimer tm(c, l == 0 && S.order == 2, s, g, nprob, c.cfg.pre_sweeps);
+    SweepTimer tm(c, l == 0 && S.order == 2, s, sweep_bytes(g, nprob, c.cfg.pre_sweeps),
+                  (long)C * c.cfg.pre_sweeps);
     for (int sw = 0; sw < c.cfg.pre_sweeps; ++sw)
       for (int col = 0; col < C; ++col) {
         launch_gs(g, op, x, b, nprob, col, c.cfg.omega, s);
@@ -738,7 +762,8 @@ void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, i
   mg_vcycle(c, S, l + 1, op, inv, inv_pg, xc, bc, nprob, s);
   launch_prolong(g, gc, S.transfers[l], xc, x, nprob, s);
   ++cnt;
-  SweepTimer tm(c, l == 0 && S.order == 2, s, g, nprob, c.cfg.post_sweeps);
+  SweepTimer tm(c, l == 0 && S.order == 2, s, sweep_bytes(g, nprob, c.cfg.post_sweeps),
+                (long)C * c.cfg.post_sweeps);
   for (int sw = 0; sw < c.cfg.post_sweeps; ++sw)
     for (int col = C - 1; col >= 0; --col) {
       launch_gs(g, op, x, b, nprob, col, c.cfg.omega, s);
@@ -749,6 +774,46 @@ void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, i
 // x = MG(A; b): mg_cycles V-cycles from x = 0
 void mg_solve(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, int inv_pg, View x, View b, int nprob,
               cudaStream_t s) {
+  if (c.mg_mode == 0) {
+    MGArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.nlev = S.nlev;
+    a.cycles = c.cfg.mg_cycles;
+    a.pre = c.cfg.pre_sweeps;
+    a.post = c.cfg.post_sweeps;
+    a.omega = c.cfg.omega;
+    for (int l = 0; l < S.nlev; ++l) {
+      a.g[l] = S.grids[l];
+      a.t[l] = S.transfers[l];
+      a.xw[l] = S.x[l];
+      a.bw[l] = S.b[l];
+      a.rw[l] = S.r[l];
+    }
+    a.x0 = x;
+    a.b0 = b;
+    a.op = op;
+    a.inv = inv;
+    a.inv_pg = inv_pg;
+    a.unk = S.coarse_unk;
+    a.nu = S.ncoarse_unk;
+    // shared-memory residency: coarsest levels first while x and b fit in the budget
+    const char* bud = std::getenv("AAO_SMEM_BUDGET");
+    const size_t budget = bud ? (size_t)std::atol(bud) : 200 * 1024;
+    size_t used = 0;
+    a.lsm = S.nlev;
+    for (int l = S.nlev - 1; l >= 1; --l) {
+      const size_t need = 2 * S.grids[l].n * sizeof(double2);
+      if (used + need > budget) break;
+      a.sm_x[l] = (long)(used / sizeof(double2));
+      a.sm_b[l] = (long)(used / sizeof(double2)) + S.grids[l].n;
+      used += need;
+      a.lsm = l;
+    }
+    SweepTimer tm(c, S.order == 2, s, mg_bytes(c, S, nprob), 1);
+    launch_mg_cta(a, nprob, used, s);
+    ++launch_counter();
+    return;
+  }
   launch_zero(x, S.grids[0].n, nprob, s);
   ++launch_counter();
   for (int cyc = 0; cyc < c.cfg.mg_cycles; ++cyc) mg_vcycle(c, S, 0, op, inv, inv_pg, x, b, nprob, s);
@@ -759,6 +824,11 @@ void cheb_solve(Ctx& c, const Grid& g, View b, View x, int nprob, double scale, 
   const double lo1 = 0.5, hi1 = g.order == 2 ? 1.25 : 1.5;
   const double lo = std::pow(lo1, c.dim), hi = std::pow(hi1, c.dim);
   const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+  if (c.mg_mode == 0) {
+    launch_cheb_cta(g, b, x, c.Cr, c.Cd0, c.Cd1, theta, sigma, delta, c.cfg.cheb_iters, scale, nprob, s);
+    ++launch_counter();
+    return;
+  }
   View r = contig(c.Cr, g.n), d0 = contig(c.Cd0, g.n), d1 = contig(c.Cd1, g.n);
   launch_cheb_init(g, b, x, r, d0, 1.0 / theta, nprob, s);
   double rho = 1.0 / sigma;
@@ -778,12 +848,19 @@ void precond_stokes(Ctx& c, cudaStream_t s) {
   const Grid& gp = c.pres.grids[0];
   // x1 = MG(W; s1), x2 = MG(W; s2) per velocity component
   OpSel opW{c.coefW, 2 * dim, 0};
+  // pressure slots on the side stream (independent of the velocity slots): K_p^{-1} by MG and
+  // M_p^{-1} by Chebyshev, combined in the inverse transform
+  static const bool one_stream = std::getenv("AAO_ONE_STREAM") != nullptr;
+  cudaStream_t sp = one_stream ? s : c.s2;
+  cudaEventRecord(c.ev_fork, s);
+  cudaStreamWaitEvent(sp, c.ev_fork, 0);
+  OpSel opKp{c.coefKp, 1 << 30, 0};
+  mg_solve(c, c.pres, opKp, c.invKp, 1 << 30, contig(c.XpA, gp.n), contig(c.Fp, gp.n), 2 * n_f, sp);
+  cheb_solve(c, gp, contig(c.Fp, gp.n), contig(c.XpB, gp.n), 2 * n_f, 1.0, sp);
+  cudaEventRecord(c.ev_join, sp);
   mg_solve(c, c.vel, opW, c.invW, 2 * dim, contig(c.Xv, gv.n), contig(c.Fv, gv.n), n_f * 2 * dim, s);
   if (c.timing) cudaEventRecord(c.ev[2], s);
-  // pressure slots: K_p^{-1} by MG and M_p^{-1} by Chebyshev, combined in the inverse transform
-  OpSel opKp{c.coefKp, 1 << 30, 0};
-  mg_solve(c, c.pres, opKp, c.invKp, 1 << 30, contig(c.XpA, gp.n), contig(c.Fp, gp.n), 2 * n_f, s);
-  cheb_solve(c, gp, contig(c.Fp, gp.n), contig(c.XpB, gp.n), 2 * n_f, 1.0, s);
+  cudaStreamWaitEvent(s, c.ev_join, 0);
 }
 
 void precond_oseen(Ctx& c, cudaStream_t s) {
@@ -1065,8 +1142,13 @@ aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
     return AAO_ERR_CONFIG;
   aao_ctx* ctx = new aao_ctx();
   try {
+    const char* mm = std::getenv("AAO_MG_MODE");
+    ctx->c.mg_mode = (mm && mm[0] == '1') ? 1 : 0;
     aao::setup(ctx->c, *cfg);
     for (auto& e : ctx->c.ev) cudaEventCreate(&e);
+    cudaStreamCreateWithFlags(&ctx->c.s2, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ctx->c.ev_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->c.ev_join, cudaEventDisableTiming);
   } catch (const CudaError& e) {
     std::fprintf(stderr, "aao_create: %s\n", e.what());
     aao_status st = e.st;
@@ -1084,6 +1166,9 @@ void aao_destroy(aao_ctx* ctx) {
   for (auto& e : ctx->c.ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->c.prof_ev) cudaEventDestroy(e);
+  if (ctx->c.s2) cudaStreamDestroy(ctx->c.s2);
+  if (ctx->c.ev_fork) cudaEventDestroy(ctx->c.ev_fork);
+  if (ctx->c.ev_join) cudaEventDestroy(ctx->c.ev_join);
   delete ctx;
 }
 

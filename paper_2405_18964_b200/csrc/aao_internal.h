@@ -56,12 +56,24 @@ struct FreqConst {
   double dr, dc;       // Re d_k, Im d_k
 };
 
-struct MGLevel {       // device storage of one level of one space in a batch workspace
-  Grid g;
-  Transfer tr;         // to the next coarser level (unused on the coarsest)
-  double2* x;          // [nprob_max][n] (level 0: supplied by the caller)
-  double2* b;
-  double2* r;
+// Arguments of the CTA-resident multigrid solve (one CTA per problem, all levels and cycles).
+constexpr int MG_MAXL = 12;
+struct MGArgs {
+  int nlev, cycles, pre, post;
+  double omega;
+  Grid g[MG_MAXL];
+  Transfer t[MG_MAXL];
+  double2* xw[MG_MAXL];   // levels >= 1: [nprob][n_l]
+  double2* bw[MG_MAXL];
+  double2* rw[MG_MAXL];   // all levels: [nprob][n_l]
+  View x0, b0;            // finest level solution / right-hand side
+  OpSel op;
+  const double2* inv;     // coarsest-level dense inverses [groups][nu][nu]
+  int inv_pg;
+  const int* unk;
+  int nu;
+  int lsm;                // levels >= lsm keep x and b in shared memory (offsets below, in double2)
+  long sm_x[MG_MAXL], sm_b[MG_MAXL];
 };
 
 struct MGSpace {       // an MG hierarchy for one space, with batch workspace
@@ -119,6 +131,9 @@ struct Ctx {
   cudaEvent_t ev[5] = {};
   double phase_ms[4] = {0, 0, 0, 0};
   // live timing of the dominant kernel class (finest-level multicolour SOR sweeps)
+  cudaStream_t s2 = nullptr;               // side stream: pressure solves overlap the velocity MG
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int mg_mode = 0;       // 0: CTA-resident solves (default), 1: one launch per level / colour (AAO_MG_MODE=1)
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;   // pairs (start, end)
   size_t prof_used = 0;
@@ -147,6 +162,9 @@ void launch_lincomb(const Grid& g, View out, double cb, View b, const OpSel& A1,
                     const OpSel& A2, View x2, int nprob, cudaStream_t s);
 // y = a*y + bcoef*x  (pointwise, masked entries stay 0)
 void launch_axpby(const Grid& g, View y, double2 a, View x, double2 bcoef, int nprob, cudaStream_t s);
+void launch_mg_cta(const MGArgs& a, int nprob, size_t smem, cudaStream_t s);
+void launch_cheb_cta(const Grid& g, View b, View x, double2* r, double2* d0, double2* d1, double theta, double sigma,
+                     double delta, int iters, double scale, int nprob, cudaStream_t s);
 // pressure: out = sb*bp + sB * sum_c B_c v_c (v: d components per problem group)
 void launch_Bv(const Grid& g2, const Grid& g1, const double* tPm, const double* tGm, View v, View bp,
                View out, double sb, double sB, int nprob, cudaStream_t s);

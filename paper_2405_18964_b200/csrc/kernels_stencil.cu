@@ -12,6 +12,10 @@
 
 namespace aao {
 
+#ifndef MG_THREADS
+#define MG_THREADS 512
+#endif
+
 // ---------------------------------------------------------------- complex helpers
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -33,9 +37,17 @@ __device__ __forceinline__ long voff(const View& v, int p, long n) {
 
 template <int DIM>
 __device__ __forceinline__ void coords(long idx, int n1, int* c) {
-  c[0] = (int)(idx % n1);
-  c[1] = (int)((idx / n1) % n1);
-  if (DIM == 3) c[2] = (int)(idx / ((long)n1 * n1));
+  // per-problem node indices fit in 32 bits (n1^3 < 2^31 for every supported grid)
+  const unsigned u = (unsigned)idx, un = (unsigned)n1;
+  const unsigned q = u / un;
+  c[0] = (int)(u - q * un);
+  if (DIM == 2) {
+    c[1] = (int)q;
+  } else {
+    const unsigned q2 = q / un;
+    c[1] = (int)(q - q2 * un);
+    c[2] = (int)q2;
+  }
 }
 
 template <int DIM, int ORD>
@@ -50,72 +62,66 @@ __device__ __forceinline__ bool masked(const int* c, long idx, int n1) {
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // Mx = (M x)_i, Kx = (K x)_i, Cx = (C x)_i at one node; dM, dK, dC = diagonal entries.
+// Only the x-direction 1-D rows are held in registers; y/z rows are read per offset (L1 hits).
 template <int DIM, int ORD, bool CONV>
 __device__ __forceinline__ void apply_MKC(const Grid& g, const double* __restrict__ cv,
-                                          const double2* __restrict__ x, const int* c, long idx,
+                                          const double2* x, const int* c, long idx,
                                           double2& Mx, double2& Kx, double2& Cx, double& dM, double& dK,
                                           double& dC) {
   constexpr int W = 2 * ORD + 1;
-  double m[DIM][W], k[DIM][W];
+  double mx[W], kx[W];
 #pragma unroll
-  for (int a = 0; a < DIM; ++a)
-#pragma unroll
-    for (int o = 0; o < W; ++o) {
-      m[a][o] = __ldg(g.tM + c[a] * W + o);
-      k[a][o] = __ldg(g.tK + c[a] * W + o);
-    }
+  for (int o = 0; o < W; ++o) {
+    mx[o] = __ldg(g.tM + c[0] * W + o);
+    kx[o] = __ldg(g.tK + c[0] * W + o);
+  }
   const int n1 = g.n1;
   Mx = Kx = Cx = make_double2(0.0, 0.0);
   const double* cvr = CONV ? cv + idx * (DIM == 2 ? W * W : W * W * W) : nullptr;
-  if constexpr (DIM == 2) {
+  const int nz = DIM == 3 ? W : 1;
+  double mzc = 1.0, kzc = 0.0;  // z-row diagonal (3-D)
+  double myc = 0.0, kyc = 0.0;  // y-row diagonal
+#pragma unroll 1
+  for (int oc = 0; oc < nz; ++oc) {
+    double mz = 1.0, kz = 0.0;
+    int zoff = 0;
+    if (DIM == 3) {
+      mz = __ldg(g.tM + c[2] * W + oc);
+      kz = __ldg(g.tK + c[2] * W + oc);
+      if (oc == ORD) {
+        mzc = mz;
+        kzc = kz;
+      }
+      zoff = clampi(c[2] + oc - ORD, 0, n1 - 1) * n1 * n1;
+    }
 #pragma unroll
     for (int ob = 0; ob < W; ++ob) {
-      const int jj = clampi(c[1] + ob - ORD, 0, n1 - 1);
+      const double my = __ldg(g.tM + c[1] * W + ob);
+      const double ky = __ldg(g.tK + c[1] * W + ob);
+      if (ob == ORD) {
+        myc = my;
+        kyc = ky;
+      }
+      const double mzy = mz * my;
+      const double kzy = kz * my + mz * ky;
+      const int row = zoff + clampi(c[1] + ob - ORD, 0, n1 - 1) * n1;
 #pragma unroll
       for (int oa = 0; oa < W; ++oa) {
-        const int ii = clampi(c[0] + oa - ORD, 0, n1 - 1);
-        const double2 v = __ldg(x + (long)jj * n1 + ii);
-        const double mm = m[1][ob] * m[0][oa];
-        const double kk = k[1][ob] * m[0][oa] + m[1][ob] * k[0][oa];
-        Mx = cfma(mm, v, Mx);
-        Kx = cfma(kk, v, Kx);
-        if (CONV) Cx = cfma(__ldg(cvr + ob * W + oa), v, Cx);
+        const double2 v = x[row + clampi(c[0] + oa - ORD, 0, n1 - 1)];
+        Mx = cfma(mzy * mx[oa], v, Mx);
+        Kx = cfma(kzy * mx[oa] + mzy * kx[oa], v, Kx);
+        if (CONV) Cx = cfma(__ldg(cvr + (oc * W + ob) * W + oa), v, Cx);
       }
     }
-    dM = m[1][ORD] * m[0][ORD];
-    dK = k[1][ORD] * m[0][ORD] + m[1][ORD] * k[0][ORD];
-    dC = CONV ? __ldg(cvr + ORD * W + ORD) : 0.0;
-  } else {
-#pragma unroll 1
-    for (int oc = 0; oc < W; ++oc) {
-      const int kk3 = clampi(c[2] + oc - ORD, 0, n1 - 1);
-#pragma unroll
-      for (int ob = 0; ob < W; ++ob) {
-        const int jj = clampi(c[1] + ob - ORD, 0, n1 - 1);
-        const double mzy = m[2][oc] * m[1][ob];
-        const double kzy = k[2][oc] * m[1][ob] + m[2][oc] * k[1][ob];
-#pragma unroll
-        for (int oa = 0; oa < W; ++oa) {
-          const int ii = clampi(c[0] + oa - ORD, 0, n1 - 1);
-          const double2 v = __ldg(x + ((long)kk3 * n1 + jj) * n1 + ii);
-          const double mm = mzy * m[0][oa];
-          const double kk = kzy * m[0][oa] + mzy * k[0][oa];
-          Mx = cfma(mm, v, Mx);
-          Kx = cfma(kk, v, Kx);
-          if (CONV) Cx = cfma(__ldg(cvr + (oc * W + ob) * W + oa), v, Cx);
-        }
-      }
-    }
-    dM = m[2][ORD] * m[1][ORD] * m[0][ORD];
-    dK = k[2][ORD] * m[1][ORD] * m[0][ORD] + m[2][ORD] * k[1][ORD] * m[0][ORD] +
-         m[2][ORD] * m[1][ORD] * k[0][ORD];
-    dC = CONV ? __ldg(cvr + (ORD * W + ORD) * W + ORD) : 0.0;
   }
+  dM = mzc * myc * mx[ORD];
+  dK = kzc * myc * mx[ORD] + mzc * kyc * mx[ORD] + mzc * myc * kx[ORD];
+  dC = CONV ? __ldg(cvr + (DIM == 3 ? (ORD * W + ORD) * W + ORD : ORD * W + ORD)) : 0.0;
 }
 
 // (A x)_i and A_ii for A = a M + b K + c C
 template <int DIM, int ORD>
-__device__ __forceinline__ void apply_op(const Grid& g, const OpSel& op, int p, const double2* __restrict__ x,
+__device__ __forceinline__ void apply_op(const Grid& g, const OpSel& op, int p, const double2* x,
                                          const int* c, long idx, double2& Ax, double2& D) {
   const Coef cf = op.coef[p / op.per_group];
   double2 Mx, Kx, Cx;
@@ -125,6 +131,28 @@ __device__ __forceinline__ void apply_op(const Grid& g, const OpSel& op, int p, 
   } else {
     apply_MKC<DIM, ORD, true>(g, op.conv_sel == 1 ? g.conv : g.convT, x, c, idx, Mx, Kx, Cx, dM, dK, dC);
   }
+  Ax = cadd(cadd(cmul(cf.a, Mx), cmul(cf.b, Kx)), cmul(cf.c, Cx));
+  D = cadd(cadd(cscale(dM, cf.a), cscale(dK, cf.b)), cscale(dC, cf.c));
+}
+
+// real-coefficient operator without convection (Stokes W_k, K_p): A = a M + b K, a, b real
+template <int DIM, int ORD>
+__device__ __forceinline__ void apply_op_real(const Grid& g, double ca, double cb, const double2* x, const int* c,
+                                              long idx, double2& Ax, double& D) {
+  double2 Mx, Kx, Cx;
+  double dM, dK, dC;
+  apply_MKC<DIM, ORD, false>(g, nullptr, x, c, idx, Mx, Kx, Cx, dM, dK, dC);
+  Ax = make_double2(ca * Mx.x + cb * Kx.x, ca * Mx.y + cb * Kx.y);
+  D = ca * dM + cb * dK;
+}
+
+// complex coefficients with convection (Oseen Q_k, Q_k^H): A = a M + b K + c C
+template <int DIM, int ORD>
+__device__ __forceinline__ void apply_op_conv(const Grid& g, const Coef& cf, const double* cv, const double2* x,
+                                              const int* c, long idx, double2& Ax, double2& D) {
+  double2 Mx, Kx, Cx;
+  double dM, dK, dC;
+  apply_MKC<DIM, ORD, true>(g, cv, x, c, idx, Mx, Kx, Cx, dM, dK, dC);
   Ax = cadd(cadd(cmul(cf.a, Mx), cmul(cf.b, Kx)), cmul(cf.c, Cx));
   D = cadd(cadd(cscale(dM, cf.a), cscale(dK, cf.b)), cscale(dC, cf.c));
 }
@@ -480,6 +508,273 @@ __global__ void k_Bv(Grid g2, Grid g1, const double* __restrict__ tPm, const dou
   out[idx] = res;
 }
 
+// ---------------------------------------------------------------- CTA-resident solvers
+// One CTA owns one problem (one frequency / slot / component) and runs the WHOLE fixed-count
+// solve -- every level, colour, transfer and V-cycle -- with block barriers only.  The problems
+// of a batch are independent, so the batch supplies the parallelism and no grid-wide
+// synchronisation is ever needed; the iterate stays L1/L2-resident between colour steps.
+template <int DIM, int ORD>
+__device__ __forceinline__ long colour_count(int n1, int colour, int* res, int* cnt) {
+  constexpr int C1 = ORD == 2 ? 3 : 2;
+  long total = 1;
+  int cc = colour;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    res[a] = cc % C1;
+    cc /= C1;
+    cnt[a] = (n1 - res[a] + C1 - 1) / C1;
+    total *= cnt[a];
+  }
+  return total;
+}
+
+template <int DIM, int ORD, bool CONV>
+__device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
+                                          const double2* b, int sweeps, bool reverse, double omega) {
+  constexpr int C1 = ORD == 2 ? 3 : 2;
+  constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int cc = 0; cc < NC; ++cc) {
+      const int colour = reverse ? NC - 1 - cc : cc;
+      int res[DIM], cnt[DIM];
+      const long total = colour_count<DIM, ORD>(g.n1, colour, res, cnt);
+      for (int t0 = threadIdx.x; t0 < (int)total; t0 += blockDim.x) {
+        int c[DIM];
+        const unsigned q = (unsigned)t0 / (unsigned)cnt[0];
+        c[0] = res[0] + C1 * (int)((unsigned)t0 - q * (unsigned)cnt[0]);
+        if (DIM == 2) {
+          c[1] = res[1] + C1 * (int)q;
+        } else {
+          const unsigned q2 = q / (unsigned)cnt[1];
+          c[1] = res[1] + C1 * (int)(q - q2 * (unsigned)cnt[1]);
+          c[2] = res[2] + C1 * (int)q2;
+        }
+        const int idx = DIM == 2 ? c[1] * g.n1 + c[0] : (c[2] * g.n1 + c[1]) * g.n1 + c[0];
+        if (masked<DIM, ORD>(c, idx, g.n1)) continue;
+        if (CONV) {
+          double2 Ax, D;
+          apply_op_conv<DIM, ORD>(g, cf, cv, x, c, idx, Ax, D);
+          x[idx] = cadd(x[idx], cscale(omega, cdiv(csub(b[idx], Ax), D)));
+        } else {
+          double2 Ax;
+          double D;
+          apply_op_real<DIM, ORD>(g, cf.a.x, cf.b.x, x, c, idx, Ax, D);
+          const double2 r = csub(b[idx], Ax);
+          x[idx] = cadd(x[idx], cscale(omega / D, r));
+        }
+      }
+      __syncthreads();
+    }
+}
+
+template <int DIM, int ORD, bool CONV>
+__global__ void __launch_bounds__(MG_THREADS, 1) k_mg_cta(MGArgs a) {
+  extern __shared__ double2 smem[];
+  constexpr int R = ORD == 2 ? 3 : 1;
+  constexpr int WR = 2 * R + 1;
+  constexpr int NW = ORD == 2 ? 3 : 2;
+  const int p = blockIdx.x;
+  const int L = a.nlev;
+  // level pointers of this problem; coarse levels that fit live in shared memory (generic pointers)
+  auto X = [&](int l) -> double2* {
+    if (l == 0) return a.x0.p + voff(a.x0, p, a.g[0].n);
+    return l >= a.lsm ? smem + a.sm_x[l] : a.xw[l] + (long)p * a.g[l].n;
+  };
+  auto B = [&](int l) -> double2* {
+    if (l == 0) return a.b0.p + voff(a.b0, p, a.g[0].n);
+    return l >= a.lsm ? smem + a.sm_b[l] : a.bw[l] + (long)p * a.g[l].n;
+  };
+  auto Rr = [&](int l) -> double2* { return a.rw[l] + (long)p * a.g[l].n; };
+  const Coef cf = a.op.coef[p / a.op.per_group];
+  auto CV = [&](int l) -> const double* { return a.op.conv_sel == 1 ? a.g[l].conv : a.g[l].convT; };
+  for (int i = threadIdx.x; i < (int)a.g[0].n; i += blockDim.x) X(0)[i] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int cyc = 0; cyc < a.cycles; ++cyc) {
+    // ---- down: smooth, residual, restrict
+    for (int l = 0; l < L - 1; ++l) {
+      const Grid g = a.g[l];
+      if (l > 0) {
+        for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) X(l)[i] = make_double2(0.0, 0.0);
+        __syncthreads();
+      }
+      cta_sweep<DIM, ORD, CONV>(g, cf, CV(l), X(l), B(l), a.pre, false, a.omega);
+      for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) {
+        int c[DIM];
+        coords<DIM>(i, g.n1, c);
+        if (masked<DIM, ORD>(c, i, g.n1)) {
+          Rr(l)[i] = make_double2(0.0, 0.0);
+          continue;
+        }
+        double2 Ax;
+        if (CONV) {
+          double2 D;
+          apply_op_conv<DIM, ORD>(g, cf, CV(l), X(l), c, i, Ax, D);
+        } else {
+          double D;
+          apply_op_real<DIM, ORD>(g, cf.a.x, cf.b.x, X(l), c, i, Ax, D);
+        }
+        Rr(l)[i] = csub(B(l)[i], Ax);
+      }
+      __syncthreads();
+      const Grid gc = a.g[l + 1];
+      const Transfer t = a.t[l];
+      const int o7 = ORD == 2 ? 0 : 2;
+      for (int I = threadIdx.x; I < (int)gc.n; I += blockDim.x) {
+        int c[DIM];
+        coords<DIM>(I, gc.n1, c);
+        if (masked<DIM, ORD>(c, I, gc.n1)) {
+          B(l + 1)[I] = make_double2(0.0, 0.0);
+          continue;
+        }
+        double w[DIM][WR];
+#pragma unroll
+        for (int d = 0; d < DIM; ++d)
+#pragma unroll
+          for (int o = 0; o < WR; ++o) w[d][o] = __ldg(t.tR + c[d] * 7 + o7 + o);
+        double2 acc = make_double2(0.0, 0.0);
+        const int n1 = g.n1;
+        if constexpr (DIM == 2) {
+          for (int ob = 0; ob < WR; ++ob) {
+            if (w[1][ob] == 0.0) continue;
+            const int jj = 2 * c[1] + ob - R;
+            for (int oa = 0; oa < WR; ++oa) {
+              if (w[0][oa] == 0.0) continue;
+              acc = cfma(w[1][ob] * w[0][oa], Rr(l)[jj * n1 + 2 * c[0] + oa - R], acc);
+            }
+          }
+        } else {
+          for (int oc = 0; oc < WR; ++oc) {
+            if (w[2][oc] == 0.0) continue;
+            const int kk = 2 * c[2] + oc - R;
+            for (int ob = 0; ob < WR; ++ob) {
+              if (w[1][ob] == 0.0) continue;
+              const int jj = 2 * c[1] + ob - R;
+              for (int oa = 0; oa < WR; ++oa) {
+                if (w[0][oa] == 0.0) continue;
+                acc = cfma(w[2][oc] * w[1][ob] * w[0][oa], Rr(l)[(kk * n1 + jj) * n1 + 2 * c[0] + oa - R], acc);
+              }
+            }
+          }
+        }
+        B(l + 1)[I] = acc;
+      }
+      __syncthreads();
+    }
+    // ---- coarsest level: dense inverse
+    {
+      // masked (boundary / pinned) entries of the coarsest iterate must read as 0 in the prolongation
+      for (int i = threadIdx.x; i < (int)a.g[L - 1].n; i += blockDim.x) X(L - 1)[i] = make_double2(0.0, 0.0);
+      __syncthreads();
+      const double2* A = a.inv + (long)(p / a.inv_pg) * a.nu * a.nu;
+      for (int i = threadIdx.x; i < a.nu; i += blockDim.x) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int j = 0; j < a.nu; ++j) acc = cadd(acc, cmul(A[(long)i * a.nu + j], B(L - 1)[a.unk[j]]));
+        X(L - 1)[a.unk[i]] = acc;
+      }
+      __syncthreads();
+    }
+    // ---- up: prolongate + correct, smooth
+    for (int l = L - 2; l >= 0; --l) {
+      const Grid g = a.g[l];
+      const Grid gc = a.g[l + 1];
+      const Transfer t = a.t[l];
+      for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) {
+        int c[DIM];
+        coords<DIM>(i, g.n1, c);
+        if (masked<DIM, ORD>(c, i, g.n1)) continue;
+        int base[DIM];
+        double w[DIM][NW];
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          base[d] = (int)__ldg(t.tP + c[d] * 4);
+#pragma unroll
+          for (int o = 0; o < NW; ++o) w[d][o] = __ldg(t.tP + c[d] * 4 + 1 + o);
+        }
+        const int n1 = gc.n1;
+        const double2* xc = X(l + 1);
+        double2 acc = make_double2(0.0, 0.0);
+        if constexpr (DIM == 2) {
+#pragma unroll
+          for (int ob = 0; ob < NW; ++ob)
+#pragma unroll
+            for (int oa = 0; oa < NW; ++oa) {
+              const double ww = w[1][ob] * w[0][oa];
+              if (ww != 0.0) acc = cfma(ww, xc[(base[1] + ob) * n1 + base[0] + oa], acc);
+            }
+        } else {
+#pragma unroll
+          for (int oc = 0; oc < NW; ++oc)
+#pragma unroll
+            for (int ob = 0; ob < NW; ++ob)
+#pragma unroll
+              for (int oa = 0; oa < NW; ++oa) {
+                const double ww = w[2][oc] * w[1][ob] * w[0][oa];
+                if (ww != 0.0)
+                  acc = cfma(ww, xc[((base[2] + oc) * n1 + base[1] + ob) * n1 + base[0] + oa], acc);
+              }
+        }
+        X(l)[i] = cadd(X(l)[i], acc);
+      }
+      __syncthreads();
+      cta_sweep<DIM, ORD, CONV>(g, cf, CV(l), X(l), B(l), a.post, true, a.omega);
+    }
+  }
+}
+
+// Chebyshev semi-iteration on a mass matrix, one CTA per problem
+template <int DIM, int ORD>
+__global__ void __launch_bounds__(MG_THREADS, 1) k_cheb_cta(Grid g, View bv, View xv, double2* rw, double2* d0w, double2* d1w,
+                                                   double theta, double sigma, double delta, int iters, double scale) {
+  const int p = blockIdx.x;
+  const double2* b = bv.p + voff(bv, p, g.n);
+  double2* x = xv.p + voff(xv, p, g.n);
+  double2* r = rw + (long)p * g.n;
+  double2* d0 = d0w + (long)p * g.n;
+  double2* d1 = d1w + (long)p * g.n;
+  const double2 z = make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) {
+    int c[DIM];
+    coords<DIM>(i, g.n1, c);
+    x[i] = z;
+    if (masked<DIM, ORD>(c, i, g.n1)) {
+      r[i] = z;
+      d0[i] = z;
+    } else {
+      const double2 bb = b[i];
+      r[i] = bb;
+      d0[i] = cscale(1.0 / theta, cscale(1.0 / mass_diag<DIM, ORD>(g, c), bb));
+    }
+  }
+  __syncthreads();
+  double rho = 1.0 / sigma;
+  for (int k = 0; k < iters - 1; ++k) {
+    const double rho1 = 1.0 / (2.0 * sigma - rho);
+    const double c1 = rho1 * rho, c2 = 2.0 * rho1 / delta;
+    for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) {
+      int c[DIM];
+      coords<DIM>(i, g.n1, c);
+      if (masked<DIM, ORD>(c, i, g.n1)) {
+        d1[i] = z;
+        continue;
+      }
+      double2 Mx, Kx, Cx;
+      double dM, dK, dC;
+      apply_MKC<DIM, ORD, false>(g, nullptr, d0, c, i, Mx, Kx, Cx, dM, dK, dC);
+      const double2 d = d0[i];
+      x[i] = cadd(x[i], d);
+      const double2 rr = csub(r[i], Mx);
+      r[i] = rr;
+      d1[i] = cadd(cscale(c1, d), cscale(c2, cscale(1.0 / dM, rr)));
+    }
+    __syncthreads();
+    double2* tmp = d0;
+    d0 = d1;
+    d1 = tmp;
+    rho = rho1;
+  }
+  for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) x[i] = cscale(scale, cadd(x[i], d0[i]));
+}
+
 // ---------------------------------------------------------------- launchers
 static inline dim3 grid1(long n, int nprob, int bs) { return dim3((unsigned)((n + bs - 1) / bs), nprob); }
 constexpr int BS = 128;
@@ -589,6 +884,33 @@ static void ax_t(const Grid& g, View y, double2 a, View x, double2 bc, int nprob
 }
 void launch_axpby(const Grid& g, View y, double2 a, View x, double2 bcoef, int nprob, cudaStream_t s) {
   SWITCH_DO(g, ax_t, g, y, a, x, bcoef, nprob, s);
+}
+
+template <int DIM, int ORD>
+static void mgcta_t(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mg_cta<DIM, ORD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_mg_cta<DIM, ORD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  if (a.op.conv_sel == 0)
+    k_mg_cta<DIM, ORD, false><<<nprob, MG_THREADS, smem, s>>>(a);
+  else
+    k_mg_cta<DIM, ORD, true><<<nprob, MG_THREADS, smem, s>>>(a);
+}
+void launch_mg_cta(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
+  SWITCH_DO(a.g[0], mgcta_t, a, nprob, smem, s);
+}
+
+template <int DIM, int ORD>
+static void chcta_t(const Grid& g, View b, View x, double2* r, double2* d0, double2* d1, double theta, double sigma,
+                    double delta, int iters, double scale, int nprob, cudaStream_t s) {
+  k_cheb_cta<DIM, ORD><<<nprob, MG_THREADS, 0, s>>>(g, b, x, r, d0, d1, theta, sigma, delta, iters, scale);
+}
+void launch_cheb_cta(const Grid& g, View b, View x, double2* r, double2* d0, double2* d1, double theta, double sigma,
+                     double delta, int iters, double scale, int nprob, cudaStream_t s) {
+  SWITCH_DO(g, chcta_t, g, b, x, r, d0, d1, theta, sigma, delta, iters, scale, nprob, s);
 }
 
 void launch_Bv(const Grid& g2, const Grid& g1, const double* tPm, const double* tGm, View v, View bp, View out,

@@ -208,3 +208,15 @@ def test_full_size_frequency_sampled_parity(name):
         blk = ctx.debug_freq_block(k)
         for h in range(2):
             assert rel(blk[h], prob_block(cfg, Y[h], Q[h])) <= PRECOND_TOL
+
+
+@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[3], SMALL[5]], ids=lambda c: c.name)
+def test_per_level_launch_mode_matches_oracle(cfg, monkeypatch):
+    """The per-level / per-colour launch schedule (AAO_MG_MODE=1) computes the same map."""
+    torch = _torch()
+    monkeypatch.setenv("AAO_MG_MODE", "1")
+    _, pc = oracle_for(cfg)
+    ctx = gpu_ctx(cfg)
+    r = synth.probe_vector(cfg)
+    z = ctx.precond_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert rel(z, pc.apply(r)) <= PRECOND_TOL
