@@ -733,10 +733,17 @@ double mg_bytes(const Ctx& c, const MGSpace& S, int nprob) {
   return b * c.cfg.mg_cycles * nprob;
 }
 
+void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double2* inv, int inv_pg, View x, View b,
+                       int nprob, int cycles, cudaStream_t s);
+
 void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, int inv_pg, View x, View b, int nprob,
                cudaStream_t s) {
   const Grid& g = S.grids[l];
   auto& cnt = launch_counter();
+  if (c.tail > 0 && l == c.tail) {   // one V-cycle from zero on levels >= l, CTA-resident
+    launch_cta_levels(c, S, l, op, inv, inv_pg, x, b, nprob, 1, s);
+    return;
+  }
   if (l == S.nlev - 1) {
     launch_coarse(g, inv, inv_pg, S.coarse_unk, S.ncoarse_unk, b, x, nprob, s);
     ++cnt;
@@ -744,7 +751,7 @@ void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, i
   }
   const int C = S.order == 2 ? (c.dim == 2 ? 9 : 27) : (c.dim == 2 ? 4 : 8);
   {
-    SweepTimer tm(c, l == 0 && S.order == 2, s, sweep_bytes(g, nprob, c.cfg.pre_sweeps),
+    SweepTimer tm(c, false && l == 0 && S.order == 2, s, sweep_bytes(g, nprob, c.cfg.pre_sweeps),
                   (long)C * c.cfg.pre_sweeps);
     for (int sw = 0; sw < c.cfg.pre_sweeps; ++sw)
       for (int col = 0; col < C; ++col) {
@@ -762,7 +769,7 @@ void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, i
   mg_vcycle(c, S, l + 1, op, inv, inv_pg, xc, bc, nprob, s);
   launch_prolong(g, gc, S.transfers[l], xc, x, nprob, s);
   ++cnt;
-  SweepTimer tm(c, l == 0 && S.order == 2, s, sweep_bytes(g, nprob, c.cfg.post_sweeps),
+  SweepTimer tm(c, false && l == 0 && S.order == 2, s, sweep_bytes(g, nprob, c.cfg.post_sweeps),
                 (long)C * c.cfg.post_sweeps);
   for (int sw = 0; sw < c.cfg.post_sweeps; ++sw)
     for (int col = C - 1; col >= 0; --col) {
@@ -771,49 +778,133 @@ void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, i
     }
 }
 
+// CTA-resident solve over levels [l0, nlev): `cycles` V-cycles from x = 0 at level l0.
+void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double2* inv, int inv_pg, View x, View b,
+                       int nprob, int cycles, cudaStream_t s) {
+  MGArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.nlev = S.nlev - l0;
+  a.cycles = cycles;
+  a.pre = c.cfg.pre_sweeps;
+  a.post = c.cfg.post_sweeps;
+  a.omega = c.cfg.omega;
+  for (int i = 0; i < a.nlev; ++i) {
+    a.g[i] = S.grids[l0 + i];
+    a.t[i] = S.transfers[l0 + i];
+    a.xw[i] = S.x[l0 + i];
+    a.bw[i] = S.b[l0 + i];
+    a.rw[i] = S.r[l0 + i];
+  }
+  a.x0 = x;
+  a.b0 = b;
+  a.op = op;
+  a.inv = inv;
+  a.inv_pg = inv_pg;
+  a.unk = S.coarse_unk;
+  a.nu = S.ncoarse_unk;
+  // shared-memory residency: coarsest levels first while x and b fit in the budget
+  static const char* bud = std::getenv("AAO_SMEM_BUDGET");
+  // measured (tools/smem_sweep.sh): keeping only the smallest levels in shared memory leaves the L1
+  // to the finest level, which matters more (c2 3.02 vs 3.17 ms, c3 277 vs 437 ms)
+  const size_t budget = bud ? (size_t)std::atol(bud) : 20 * 1024;
+  size_t used = 0;
+  a.lsm = a.nlev;
+  for (int l = a.nlev - 1; l >= 1; --l) {
+    const size_t need = 2 * a.g[l].n * sizeof(double2);
+    if (used + need > budget) break;
+    a.sm_x[l] = (long)(used / sizeof(double2));
+    a.sm_b[l] = (long)(used / sizeof(double2)) + a.g[l].n;
+    used += need;
+    a.lsm = l;
+  }
+  launch_mg_cta(a, nprob, used, s);
+  ++launch_counter();
+}
+
+// schedule: 0 = whole solve CTA-resident, 1 = one launch per level / colour, 2 = hybrid (launches on the
+// levels whose x and b do not fit in shared memory, CTA-resident tail below); -1 = automatic
+int tail_level(const Ctx& c, const MGSpace& S, int mode) {
+  if (mode == 1) return -1;
+  if (mode == 0) return 0;
+  for (int l = 1; l < S.nlev; ++l)
+    if (2 * S.grids[l].n * sizeof(double2) <= 200 * 1024) return l;
+  return S.nlev - 1;
+}
+
+int choose_mode(const Ctx& c, const MGSpace& S) {
+  if (c.mg_mode >= 0) return c.mg_mode;
+  // measured (tools/modes_bench.sh): the CTA-resident schedule is fastest or on par for every config
+  // (c2 3.0 ms vs 4.1 hybrid; c3 277 vs 286; c4_64 60 vs 57-70; c5 254 vs 296)
+  (void)S;
+  return 0;
+}
+
+// real-split CTA-resident solve for real operators; returns false if it does not apply
+bool launch_real_split(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, int inv_pg, View x, View b,
+                       int nprob, cudaStream_t s, bool force) {
+  if (op.conv_sel != 0) return false;
+  MGRealArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.nlev = S.nlev;
+  a.cycles = c.cfg.mg_cycles;
+  a.pre = c.cfg.pre_sweeps;
+  a.post = c.cfg.post_sweeps;
+  a.omega = c.cfg.omega;
+  const size_t budget = 232448 - 2048;
+  size_t used = 0;
+  for (int l = 0; l < S.nlev; ++l) {
+    a.g[l] = S.grids[l];
+    a.t[l] = S.transfers[l];
+    a.xw[l] = l == 0 ? reinterpret_cast<double*>(S.r[0]) + (long)S.grids[0].n * nprob
+                     : reinterpret_cast<double*>(S.x[l]);
+    a.bw[l] = reinterpret_cast<double*>(S.b[l]);
+    a.rw[l] = reinterpret_cast<double*>(S.r[l]);
+    a.xsm[l] = a.bsm[l] = -1;
+  }
+  // finest iterate first, then coarse x, b from the coarsest level up
+  const size_t n0 = S.grids[0].n * sizeof(double);
+  if (n0 <= budget) {
+    a.xsm[0] = 0;
+    used = n0;
+  } else if (!force) {
+    return false;
+  }
+  for (int l = S.nlev - 1; l >= 1; --l) {
+    const size_t need = 2 * S.grids[l].n * sizeof(double);
+    if (used + need > budget) break;
+    a.xsm[l] = (long)(used / sizeof(double));
+    a.bsm[l] = a.xsm[l] + S.grids[l].n;
+    used += need;
+  }
+  a.x0 = x;
+  a.b0 = b;
+  a.op = op;
+  a.inv = inv;
+  a.inv_pg = inv_pg;
+  a.unk = S.coarse_unk;
+  a.nu = S.ncoarse_unk;
+  launch_mg_real(a, nprob, used, s);
+  ++launch_counter();
+  return true;
+}
+
 // x = MG(A; b): mg_cycles V-cycles from x = 0
 void mg_solve(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, int inv_pg, View x, View b, int nprob,
               cudaStream_t s) {
-  if (c.mg_mode == 0) {
-    MGArgs a;
-    std::memset(&a, 0, sizeof(a));
-    a.nlev = S.nlev;
-    a.cycles = c.cfg.mg_cycles;
-    a.pre = c.cfg.pre_sweeps;
-    a.post = c.cfg.post_sweeps;
-    a.omega = c.cfg.omega;
-    for (int l = 0; l < S.nlev; ++l) {
-      a.g[l] = S.grids[l];
-      a.t[l] = S.transfers[l];
-      a.xw[l] = S.x[l];
-      a.bw[l] = S.b[l];
-      a.rw[l] = S.r[l];
-    }
-    a.x0 = x;
-    a.b0 = b;
-    a.op = op;
-    a.inv = inv;
-    a.inv_pg = inv_pg;
-    a.unk = S.coarse_unk;
-    a.nu = S.ncoarse_unk;
-    // shared-memory residency: coarsest levels first while x and b fit in the budget
-    const char* bud = std::getenv("AAO_SMEM_BUDGET");
-    const size_t budget = bud ? (size_t)std::atol(bud) : 200 * 1024;
-    size_t used = 0;
-    a.lsm = S.nlev;
-    for (int l = S.nlev - 1; l >= 1; --l) {
-      const size_t need = 2 * S.grids[l].n * sizeof(double2);
-      if (used + need > budget) break;
-      a.sm_x[l] = (long)(used / sizeof(double2));
-      a.sm_b[l] = (long)(used / sizeof(double2)) + S.grids[l].n;
-      used += need;
-      a.lsm = l;
-    }
+  const bool fits = S.grids[0].n * sizeof(double) <= 232448 - 2048;
+  if (op.conv_sel == 0 && (c.mg_mode == 3 || (c.mg_mode < 0 && fits && c.real_split_auto))) {
     SweepTimer tm(c, S.order == 2, s, mg_bytes(c, S, nprob), 1);
-    launch_mg_cta(a, nprob, used, s);
-    ++launch_counter();
+    launch_real_split(c, S, op, inv, inv_pg, x, b, nprob, s, true);
     return;
   }
+  const int mode = choose_mode(c, S);
+  if (mode == 0) {
+    SweepTimer tm(c, S.order == 2, s, mg_bytes(c, S, nprob), 1);
+    launch_cta_levels(c, S, 0, op, inv, inv_pg, x, b, nprob, c.cfg.mg_cycles, s);
+    return;
+  }
+  c.tail = tail_level(c, S, mode);
+  SweepTimer tm(c, S.order == 2, s, mg_bytes(c, S, nprob), 0);
   launch_zero(x, S.grids[0].n, nprob, s);
   ++launch_counter();
   for (int cyc = 0; cyc < c.cfg.mg_cycles; ++cyc) mg_vcycle(c, S, 0, op, inv, inv_pg, x, b, nprob, s);
@@ -824,7 +915,7 @@ void cheb_solve(Ctx& c, const Grid& g, View b, View x, int nprob, double scale, 
   const double lo1 = 0.5, hi1 = g.order == 2 ? 1.25 : 1.5;
   const double lo = std::pow(lo1, c.dim), hi = std::pow(hi1, c.dim);
   const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
-  if (c.mg_mode == 0) {
+  if (c.mg_mode != 1) {
     launch_cheb_cta(g, b, x, c.Cr, c.Cd0, c.Cd1, theta, sigma, delta, c.cfg.cheb_iters, scale, nprob, s);
     ++launch_counter();
     return;
@@ -946,7 +1037,7 @@ void gmres_alloc(Ctx& c, int m) {
   c.gu = dalloc<double>(c, N);
   c.gr = dalloc<double>(c, N);
   c.gH = dalloc<double>(c, (size_t)(m + 2) * (m + 1));
-  c.gpart = dalloc<double>(c, dot_blocks());
+  c.gpart = dalloc<double>(c, std::max((long)dot_blocks(), (long)(m + 3) * mgs_blocks()));
   c.gscal = dalloc<double>(c, 4 * (m + 2));
   std::vector<double*> ptr(m + 1);
   for (int i = 0; i <= m; ++i) ptr[i] = c.gV + (size_t)i * N;
@@ -1002,15 +1093,10 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
       precond_apply(c, Vk, c.gz, s);
       kkt_apply(c, c.gz, w, s);
       inf.precond_applies++;
-      // modified Gram-Schmidt with device-resident coefficients
+      // modified Gram-Schmidt, device-resident coefficients, one cooperative launch
       double* hcol = c.gH + (size_t)k * (m + 1);
-      for (int i = 0; i <= k; ++i) {
-        launch_dot(w, c.gV + (size_t)i * N, N, c.gpart, dot_blocks(), hcol + i, 0, s);
-        launch_axpy_dev(w, c.gV + (size_t)i * N, hcol + i, -1.0, N, s);
-        launch_counter() += 3;
-      }
-      launch_dot(w, w, N, c.gpart, dot_blocks(), hcol + k + 1, 1, s);
-      launch_counter() += 2;
+      CK(launch_mgs(w, (const double* const*)c.gVptr, k, N, hcol, c.gpart, s));
+      ++launch_counter();
       CK(cudaMemcpyAsync(c.hostH, hcol, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       for (int i = 0; i <= k + 1; ++i) H[(size_t)i * m + k] = c.hostH[i];
@@ -1143,7 +1229,8 @@ aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
   aao_ctx* ctx = new aao_ctx();
   try {
     const char* mm = std::getenv("AAO_MG_MODE");
-    ctx->c.mg_mode = (mm && mm[0] == '1') ? 1 : 0;
+    ctx->c.mg_mode = mm ? std::atoi(mm) : -1;
+    ctx->c.real_split_auto = std::getenv("AAO_REAL_SPLIT") != nullptr;
     aao::setup(ctx->c, *cfg);
     for (auto& e : ctx->c.ev) cudaEventCreate(&e);
     cudaStreamCreateWithFlags(&ctx->c.s2, cudaStreamNonBlocking);

@@ -133,7 +133,9 @@ struct Ctx {
   // live timing of the dominant kernel class (finest-level multicolour SOR sweeps)
   cudaStream_t s2 = nullptr;               // side stream: pressure solves overlap the velocity MG
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  int mg_mode = 0;       // 0: CTA-resident solves (default), 1: one launch per level / colour (AAO_MG_MODE=1)
+  int mg_mode = -1;      // MG schedule: -1 auto, 0 CTA-resident, 1 per level/colour launches, 2 hybrid (AAO_MG_MODE)
+  int tail = -1;
+  bool real_split_auto = false;   // real-split MG in auto mode (AAO_REAL_SPLIT); measured slower on c2         // hybrid: first CTA-resident level of the current solve
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;   // pairs (start, end)
   size_t prof_used = 0;
@@ -163,6 +165,25 @@ void launch_lincomb(const Grid& g, View out, double cb, View b, const OpSel& A1,
 // y = a*y + bcoef*x  (pointwise, masked entries stay 0)
 void launch_axpby(const Grid& g, View y, double2 a, View x, double2 bcoef, int nprob, cudaStream_t s);
 void launch_mg_cta(const MGArgs& a, int nprob, size_t smem, cudaStream_t s);
+
+// real-split CTA-resident MG for real operators (no convection): real / imaginary parts in turn
+struct MGRealArgs {
+  int nlev, cycles, pre, post;
+  double omega;
+  Grid g[MG_MAXL];
+  Transfer t[MG_MAXL];
+  double* xw[MG_MAXL];    // global real scratch [nprob][n_l] (levels not in shared memory)
+  double* bw[MG_MAXL];
+  double* rw[MG_MAXL];
+  long xsm[MG_MAXL], bsm[MG_MAXL];   // shared-memory offsets in doubles, -1 = global
+  View x0, b0;            // complex finest-level solution / right-hand side
+  OpSel op;               // real parts of coef a, b are used
+  const double2* inv;
+  int inv_pg;
+  const int* unk;
+  int nu;
+};
+void launch_mg_real(const MGRealArgs& a, int nprob, size_t smem, cudaStream_t s);
 void launch_cheb_cta(const Grid& g, View b, View x, double2* r, double2* d0, double2* d1, double theta, double sigma,
                      double delta, int iters, double scale, int nprob, cudaStream_t s);
 // pressure: out = sb*bp + sB * sum_c B_c v_c (v: d components per problem group)
@@ -186,5 +207,8 @@ void launch_axpy(double* y, const double* x, double alpha, long n, cudaStream_t 
 void launch_copy_sub(double* y, const double* b, const double* ax, long n, cudaStream_t s);  // y = b - ax
 void launch_multi_axpy(double* u, const double* const* V, const double* coef, int k, long n, cudaStream_t s);
 int dot_blocks();
+int mgs_blocks();
+// whole MGS sweep (dots, updates, norm) in one cooperative launch; partial: [(k+2) * mgs_blocks()]
+cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double* H, double* partial, cudaStream_t s);
 
 }  // namespace aao

@@ -1,7 +1,11 @@
 // GMRES vector kernels (step A1): deterministic two-stage reductions with warp
 // shuffles (fixed grid, fixed order -> bitwise reproducible), device-scalar axpys
 // so Gram-Schmidt coefficients never round-trip through the host.
+#include <cooperative_groups.h>
+
 #include "aao_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace aao {
 
@@ -100,6 +104,86 @@ __global__ void k_multi_axpy(double* __restrict__ u, const double* const* __rest
 }
 void launch_multi_axpy(double* u, const double* const* V, const double* coef, int k, long n, cudaStream_t s) {
   k_multi_axpy<<<DOT_BLOCKS, 256, 0, s>>>(u, V, coef, k, n);
+}
+
+// Modified Gram-Schmidt of w against V_0..V_k in ONE cooperative launch (step A1):
+//   h_i = <w, V_i>; w -= h_i V_i  (i = 0..k, sequentially, as MGS requires);  h_{k+1} = ||w||.
+// Each block owns a fixed contiguous chunk; the dot for step i+1 is fused into the update pass of
+// step i, so every step costs one pass over the chunk and one grid barrier.  Block partials are
+// reduced in a fixed order by every block (deterministic, bitwise reproducible).
+constexpr int MGS_THREADS = 512;
+
+__global__ void __launch_bounds__(MGS_THREADS) k_mgs(double* __restrict__ w, const double* const* __restrict__ V,
+                                                     int k, long n, double* __restrict__ H,
+                                                     double* __restrict__ partial) {
+  cg::grid_group grid = cg::this_grid();
+  const int nb = gridDim.x;
+  const long chunk = (n + nb - 1) / nb;
+  const long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  __shared__ double hs;
+  // dot for step 0
+  double acc = 0.0;
+  const double* v0 = V[0];
+  for (long j = lo + threadIdx.x; j < hi; j += blockDim.x) acc = fma(w[j], v0[j], acc);
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+  grid.sync();
+  for (int i = 0; i <= k; ++i) {
+    if (threadIdx.x < 32) {
+      double s = 0.0;
+      for (int b = threadIdx.x; b < nb; b += 32) s += partial[(long)i * nb + b];
+      s = warp_sum(s);
+      if (threadIdx.x == 0) {
+        hs = s;
+        if (blockIdx.x == 0) H[i] = s;
+      }
+    }
+    __syncthreads();
+    const double h = hs;
+    const double* vi = V[i];
+    const double* vn = i < k ? V[i + 1] : nullptr;
+    double a2 = 0.0;
+    if (vn) {
+      for (long j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+        const double wj = fma(-h, vi[j], w[j]);
+        w[j] = wj;
+        a2 = fma(wj, vn[j], a2);
+      }
+    } else {
+      for (long j = lo + threadIdx.x; j < hi; j += blockDim.x) {
+        const double wj = fma(-h, vi[j], w[j]);
+        w[j] = wj;
+        a2 = fma(wj, wj, a2);
+      }
+    }
+    a2 = block_sum(a2);
+    if (threadIdx.x == 0) partial[(long)(i + 1) * nb + blockIdx.x] = a2;
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nb; b += 32) s += partial[(long)(k + 1) * nb + b];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) H[k + 1] = sqrt(s);
+  }
+}
+
+int mgs_blocks() {
+  static int nb = 0;
+  if (nb == 0) {
+    int dev, sms, per;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mgs, MGS_THREADS, 0);
+    nb = sms * (per < 2 ? per : 2);
+  }
+  return nb;
+}
+
+cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double* H, double* partial, cudaStream_t s) {
+  int nb = mgs_blocks();
+  void* args[] = {&w, (void*)&V, &k, &n, &H, &partial};
+  return cudaLaunchCooperativeKernel((void*)k_mgs, dim3(nb), dim3(MGS_THREADS), args, 0, s);
 }
 
 }  // namespace aao

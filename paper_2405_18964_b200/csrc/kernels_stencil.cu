@@ -62,9 +62,9 @@ __device__ __forceinline__ bool masked(const int* c, long idx, int n1) {
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // Mx = (M x)_i, Kx = (K x)_i, Cx = (C x)_i at one node; dM, dK, dC = diagonal entries.
-// Only the x-direction 1-D rows are held in registers; y/z rows are read per offset (L1 hits).
+// Generic version (clamped taps): used for the Q1 pressure space.
 template <int DIM, int ORD, bool CONV>
-__device__ __forceinline__ void apply_MKC(const Grid& g, const double* __restrict__ cv,
+__device__ __forceinline__ void apply_MKC_generic(const Grid& g, const double* __restrict__ cv,
                                           const double2* x, const int* c, long idx,
                                           double2& Mx, double2& Kx, double2& Cx, double& dM, double& dK,
                                           double& dC) {
@@ -117,6 +117,96 @@ __device__ __forceinline__ void apply_MKC(const Grid& g, const double* __restric
   dM = mzc * myc * mx[ORD];
   dK = kzc * myc * mx[ORD] + mzc * kyc * mx[ORD] + mzc * myc * kx[ORD];
   dC = CONV ? __ldg(cvr + (DIM == 3 ? (ORD * W + ORD) * W + ORD : ORD * W + ORD)) : 0.0;
+}
+
+// Q2 specialisation.  A Q2 node with an odd index along an axis is an element midpoint and
+// couples only to offsets -1..1 along that axis; even (vertex) nodes couple to -2..2.  Taking the
+// parity as a template argument gives 16 taps on average in 2-D (64 in 3-D) instead of 25 (125),
+// and no tap of an interior node ever leaves the grid, so no clamping is needed.  The Kronecker
+// coefficients are applied row by row (sum factorisation): per row rm = sum mx v, rk = sum kx v.
+template <int DIM, bool CONV, int PY, int PZ>
+__device__ __forceinline__ void q2_MKC(const Grid& g, const double* __restrict__ cv, const double2* x, const int* c,
+                                       int idx, double2& Mx, double2& Kx, double2& Cx, double& dM, double& dK,
+                                       double& dC) {
+  constexpr int AY0 = PY ? 1 : 0, AY1 = PY ? 4 : 5;
+  constexpr int AZ0 = DIM == 3 ? (PZ ? 1 : 0) : 2, AZ1 = DIM == 3 ? (PZ ? 4 : 5) : 3;
+  const int n1 = g.n1;
+  double mx[5], kx[5];
+#pragma unroll
+  for (int oa = 0; oa < 5; ++oa) {
+    mx[oa] = __ldg(g.tM + c[0] * 5 + oa);   // zero outside the element support (odd nodes: oa = 0, 4)
+    kx[oa] = __ldg(g.tK + c[0] * 5 + oa);
+  }
+  // the two outer x-taps may leave the grid next to the boundary (with zero coefficient): clamp them
+  const int xl = c[0] >= 2 ? c[0] - 2 : c[0], xr = c[0] + 2 <= n1 - 1 ? c[0] + 2 : c[0];
+  Mx = Kx = Cx = make_double2(0.0, 0.0);
+  const double* cvr = CONV ? cv + (long)idx * (DIM == 2 ? 25 : 125) : nullptr;
+  double mzc = 1.0, kzc = 0.0, myc = 0.0, kyc = 0.0;
+#pragma unroll
+  for (int oc = AZ0; oc < AZ1; ++oc) {
+    double mz = 1.0, kz = 0.0;
+    int zrow = 0;
+    if (DIM == 3) {
+      mz = __ldg(g.tM + c[2] * 5 + oc);
+      kz = __ldg(g.tK + c[2] * 5 + oc);
+      zrow = (c[2] + oc - 2) * n1;
+      if (oc == 2) {
+        mzc = mz;
+        kzc = kz;
+      }
+    }
+#pragma unroll
+    for (int ob = AY0; ob < AY1; ++ob) {
+      const double my = __ldg(g.tM + c[1] * 5 + ob);
+      const double ky = __ldg(g.tK + c[1] * 5 + ob);
+      if (ob == 2) {
+        myc = my;
+        kyc = ky;
+      }
+      const double2* row = x + (zrow + c[1] + ob - 2) * n1;
+      double2 rm = make_double2(0.0, 0.0), rk = rm;
+#pragma unroll
+      for (int oa = 0; oa < 5; ++oa) {
+        const int col = oa == 0 ? xl : (oa == 4 ? xr : c[0] + oa - 2);
+        const double2 v = row[col];
+        rm = cfma(mx[oa], v, rm);
+        rk = cfma(kx[oa], v, rk);
+        if (CONV) Cx = cfma(__ldg(cvr + ((DIM == 3 ? oc * 5 : 0) + ob) * 5 + oa), v, Cx);
+      }
+      const double mzy = mz * my, kzy = kz * my + mz * ky;
+      Mx = cfma(mzy, rm, Mx);
+      Kx = cfma(kzy, rm, cfma(mzy, rk, Kx));
+    }
+  }
+  dM = mzc * myc * mx[2];
+  dK = kzc * myc * mx[2] + mzc * kyc * mx[2] + mzc * myc * kx[2];
+  dC = CONV ? __ldg(cvr + (DIM == 3 ? 62 : 12)) : 0.0;
+}
+
+template <int DIM, bool CONV>
+__device__ __forceinline__ void q2_dispatch(const Grid& g, const double* __restrict__ cv, const double2* x,
+                                            const int* c, int idx, double2& Mx, double2& Kx, double2& Cx, double& dM,
+                                            double& dK, double& dC) {
+  const int cls = (c[1] & 1) | (DIM == 3 ? ((c[2] & 1) << 1) : 0);
+#define Q2C(b, cc) q2_MKC<DIM, CONV, b, cc>(g, cv, x, c, idx, Mx, Kx, Cx, dM, dK, dC)
+  switch (cls) {
+    case 0: Q2C(0, 0); break;
+    case 1: Q2C(1, 0); break;
+    case 2: if (DIM == 3) Q2C(0, 1); break;
+    default: if (DIM == 3) Q2C(1, 1); break;
+  }
+#undef Q2C
+}
+
+template <int DIM, int ORD, bool CONV>
+__device__ __forceinline__ void apply_MKC(const Grid& g, const double* __restrict__ cv, const double2* x,
+                                          const int* c, long idx, double2& Mx, double2& Kx, double2& Cx, double& dM,
+                                          double& dK, double& dC) {
+  if constexpr (ORD == 2) {
+    q2_dispatch<DIM, CONV>(g, cv, x, c, (int)idx, Mx, Kx, Cx, dM, dK, dC);
+  } else {
+    apply_MKC_generic<DIM, ORD, CONV>(g, cv, x, c, idx, Mx, Kx, Cx, dM, dK, dC);
+  }
 }
 
 // (A x)_i and A_ii for A = a M + b K + c C
@@ -528,6 +618,82 @@ __device__ __forceinline__ long colour_count(int n1, int colour, int* res, int* 
   return total;
 }
 
+// node update of one multicolour SOR step: x_i += omega (b_i - (A x)_i) / A_ii
+template <int DIM, int ORD, bool CONV>
+__device__ __forceinline__ void sor_node(const Grid& g, const Coef& cf, const double* cv, double2* x, const double2* b,
+                                         const int* c, int idx, double omega) {
+  if (CONV) {
+    double2 Ax, D;
+    apply_op_conv<DIM, ORD>(g, cf, cv, x, c, idx, Ax, D);
+    x[idx] = cadd(x[idx], cscale(omega, cdiv(csub(b[idx], Ax), D)));
+  } else {
+    double2 Ax;
+    double D;
+    apply_op_real<DIM, ORD>(g, cf.a.x, cf.b.x, x, c, idx, Ax, D);
+    x[idx] = cadd(x[idx], cscale(omega / D, csub(b[idx], Ax)));
+  }
+}
+
+// Visit the unknown nodes with per-axis start s[a] and stride st[a] (interior range [lo, hi]),
+// distributing them over the CTA's threads.
+template <int DIM, class F>
+__device__ __forceinline__ void cta_visit(int n1, const int* s0, const int* sta, int lo, int hi, F&& f) {
+  int cnt[DIM], start[DIM], stv[DIM];
+  int total = 1;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    int s = s0[a];
+    while (s < lo) s += sta[a];
+    start[a] = s;
+    stv[a] = sta[a];
+    cnt[a] = s > hi ? 0 : (hi - s) / sta[a] + 1;
+    total *= cnt[a];
+  }
+  if (total == 0) return;
+  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    int c[DIM];
+    const unsigned q = (unsigned)t / (unsigned)cnt[0];
+    c[0] = start[0] + stv[0] * (int)((unsigned)t - q * (unsigned)cnt[0]);
+    if (DIM == 2) {
+      c[1] = start[1] + stv[1] * (int)q;
+    } else {
+      const unsigned q2 = q / (unsigned)cnt[1];
+      c[1] = start[1] + stv[1] * (int)(q - q2 * (unsigned)cnt[1]);
+      c[2] = start[2] + stv[2] * (int)q2;
+    }
+    const int idx = DIM == 2 ? c[1] * n1 + c[0] : (c[2] * n1 + c[1]) * n1 + c[0];
+    f(c, idx);
+  }
+}
+
+// all unknowns of a level: Q2 in parity classes (uniform taps per warp), Q1 in one pass
+template <int DIM, int ORD, class F>
+__device__ __forceinline__ void cta_all_unknowns(int n1, F&& f) {
+  if (ORD == 2) {
+    for (int cls = 0; cls < (1 << (DIM - 1)); ++cls) {
+      int s0[DIM], st[DIM];
+      s0[0] = 1;
+      st[0] = 1;
+#pragma unroll
+      for (int a = 1; a < DIM; ++a) {
+        s0[a] = ((cls >> (a - 1)) & 1) ? 1 : 2;
+        st[a] = 2;
+      }
+      cta_visit<DIM>(n1, s0, st, 1, n1 - 2, f);
+    }
+  } else {
+    int s0[DIM], st[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+      s0[a] = 0;
+      st[a] = 1;
+    }
+    cta_visit<DIM>(n1, s0, st, 0, n1 - 1, [&](const int* c, int idx) {
+      if (idx != 0) f(c, idx);  // pinned node
+    });
+  }
+}
+
 template <int DIM, int ORD, bool CONV>
 __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
                                           const double2* b, int sweeps, bool reverse, double omega) {
@@ -536,32 +702,35 @@ __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const d
   for (int sw = 0; sw < sweeps; ++sw)
     for (int cc = 0; cc < NC; ++cc) {
       const int colour = reverse ? NC - 1 - cc : cc;
-      int res[DIM], cnt[DIM];
-      const long total = colour_count<DIM, ORD>(g.n1, colour, res, cnt);
-      for (int t0 = threadIdx.x; t0 < (int)total; t0 += blockDim.x) {
-        int c[DIM];
-        const unsigned q = (unsigned)t0 / (unsigned)cnt[0];
-        c[0] = res[0] + C1 * (int)((unsigned)t0 - q * (unsigned)cnt[0]);
-        if (DIM == 2) {
-          c[1] = res[1] + C1 * (int)q;
-        } else {
-          const unsigned q2 = q / (unsigned)cnt[1];
-          c[1] = res[1] + C1 * (int)(q - q2 * (unsigned)cnt[1]);
-          c[2] = res[2] + C1 * (int)q2;
+      int res[DIM];
+      int col = colour;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        res[a] = col % C1;
+        col /= C1;
+      }
+      auto upd = [&](const int* c, int idx) { sor_node<DIM, ORD, CONV>(g, cf, cv, x, b, c, idx, omega); };
+      if (ORD == 2) {
+        // colour residue r: x nodes r + 3m (coalesced); y/z in parity classes r + 3p + 6m so that
+        // the row taps are warp-uniform
+        for (int cls = 0; cls < (1 << (DIM - 1)); ++cls) {
+          int s0[DIM], st[DIM];
+          s0[0] = res[0];
+          st[0] = 3;
+#pragma unroll
+          for (int a = 1; a < DIM; ++a) {
+            s0[a] = res[a] + 3 * ((cls >> (a - 1)) & 1);
+            st[a] = 6;
+          }
+          cta_visit<DIM>(g.n1, s0, st, 1, g.n1 - 2, upd);
         }
-        const int idx = DIM == 2 ? c[1] * g.n1 + c[0] : (c[2] * g.n1 + c[1]) * g.n1 + c[0];
-        if (masked<DIM, ORD>(c, idx, g.n1)) continue;
-        if (CONV) {
-          double2 Ax, D;
-          apply_op_conv<DIM, ORD>(g, cf, cv, x, c, idx, Ax, D);
-          x[idx] = cadd(x[idx], cscale(omega, cdiv(csub(b[idx], Ax), D)));
-        } else {
-          double2 Ax;
-          double D;
-          apply_op_real<DIM, ORD>(g, cf.a.x, cf.b.x, x, c, idx, Ax, D);
-          const double2 r = csub(b[idx], Ax);
-          x[idx] = cadd(x[idx], cscale(omega / D, r));
-        }
+      } else {
+        int st[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) st[a] = 2;
+        cta_visit<DIM>(g.n1, res, st, 0, g.n1 - 1, [&](const int* c, int idx) {
+          if (idx != 0) upd(c, idx);
+        });
       }
       __syncthreads();
     }
@@ -598,22 +767,22 @@ __global__ void __launch_bounds__(MG_THREADS, 1) k_mg_cta(MGArgs a) {
         __syncthreads();
       }
       cta_sweep<DIM, ORD, CONV>(g, cf, CV(l), X(l), B(l), a.pre, false, a.omega);
-      for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) {
-        int c[DIM];
-        coords<DIM>(i, g.n1, c);
-        if (masked<DIM, ORD>(c, i, g.n1)) {
-          Rr(l)[i] = make_double2(0.0, 0.0);
-          continue;
-        }
-        double2 Ax;
-        if (CONV) {
-          double2 D;
-          apply_op_conv<DIM, ORD>(g, cf, CV(l), X(l), c, i, Ax, D);
-        } else {
-          double D;
-          apply_op_real<DIM, ORD>(g, cf.a.x, cf.b.x, X(l), c, i, Ax, D);
-        }
-        Rr(l)[i] = csub(B(l)[i], Ax);
+      {
+        double2* rl = Rr(l);
+        const double2* xl = X(l);
+        const double2* bl = B(l);
+        const double* cvl = CV(l);
+        cta_all_unknowns<DIM, ORD>(g.n1, [&](const int* c, int i) {
+          double2 Ax;
+          if (CONV) {
+            double2 D;
+            apply_op_conv<DIM, ORD>(g, cf, cvl, xl, c, i, Ax, D);
+          } else {
+            double D;
+            apply_op_real<DIM, ORD>(g, cf.a.x, cf.b.x, xl, c, i, Ax, D);
+          }
+          rl[i] = csub(bl[i], Ax);
+        });
       }
       __syncthreads();
       const Grid gc = a.g[l + 1];
@@ -736,6 +905,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) k_cheb_cta(Grid g, View bv, Vie
     int c[DIM];
     coords<DIM>(i, g.n1, c);
     x[i] = z;
+    d1[i] = z;
     if (masked<DIM, ORD>(c, i, g.n1)) {
       r[i] = z;
       d0[i] = z;
@@ -750,22 +920,18 @@ __global__ void __launch_bounds__(MG_THREADS, 1) k_cheb_cta(Grid g, View bv, Vie
   for (int k = 0; k < iters - 1; ++k) {
     const double rho1 = 1.0 / (2.0 * sigma - rho);
     const double c1 = rho1 * rho, c2 = 2.0 * rho1 / delta;
-    for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) {
-      int c[DIM];
-      coords<DIM>(i, g.n1, c);
-      if (masked<DIM, ORD>(c, i, g.n1)) {
-        d1[i] = z;
-        continue;
-      }
+    const double2* dold = d0;
+    double2* dnew = d1;
+    cta_all_unknowns<DIM, ORD>(g.n1, [&](const int* c, int i) {
       double2 Mx, Kx, Cx;
       double dM, dK, dC;
-      apply_MKC<DIM, ORD, false>(g, nullptr, d0, c, i, Mx, Kx, Cx, dM, dK, dC);
-      const double2 d = d0[i];
+      apply_MKC<DIM, ORD, false>(g, nullptr, dold, c, i, Mx, Kx, Cx, dM, dK, dC);
+      const double2 d = dold[i];
       x[i] = cadd(x[i], d);
       const double2 rr = csub(r[i], Mx);
       r[i] = rr;
-      d1[i] = cadd(cscale(c1, d), cscale(c2, cscale(1.0 / dM, rr)));
-    }
+      dnew[i] = cadd(cscale(c1, d), cscale(c2, cscale(1.0 / dM, rr)));
+    });
     __syncthreads();
     double2* tmp = d0;
     d0 = d1;
@@ -773,6 +939,325 @@ __global__ void __launch_bounds__(MG_THREADS, 1) k_cheb_cta(Grid g, View bv, Vie
     rho = rho1;
   }
   for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) x[i] = cscale(scale, cadd(x[i], d0[i]));
+}
+
+// ---------------------------------------------------------------- real-split CTA-resident MG
+// For real operators (Stokes W_k = (1+c1)M + c2 nu K and K_p) the real and imaginary parts of a
+// complex right-hand side are two independent real problems.  Solving them in turn halves every
+// array, so the finest level of c1/c2-sized problems lives in shared memory with all coarse levels:
+// the whole 4-V-cycle solve then touches global memory only for b, the finest residual and the
+// result.  Same arithmetic as k_mg_cta per component.
+template <int DIM, int PY, int PZ>
+__device__ __forceinline__ void q2_MK_real(const Grid& g, const double* x, const int* c, double& Mx, double& Kx,
+                                           double& dM, double& dK) {
+  constexpr int AY0 = PY ? 1 : 0, AY1 = PY ? 4 : 5;
+  constexpr int AZ0 = DIM == 3 ? (PZ ? 1 : 0) : 2, AZ1 = DIM == 3 ? (PZ ? 4 : 5) : 3;
+  const int n1 = g.n1;
+  double mx[5], kx[5];
+#pragma unroll
+  for (int oa = 0; oa < 5; ++oa) {
+    mx[oa] = __ldg(g.tM + c[0] * 5 + oa);
+    kx[oa] = __ldg(g.tK + c[0] * 5 + oa);
+  }
+  const int xl = c[0] >= 2 ? c[0] - 2 : c[0], xr = c[0] + 2 <= n1 - 1 ? c[0] + 2 : c[0];
+  Mx = Kx = 0.0;
+  double mzc = 1.0, kzc = 0.0, myc = 0.0, kyc = 0.0;
+#pragma unroll
+  for (int oc = AZ0; oc < AZ1; ++oc) {
+    double mz = 1.0, kz = 0.0;
+    int zrow = 0;
+    if (DIM == 3) {
+      mz = __ldg(g.tM + c[2] * 5 + oc);
+      kz = __ldg(g.tK + c[2] * 5 + oc);
+      zrow = (c[2] + oc - 2) * n1;
+      if (oc == 2) {
+        mzc = mz;
+        kzc = kz;
+      }
+    }
+#pragma unroll
+    for (int ob = AY0; ob < AY1; ++ob) {
+      const double my = __ldg(g.tM + c[1] * 5 + ob);
+      const double ky = __ldg(g.tK + c[1] * 5 + ob);
+      if (ob == 2) {
+        myc = my;
+        kyc = ky;
+      }
+      const double* row = x + (zrow + c[1] + ob - 2) * n1;
+      double rm = 0.0, rk = 0.0;
+#pragma unroll
+      for (int oa = 0; oa < 5; ++oa) {
+        const double v = row[oa == 0 ? xl : (oa == 4 ? xr : c[0] + oa - 2)];
+        rm = fma(mx[oa], v, rm);
+        rk = fma(kx[oa], v, rk);
+      }
+      const double mzy = mz * my, kzy = kz * my + mz * ky;
+      Mx = fma(mzy, rm, Mx);
+      Kx = fma(kzy, rm, fma(mzy, rk, Kx));
+    }
+  }
+  dM = mzc * myc * mx[2];
+  dK = kzc * myc * mx[2] + mzc * kyc * mx[2] + mzc * myc * kx[2];
+}
+
+template <int DIM>
+__device__ __forceinline__ void q1_MK_real(const Grid& g, const double* x, const int* c, double& Mx, double& Kx,
+                                           double& dM, double& dK) {
+  const int n1 = g.n1;
+  double mx[3], kx[3];
+#pragma unroll
+  for (int o = 0; o < 3; ++o) {
+    mx[o] = __ldg(g.tM + c[0] * 3 + o);
+    kx[o] = __ldg(g.tK + c[0] * 3 + o);
+  }
+  const int xl = c[0] >= 1 ? c[0] - 1 : c[0], xr = c[0] + 1 <= n1 - 1 ? c[0] + 1 : c[0];
+  Mx = Kx = 0.0;
+  double mzc = 1.0, kzc = 0.0, myc = 0.0, kyc = 0.0;
+  const int nz = DIM == 3 ? 3 : 1;
+#pragma unroll
+  for (int oc = 0; oc < nz; ++oc) {
+    double mz = 1.0, kz = 0.0;
+    int zrow = 0;
+    if (DIM == 3) {
+      mz = __ldg(g.tM + c[2] * 3 + oc);
+      kz = __ldg(g.tK + c[2] * 3 + oc);
+      zrow = clampi(c[2] + oc - 1, 0, n1 - 1) * n1;
+      if (oc == 1) {
+        mzc = mz;
+        kzc = kz;
+      }
+    }
+#pragma unroll
+    for (int ob = 0; ob < 3; ++ob) {
+      const double my = __ldg(g.tM + c[1] * 3 + ob);
+      const double ky = __ldg(g.tK + c[1] * 3 + ob);
+      if (ob == 1) {
+        myc = my;
+        kyc = ky;
+      }
+      const double* row = x + (zrow + clampi(c[1] + ob - 1, 0, n1 - 1)) * n1;
+      const double v0 = row[xl], v1 = row[c[0]], v2 = row[xr];
+      const double rm = fma(mx[0], v0, fma(mx[1], v1, mx[2] * v2));
+      const double rk = fma(kx[0], v0, fma(kx[1], v1, kx[2] * v2));
+      const double mzy = mz * my, kzy = kz * my + mz * ky;
+      Mx = fma(mzy, rm, Mx);
+      Kx = fma(kzy, rm, fma(mzy, rk, Kx));
+    }
+  }
+  dM = mzc * myc * mx[1];
+  dK = kzc * myc * mx[1] + mzc * kyc * mx[1] + mzc * myc * kx[1];
+}
+
+// (A x)_i, A_ii for A = a M + b K on a real vector
+template <int DIM, int ORD>
+__device__ __forceinline__ void apply_real(const Grid& g, double ca, double cb, const double* x, const int* c,
+                                           double& Ax, double& D) {
+  double Mx, Kx, dM, dK;
+  if (ORD == 2) {
+    const int cls = (c[1] & 1) | (DIM == 3 ? ((c[2] & 1) << 1) : 0);
+    switch (cls) {
+      case 0: q2_MK_real<DIM, 0, 0>(g, x, c, Mx, Kx, dM, dK); break;
+      case 1: q2_MK_real<DIM, 1, 0>(g, x, c, Mx, Kx, dM, dK); break;
+      case 2: q2_MK_real<DIM, 0, 1>(g, x, c, Mx, Kx, dM, dK); break;
+      default: q2_MK_real<DIM, 1, 1>(g, x, c, Mx, Kx, dM, dK); break;
+    }
+  } else {
+    q1_MK_real<DIM>(g, x, c, Mx, Kx, dM, dK);
+  }
+  Ax = ca * Mx + cb * Kx;
+  D = ca * dM + cb * dK;
+}
+
+template <int DIM, int ORD>
+__device__ __forceinline__ void cta_sweep_real(const Grid& g, double ca, double cb, double* x, const double* b,
+                                               int bs, int sweeps, bool reverse, double omega) {
+  constexpr int C1 = ORD == 2 ? 3 : 2;
+  constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int cc = 0; cc < NC; ++cc) {
+      const int colour = reverse ? NC - 1 - cc : cc;
+      int res[DIM];
+      int col = colour;
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        res[a] = col % C1;
+        col /= C1;
+      }
+      auto upd = [&](const int* c, int idx) {
+        double Ax, D;
+        apply_real<DIM, ORD>(g, ca, cb, x, c, Ax, D);
+        x[idx] += omega * (b[(long)idx * bs] - Ax) / D;
+      };
+      if (ORD == 2) {
+        for (int cls = 0; cls < (1 << (DIM - 1)); ++cls) {
+          int s0[DIM], st[DIM];
+          s0[0] = res[0];
+          st[0] = 3;
+#pragma unroll
+          for (int a = 1; a < DIM; ++a) {
+            s0[a] = res[a] + 3 * ((cls >> (a - 1)) & 1);
+            st[a] = 6;
+          }
+          cta_visit<DIM>(g.n1, s0, st, 1, g.n1 - 2, upd);
+        }
+      } else {
+        int st[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) st[a] = 2;
+        cta_visit<DIM>(g.n1, res, st, 0, g.n1 - 1, [&](const int* c, int idx) {
+          if (idx != 0) upd(c, idx);
+        });
+      }
+      __syncthreads();
+    }
+}
+
+template <int DIM, int ORD>
+__global__ void __launch_bounds__(MG_THREADS, 1) k_mg_real(MGRealArgs a) {
+  extern __shared__ double dsm[];
+  constexpr int R = ORD == 2 ? 3 : 1;
+  constexpr int WR = 2 * R + 1;
+  constexpr int NW = ORD == 2 ? 3 : 2;
+  const int p = blockIdx.x;
+  const int L = a.nlev;
+  const Coef cf = a.op.coef[p / a.op.per_group];
+  const double ca = cf.a.x, cb = cf.b.x;
+  const double* inv = reinterpret_cast<const double*>(a.inv + (long)(p / a.inv_pg) * a.nu * a.nu);  // (re, im) pairs
+  double2* xc0 = a.x0.p + voff(a.x0, p, a.g[0].n);
+  const double2* bc0 = a.b0.p + voff(a.b0, p, a.g[0].n);
+  auto X = [&](int l) -> double* { return a.xsm[l] >= 0 ? dsm + a.xsm[l] : a.xw[l] + (long)p * a.g[l].n; };
+  auto B = [&](int l) -> double* { return a.bsm[l] >= 0 ? dsm + a.bsm[l] : a.bw[l] + (long)p * a.g[l].n; };
+  auto Rr = [&](int l) -> double* { return a.rw[l] + (long)p * a.g[l].n; };
+  for (int part = 0; part < 2; ++part) {
+    const double* b0 = reinterpret_cast<const double*>(bc0) + part;   // stride 2
+    {
+      double* x0 = X(0);
+      for (int i = threadIdx.x; i < (int)a.g[0].n; i += blockDim.x) x0[i] = 0.0;
+    }
+    __syncthreads();
+    for (int cyc = 0; cyc < a.cycles; ++cyc) {
+      for (int l = 0; l < L - 1; ++l) {
+        const Grid g = a.g[l];
+        double* xl = X(l);
+        const double* bl = l == 0 ? b0 : B(l);
+        const int bs = l == 0 ? 2 : 1;
+        if (l > 0) {
+          for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) xl[i] = 0.0;
+          __syncthreads();
+        }
+        cta_sweep_real<DIM, ORD>(g, ca, cb, xl, bl, bs, a.pre, false, a.omega);
+        double* rl = Rr(l);
+        cta_all_unknowns<DIM, ORD>(g.n1, [&](const int* c, int i) {
+          double Ax, D;
+          apply_real<DIM, ORD>(g, ca, cb, xl, c, Ax, D);
+          rl[i] = bl[(long)i * bs] - Ax;
+        });
+        __syncthreads();
+        const Grid gc = a.g[l + 1];
+        const Transfer t = a.t[l];
+        const int o7 = ORD == 2 ? 0 : 2;
+        double* bn = B(l + 1);
+        for (int I = threadIdx.x; I < (int)gc.n; I += blockDim.x) {
+          int c[DIM];
+          coords<DIM>(I, gc.n1, c);
+          if (masked<DIM, ORD>(c, I, gc.n1)) {
+            bn[I] = 0.0;
+            continue;
+          }
+          double w[DIM][WR];
+#pragma unroll
+          for (int d = 0; d < DIM; ++d)
+#pragma unroll
+            for (int o = 0; o < WR; ++o) w[d][o] = __ldg(t.tR + c[d] * 7 + o7 + o);
+          double acc = 0.0;
+          const int n1 = g.n1;
+          if constexpr (DIM == 2) {
+#pragma unroll
+            for (int ob = 0; ob < WR; ++ob) {
+              if (w[1][ob] == 0.0) continue;
+              const double* rrow = rl + (2 * c[1] + ob - R) * n1 + 2 * c[0] - R;
+#pragma unroll
+              for (int oa = 0; oa < WR; ++oa)
+                if (w[0][oa] != 0.0) acc = fma(w[1][ob] * w[0][oa], rrow[oa], acc);
+            }
+          } else {
+            for (int oc = 0; oc < WR; ++oc) {
+              if (w[2][oc] == 0.0) continue;
+              for (int ob = 0; ob < WR; ++ob) {
+                if (w[1][ob] == 0.0) continue;
+                const double* rrow = rl + ((2 * c[2] + oc - R) * n1 + 2 * c[1] + ob - R) * n1 + 2 * c[0] - R;
+#pragma unroll
+                for (int oa = 0; oa < WR; ++oa)
+                  if (w[0][oa] != 0.0) acc = fma(w[2][oc] * w[1][ob] * w[0][oa], rrow[oa], acc);
+              }
+            }
+          }
+          bn[I] = acc;
+        }
+        __syncthreads();
+      }
+      {
+        double* xL = X(L - 1);
+        const double* bL = B(L - 1);
+        for (int i = threadIdx.x; i < (int)a.g[L - 1].n; i += blockDim.x) xL[i] = 0.0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < a.nu; i += blockDim.x) {
+          double acc = 0.0;
+          for (int j = 0; j < a.nu; ++j) acc = fma(inv[2 * ((long)i * a.nu + j)], bL[a.unk[j]], acc);
+          xL[a.unk[i]] = acc;
+        }
+        __syncthreads();
+      }
+      for (int l = L - 2; l >= 0; --l) {
+        const Grid g = a.g[l];
+        const Grid gc = a.g[l + 1];
+        const Transfer t = a.t[l];
+        double* xl = X(l);
+        const double* xcl = X(l + 1);
+        cta_all_unknowns<DIM, ORD>(g.n1, [&](const int* c, int i) {
+          int base[DIM];
+          double w[DIM][NW];
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            base[d] = (int)__ldg(t.tP + c[d] * 4);
+#pragma unroll
+            for (int o = 0; o < NW; ++o) w[d][o] = __ldg(t.tP + c[d] * 4 + 1 + o);
+          }
+          const int n1 = gc.n1;
+          double acc = 0.0;
+          if constexpr (DIM == 2) {
+#pragma unroll
+            for (int ob = 0; ob < NW; ++ob)
+#pragma unroll
+              for (int oa = 0; oa < NW; ++oa) {
+                const double ww = w[1][ob] * w[0][oa];
+                if (ww != 0.0) acc = fma(ww, xcl[(base[1] + ob) * n1 + base[0] + oa], acc);
+              }
+          } else {
+#pragma unroll
+            for (int oc = 0; oc < NW; ++oc)
+#pragma unroll
+              for (int ob = 0; ob < NW; ++ob)
+#pragma unroll
+                for (int oa = 0; oa < NW; ++oa) {
+                  const double ww = w[2][oc] * w[1][ob] * w[0][oa];
+                  if (ww != 0.0) acc = fma(ww, xcl[((base[2] + oc) * n1 + base[1] + ob) * n1 + base[0] + oa], acc);
+                }
+          }
+          xl[i] += acc;
+        });
+        __syncthreads();
+        cta_sweep_real<DIM, ORD>(g, ca, cb, xl, l == 0 ? b0 : B(l), l == 0 ? 2 : 1, a.post, true, a.omega);
+      }
+    }
+    // write this component of the solution (masked entries are 0 in x)
+    {
+      const double* x0 = X(0);
+      double* out = reinterpret_cast<double*>(xc0) + part;
+      for (int i = threadIdx.x; i < (int)a.g[0].n; i += blockDim.x) out[2L * i] = x0[i];
+    }
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------- launchers
@@ -911,6 +1396,19 @@ static void chcta_t(const Grid& g, View b, View x, double2* r, double2* d0, doub
 void launch_cheb_cta(const Grid& g, View b, View x, double2* r, double2* d0, double2* d1, double theta, double sigma,
                      double delta, int iters, double scale, int nprob, cudaStream_t s) {
   SWITCH_DO(g, chcta_t, g, b, x, r, d0, d1, theta, sigma, delta, iters, scale, nprob, s);
+}
+
+template <int DIM, int ORD>
+static void mgreal_t(const MGRealArgs& a, int nprob, size_t smem, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mg_real<DIM, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    attr = true;
+  }
+  k_mg_real<DIM, ORD><<<nprob, MG_THREADS, smem, s>>>(a);
+}
+void launch_mg_real(const MGRealArgs& a, int nprob, size_t smem, cudaStream_t s) {
+  SWITCH_DO(a.g[0], mgreal_t, a, nprob, smem, s);
 }
 
 void launch_Bv(const Grid& g2, const Grid& g1, const double* tPm, const double* tGm, View v, View bp, View out,

@@ -11,6 +11,8 @@
 // load/store is a coalesced row segment, the time DFT runs along the tile in
 // shared memory, and the frequency layout [k][half][field][node] (space
 // contiguous again) falls out of the same tile.  No separate transpose pass.
+#include <cstdlib>
+
 #include "aao_internal.h"
 
 namespace aao {
@@ -319,6 +321,151 @@ __global__ void k_kkt_vel(Geo G, KKTTab T, const double* __restrict__ x, double*
   *yo = Mw + tau * (G.nu * KL + CL) + tau * BTq;
 }
 
+// Tiled version of the velocity rows (same formulas).  A CTA owns a TX x TY (x TZ) tile of one
+// (half, t, component) slice; it forms the mass operand w = cA v_t + cB lam_t + cO other and the
+// L-operand u once per node of the tile + 2-halo in shared memory (masked / outside nodes = 0,
+// which is exactly the elimination), plus the pressure tile for B^T.
+template <int DIM>
+struct KT {
+  static constexpr int TX = 32, TY = DIM == 2 ? 8 : 4, TZ = DIM == 2 ? 1 : 2;
+  static constexpr int SX = TX + 4, SY = TY + 4, SZ = DIM == 2 ? 1 : TZ + 4;
+  static constexpr int PX = TX / 2 + 4, PY = TY / 2 + 4, PZ = DIM == 2 ? 1 : TZ / 2 + 4;
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_kkt_vel_tiled(Geo G, KKTTab T, const double* __restrict__ x,
+                                                       double* __restrict__ y, int oseen, int tiles_x, int tiles_y) {
+  using K = KT<DIM>;
+  __shared__ double sw[K::SZ][K::SY][K::SX];
+  __shared__ double su[K::SZ][K::SY][K::SX];
+  __shared__ double sq[K::PZ][K::PY][K::PX];
+  const int row = blockIdx.y;  // h * n_b + t
+  const int h = row / G.n_b, t = row % G.n_b;
+  const int comp = blockIdx.z;
+  const int tile = blockIdx.x;
+  const int txi = tile % tiles_x, tyi = (tile / tiles_x) % tiles_y, tzi = tile / (tiles_x * tiles_y);
+  const int x0 = txi * K::TX, y0 = tyi * K::TY, z0 = DIM == 3 ? tzi * K::TZ : 0;
+  const int n1 = G.n1q2, m1 = G.n1q1;
+  const long nblk = G.nblk, n_b = G.n_b, ns = G.n_s;
+  const double tau = G.tau;
+  const double* xv = x + (long)t * nblk + comp * ns;
+  const double* xl = x + (long)(n_b + t) * nblk + comp * ns;
+  const double* xo = nullptr;
+  double cA, cB, cO;
+  if (h == 0) {
+    cA = tau; cB = 1.0; cO = -1.0;
+    if (t + 1 < n_b) xo = x + (long)(n_b + t + 1) * nblk + comp * ns;
+  } else {
+    cA = 1.0; cB = -tau / G.beta; cO = -1.0;
+    if (t >= 1) xo = x + (long)(t - 1) * nblk + comp * ns;
+  }
+  const int tid = threadIdx.x;
+  const int NS = K::SX * K::SY * K::SZ;
+  for (int e = tid; e < NS; e += blockDim.x) {
+    const int li = e % K::SX, lj = (e / K::SX) % K::SY, lk = e / (K::SX * K::SY);
+    const int gi = x0 - 2 + li, gj = y0 - 2 + lj, gk = DIM == 3 ? z0 - 2 + lk : 0;
+    double wv = 0.0, uv = 0.0;
+    bool in = gi > 0 && gi < n1 - 1 && gj > 0 && gj < n1 - 1;
+    if (DIM == 3) in = in && gk > 0 && gk < n1 - 1;
+    if (in) {
+      const long nd = ((long)gk * n1 + gj) * n1 + gi;
+      const double a = xv[nd], l = xl[nd];
+      wv = cA * a + cB * l;
+      if (xo) wv += cO * xo[nd];
+      uv = h == 0 ? l : a;
+    }
+    sw[lk][lj][li] = wv;
+    su[lk][lj][li] = uv;
+  }
+  // pressure tile: Q1 nodes from floor((x0-1)/2)
+  const int P0x = (x0 >= 1) ? (x0 - 1) / 2 : -1, P0y = (y0 >= 1) ? (y0 - 1) / 2 : -1;
+  const int P0z = DIM == 3 ? ((z0 >= 1) ? (z0 - 1) / 2 : -1) : 0;
+  const double* q = x + (long)(h == 0 ? (n_b + t) : t) * nblk + G.n_v;
+  const int NP = K::PX * K::PY * K::PZ;
+  for (int e = tid; e < NP; e += blockDim.x) {
+    const int li = e % K::PX, lj = (e / K::PX) % K::PY, lk = e / (K::PX * K::PY);
+    const int I = P0x + li, J = P0y + lj, Kk = DIM == 3 ? P0z + lk : 0;
+    double v = 0.0;
+    if (I >= 0 && I < m1 && J >= 0 && J < m1 && Kk >= 0 && Kk < m1) {
+      const long pn = ((long)Kk * m1 + J) * m1 + I;
+      if (pn != 0) v = q[pn];  // pinned pressure node: eliminated column
+    }
+    sq[lk][lj][li] = v;
+  }
+  __syncthreads();
+  const int lx = tid % K::TX, ly = (tid / K::TX) % K::TY, lz = DIM == 3 ? tid / (K::TX * K::TY) : 0;
+  const int i = x0 + lx, j = y0 + ly, k = z0 + lz;
+  if (i >= n1 || j >= n1 || (DIM == 3 && k >= n1)) return;
+  const long node = ((long)k * n1 + j) * n1 + i;
+  double* yo = y + (long)row * nblk + comp * ns + node;
+  bool interior = i > 0 && i < n1 - 1 && j > 0 && j < n1 - 1;
+  if (DIM == 3) interior = interior && k > 0 && k < n1 - 1;
+  if (!interior) {
+    *yo = 0.0;
+    return;
+  }
+  double mx[5], kx[5];
+#pragma unroll
+  for (int o = 0; o < 5; ++o) {
+    mx[o] = __ldg(T.tM + i * 5 + o);
+    kx[o] = __ldg(T.tK + i * 5 + o);
+  }
+  const double* cv = oseen ? ((h == 0 ? T.convT : T.conv) + node * (DIM == 2 ? 25 : 125)) : nullptr;
+  double Mw = 0, KL = 0, CL = 0;
+  const int zb = DIM == 3 ? 0 : 2, ze = DIM == 3 ? 5 : 3;
+  for (int oc = zb; oc < ze; ++oc) {
+    const double mz = DIM == 3 ? __ldg(T.tM + k * 5 + oc) : 1.0;
+    const double kz = DIM == 3 ? __ldg(T.tK + k * 5 + oc) : 0.0;
+    if (DIM == 3 && mz == 0.0 && kz == 0.0) continue;
+    const int sz = DIM == 3 ? lz + oc : 0;
+#pragma unroll
+    for (int ob = 0; ob < 5; ++ob) {
+      const double my = __ldg(T.tM + j * 5 + ob), ky = __ldg(T.tK + j * 5 + ob);
+      if (my == 0.0 && ky == 0.0) continue;
+      const double* wr = &sw[sz][ly + ob][lx];
+      const double* ur = &su[sz][ly + ob][lx];
+      double rmw = 0, rmu = 0, rku = 0;
+#pragma unroll
+      for (int oa = 0; oa < 5; ++oa) {
+        rmw = fma(mx[oa], wr[oa], rmw);
+        rmu = fma(mx[oa], ur[oa], rmu);
+        rku = fma(kx[oa], ur[oa], rku);
+        if (oseen) CL = fma(__ldg(cv + ((DIM == 3 ? oc * 5 : 0) + ob) * 5 + oa), ur[oa], CL);
+      }
+      const double mzy = mz * my, kzy = kz * my + mz * ky;
+      Mw = fma(mzy, rmw, Mw);
+      KL = fma(kzy, rmu, fma(mzy, rku, KL));
+    }
+  }
+  // B^T q from the pressure tile
+  double P[DIM][3], Gd[DIM][3];
+  int I0[DIM];
+  const int cc[3] = {i, j, k};
+  const int P0[3] = {P0x, P0y, P0z};
+  for (int a = 0; a < DIM; ++a) {
+    I0[a] = ((cc[a] - 1 >= 0) ? (cc[a] - 1) / 2 : -1) - P0[a];
+    for (int o = 0; o < 3; ++o) {
+      P[a][o] = __ldg(T.tPmT + cc[a] * 3 + o);
+      Gd[a][o] = __ldg(T.tGmT + cc[a] * 3 + o);
+    }
+  }
+  double BTq = 0;
+  for (int oc = 0; oc < (DIM == 3 ? 3 : 1); ++oc) {
+    const double fz = DIM == 3 ? (comp == 2 ? Gd[2][oc] : P[2][oc]) : 1.0;
+    const int lzq = DIM == 3 ? I0[2] + oc : 0;
+#pragma unroll
+    for (int ob = 0; ob < 3; ++ob) {
+      const double fy = comp == 1 ? Gd[1][ob] : P[1][ob];
+#pragma unroll
+      for (int oa = 0; oa < 3; ++oa) {
+        const double fx = comp == 0 ? Gd[0][oa] : P[0][oa];
+        BTq = fma(-fz * fy * fx, sq[lzq][I0[1] + ob][I0[0] + oa], BTq);
+      }
+    }
+  }
+  *yo = Mw + tau * (G.nu * KL + CL) + tau * BTq;
+}
+
 // pressure rows: half 0 y1p_t = tau B lam_t ; half 1 y2p_t = tau B v_t
 template <int DIM>
 __global__ void k_kkt_pres(Geo G, KKTTab T, const double* __restrict__ x, double* __restrict__ y) {
@@ -502,11 +649,23 @@ void launch_kkt(const Ctx& c, const double* x, double* y, cudaStream_t s) {
   const Geo G = geo_of(c);
   dim3 gv((unsigned)((c.n_v + 127) / 128), 2 * c.n_b);
   dim3 gp((unsigned)((c.n_p + 127) / 128), 2 * c.n_b);
+  static const bool untiled = std::getenv("AAO_KKT_UNTILED") != nullptr;
   if (c.dim == 2) {
-    k_kkt_vel<2><<<gv, 128, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0);
+    if (untiled) {
+      k_kkt_vel<2><<<gv, 128, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0);
+    } else {
+      const int tx = (c.n1q2 + KT<2>::TX - 1) / KT<2>::TX, ty = (c.n1q2 + KT<2>::TY - 1) / KT<2>::TY;
+      k_kkt_vel_tiled<2><<<dim3(tx * ty, 2 * c.n_b, 2), 256, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0, tx, ty);
+    }
     k_kkt_pres<2><<<gp, 128, 0, s>>>(G, T, x, y);
   } else {
-    k_kkt_vel<3><<<gv, 128, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0);
+    if (untiled) {
+      k_kkt_vel<3><<<gv, 128, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0);
+    } else {
+      const int tx = (c.n1q2 + KT<3>::TX - 1) / KT<3>::TX, ty = (c.n1q2 + KT<3>::TY - 1) / KT<3>::TY;
+      const int tz = (c.n1q2 + KT<3>::TZ - 1) / KT<3>::TZ;
+      k_kkt_vel_tiled<3><<<dim3(tx * ty * tz, 2 * c.n_b, 3), 256, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0, tx, ty);
+    }
     k_kkt_pres<3><<<gp, 128, 0, s>>>(G, T, x, y);
   }
 }
