@@ -802,21 +802,40 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   a.inv_pg = inv_pg;
   a.unk = S.coarse_unk;
   a.nu = S.ncoarse_unk;
+  // class stencil tables (Q2, real operators, smoothing levels need n1 >= 9): first in dynamic smem
+  static const bool no_ctab = std::getenv("AAO_NO_CTAB") != nullptr;
+  size_t tab_bytes = 0;
+  a.use_ctab = 0;
+  if (!no_ctab && S.order == 2 && op.conv_sel == 0 && a.nlev >= 2 && a.g[a.nlev - 2].n1 >= 9) {
+    a.use_ctab = 1;
+    const size_t per = (size_t)(1 << c.dim) * ((c.dim == 2 ? 25 : 125) + 1);
+    tab_bytes = (a.nlev - 1) * per * sizeof(double);
+    tab_bytes = (tab_bytes + 15) / 16 * 16;
+  }
   // shared-memory residency: coarsest levels first while x and b fit in the budget
   static const char* bud = std::getenv("AAO_SMEM_BUDGET");
   // measured (tools/smem_sweep.sh): keeping only the smallest levels in shared memory leaves the L1
   // to the finest level, which matters more (c2 3.02 vs 3.17 ms, c3 277 vs 437 ms)
   const size_t budget = bud ? (size_t)std::atol(bud) : 20 * 1024;
-  size_t used = 0;
+  size_t used = tab_bytes;
   a.lsm = a.nlev;
   for (int l = a.nlev - 1; l >= 1; --l) {
     const size_t need = 2 * a.g[l].n * sizeof(double2);
-    if (used + need > budget) break;
+    if (used + need > budget + tab_bytes) break;
     a.sm_x[l] = (long)(used / sizeof(double2));
     a.sm_b[l] = (long)(used / sizeof(double2)) + a.g[l].n;
     used += need;
     a.lsm = l;
   }
+  // the bottom levels (few unknowns) run warp-synchronously: their phases are pure latency
+  static const char* wl = std::getenv("AAO_WARP_UNKNOWNS");
+  const long wmax = wl ? std::atol(wl) : 256;
+  a.lwarp = a.nlev;
+  for (int l = 1; l < a.nlev; ++l)
+    if (unknowns(a.g[l]) <= wmax) {
+      a.lwarp = l;
+      break;
+    }
   launch_mg_cta(a, nprob, used, s);
   ++launch_counter();
 }

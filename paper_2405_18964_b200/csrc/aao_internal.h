@@ -73,6 +73,8 @@ struct MGArgs {
   const int* unk;
   int nu;
   int lsm;                // levels >= lsm keep x and b in shared memory (offsets below, in double2)
+  int lwarp;              // levels >= lwarp run inside one warp (tiny bottom of the V-cycle)
+  int use_ctab;           // Q2 real operators: per-level class stencils at the start of dynamic smem
   long sm_x[MG_MAXL], sm_b[MG_MAXL];
 };
 

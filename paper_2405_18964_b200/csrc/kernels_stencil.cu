@@ -598,6 +598,85 @@ __global__ void k_Bv(Grid g2, Grid g1, const double* __restrict__ tPm, const dou
   out[idx] = res;
 }
 
+// ---------------------------------------------------------------- class stencils (Q2, real operators)
+// Masked nodes of an iterate are exact zeros, so every interior Q2 node can use the UN-eliminated
+// interior 1-D rows: a vertex row (even index) or a midpoint row (odd index) per axis.  A level of
+// a real operator A = a M + b K therefore has only 2^d distinct stencils, precomputed per CTA (per
+// frequency) in shared memory together with 1/A_ii: one coefficient lookup and two FMAs per tap.
+template <int DIM>
+struct ClassTab {
+  static constexpr int NT = DIM == 2 ? 25 : 125;   // taps
+  static constexpr int NCL = 1 << DIM;             // classes (parity per axis, x fastest)
+  static constexpr int PER_LEVEL = NCL * (NT + 1); // + 1/diag per class
+};
+
+// build the class stencils of level g for A = ca M + cb K into tab (ClassTab::PER_LEVEL doubles)
+template <int DIM>
+__device__ void build_class_tab(const Grid& g, double ca, double cb, double* tab, int tid, int nth) {
+  using CT = ClassTab<DIM>;
+  // un-eliminated interior rows: index 4 (vertex) and 3 (midpoint); needs n1 >= 9
+  for (int e = tid; e < CT::NCL * CT::NT; e += nth) {
+    const int cls = e / CT::NT, tap = e % CT::NT;
+    const int oa = tap % 5, ob = (tap / 5) % 5, oc = tap / 25;
+    const int rx = (cls & 1) ? 3 : 4, ry = ((cls >> 1) & 1) ? 3 : 4, rz = ((cls >> 2) & 1) ? 3 : 4;
+    const double mx = g.tM[rx * 5 + oa], kx = g.tK[rx * 5 + oa];
+    const double my = g.tM[ry * 5 + ob], ky = g.tK[ry * 5 + ob];
+    double mz = 1.0, kz = 0.0;
+    if (DIM == 3) {
+      mz = g.tM[rz * 5 + oc];
+      kz = g.tK[rz * 5 + oc];
+    }
+    const double m = mz * my * mx;
+    const double k = kz * my * mx + mz * ky * mx + mz * my * kx;
+    tab[cls * (CT::NT + 1) + tap] = ca * m + cb * k;
+  }
+  __syncthreads();
+  for (int cls = tid; cls < CT::NCL; cls += nth) {
+    const int centre = DIM == 2 ? 12 : 62;
+    tab[cls * (CT::NT + 1) + CT::NT] = 1.0 / tab[cls * (CT::NT + 1) + centre];
+  }
+}
+
+// (A x)_i with the class stencil; returns 1/A_ii in invD.  Rows with zero taps for odd y/z are skipped.
+template <int DIM, int PY, int PZ>
+__device__ __forceinline__ double2 class_eval_rows(const double* T, const double2* x, const int* c, int n1) {
+  constexpr int AY0 = PY ? 1 : 0, AY1 = PY ? 4 : 5;
+  constexpr int AZ0 = DIM == 3 ? (PZ ? 1 : 0) : 2, AZ1 = DIM == 3 ? (PZ ? 4 : 5) : 3;
+  const int xl = c[0] >= 2 ? c[0] - 2 : c[0], xr = c[0] + 2 <= n1 - 1 ? c[0] + 2 : c[0];
+  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int oc = AZ0; oc < AZ1; ++oc) {
+    const int zrow = DIM == 3 ? (c[2] + oc - 2) * n1 : 0;
+#pragma unroll
+    for (int ob = AY0; ob < AY1; ++ob) {
+      const double2* row = x + (zrow + c[1] + ob - 2) * n1;
+      const double* t = T + ((DIM == 3 ? oc * 5 : 0) + ob) * 5;
+      acc = cfma(t[0], row[xl], acc);
+      acc = cfma(t[1], row[c[0] - 1], acc);
+      acc = cfma(t[2], row[c[0]], acc);
+      acc = cfma(t[3], row[c[0] + 1], acc);
+      acc = cfma(t[4], row[xr], acc);
+    }
+  }
+  return acc;
+}
+
+template <int DIM>
+__device__ __forceinline__ double2 class_eval(const double* tabl, const double2* x, const int* c, int n1,
+                                              double& invD) {
+  using CT = ClassTab<DIM>;
+  const int cls = (c[0] & 1) | ((c[1] & 1) << 1) | (DIM == 3 ? ((c[2] & 1) << 2) : 0);
+  const double* T = tabl + cls * (CT::NT + 1);
+  invD = T[CT::NT];
+  const int ycls = (c[1] & 1) | (DIM == 3 ? ((c[2] & 1) << 1) : 0);
+  switch (ycls) {
+    case 0: return class_eval_rows<DIM, 0, 0>(T, x, c, n1);
+    case 1: return class_eval_rows<DIM, 1, 0>(T, x, c, n1);
+    case 2: return class_eval_rows<DIM, 0, 1>(T, x, c, n1);
+    default: return class_eval_rows<DIM, 1, 1>(T, x, c, n1);
+  }
+}
+
 // ---------------------------------------------------------------- CTA-resident solvers
 // One CTA owns one problem (one frequency / slot / component) and runs the WHOLE fixed-count
 // solve -- every level, colour, transfer and V-cycle -- with block barriers only.  The problems
@@ -634,10 +713,21 @@ __device__ __forceinline__ void sor_node(const Grid& g, const Coef& cf, const do
   }
 }
 
+// Thread groups for the CTA-resident solves: the whole block (big levels, __syncthreads) or one
+// warp (the tiny bottom levels of each V-cycle, __syncwarp -- their phases are pure latency).
+template <bool W>
+__device__ __forceinline__ void gsync() {
+  if (W)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
 // Visit the unknown nodes with per-axis start s[a] and stride st[a] (interior range [lo, hi]),
-// distributing them over the CTA's threads.
+// distributing them over the group's threads (tid, nth).
 template <int DIM, class F>
-__device__ __forceinline__ void cta_visit(int n1, const int* s0, const int* sta, int lo, int hi, F&& f) {
+__device__ __forceinline__ void cta_visit(int n1, const int* s0, const int* sta, int lo, int hi, int tid, int nth,
+                                          F&& f) {
   int cnt[DIM], start[DIM], stv[DIM];
   int total = 1;
 #pragma unroll
@@ -650,7 +740,7 @@ __device__ __forceinline__ void cta_visit(int n1, const int* s0, const int* sta,
     total *= cnt[a];
   }
   if (total == 0) return;
-  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+  for (int t = tid; t < total; t += nth) {
     int c[DIM];
     const unsigned q = (unsigned)t / (unsigned)cnt[0];
     c[0] = start[0] + stv[0] * (int)((unsigned)t - q * (unsigned)cnt[0]);
@@ -666,9 +756,9 @@ __device__ __forceinline__ void cta_visit(int n1, const int* s0, const int* sta,
   }
 }
 
-// all unknowns of a level: Q2 in parity classes (uniform taps per warp), Q1 in one pass
+// all unknowns of a level: Q2 in y/z parity classes (uniform taps per warp), Q1 in one pass
 template <int DIM, int ORD, class F>
-__device__ __forceinline__ void cta_all_unknowns(int n1, F&& f) {
+__device__ __forceinline__ void cta_all_unknowns(int n1, int tid, int nth, F&& f) {
   if (ORD == 2) {
     for (int cls = 0; cls < (1 << (DIM - 1)); ++cls) {
       int s0[DIM], st[DIM];
@@ -679,7 +769,7 @@ __device__ __forceinline__ void cta_all_unknowns(int n1, F&& f) {
         s0[a] = ((cls >> (a - 1)) & 1) ? 1 : 2;
         st[a] = 2;
       }
-      cta_visit<DIM>(n1, s0, st, 1, n1 - 2, f);
+      cta_visit<DIM>(n1, s0, st, 1, n1 - 2, tid, nth, f);
     }
   } else {
     int s0[DIM], st[DIM];
@@ -688,15 +778,16 @@ __device__ __forceinline__ void cta_all_unknowns(int n1, F&& f) {
       s0[a] = 0;
       st[a] = 1;
     }
-    cta_visit<DIM>(n1, s0, st, 0, n1 - 1, [&](const int* c, int idx) {
+    cta_visit<DIM>(n1, s0, st, 0, n1 - 1, tid, nth, [&](const int* c, int idx) {
       if (idx != 0) f(c, idx);  // pinned node
     });
   }
 }
 
-template <int DIM, int ORD, bool CONV>
+template <int DIM, int ORD, bool CONV, bool W>
 __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
-                                          const double2* b, int sweeps, bool reverse, double omega) {
+                                          const double2* b, int sweeps, bool reverse, double omega, int tid, int nth,
+                                          const double* tabl = nullptr) {
   constexpr int C1 = ORD == 2 ? 3 : 2;
   constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
   for (int sw = 0; sw < sweeps; ++sw)
@@ -709,7 +800,15 @@ __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const d
         res[a] = col % C1;
         col /= C1;
       }
-      auto upd = [&](const int* c, int idx) { sor_node<DIM, ORD, CONV>(g, cf, cv, x, b, c, idx, omega); };
+      auto upd = [&](const int* c, int idx) {
+        if (ORD == 2 && !CONV && tabl != nullptr) {
+          double invD;
+          const double2 Ax = class_eval<DIM>(tabl, x, c, g.n1, invD);
+          x[idx] = cadd(x[idx], cscale(omega * invD, csub(b[idx], Ax)));
+        } else {
+          sor_node<DIM, ORD, CONV>(g, cf, cv, x, b, c, idx, omega);
+        }
+      };
       if (ORD == 2) {
         // colour residue r: x nodes r + 3m (coalesced); y/z in parity classes r + 3p + 6m so that
         // the row taps are warp-uniform
@@ -722,171 +821,209 @@ __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const d
             s0[a] = res[a] + 3 * ((cls >> (a - 1)) & 1);
             st[a] = 6;
           }
-          cta_visit<DIM>(g.n1, s0, st, 1, g.n1 - 2, upd);
+          cta_visit<DIM>(g.n1, s0, st, 1, g.n1 - 2, tid, nth, upd);
         }
       } else {
         int st[DIM];
 #pragma unroll
         for (int a = 0; a < DIM; ++a) st[a] = 2;
-        cta_visit<DIM>(g.n1, res, st, 0, g.n1 - 1, [&](const int* c, int idx) {
+        cta_visit<DIM>(g.n1, res, st, 0, g.n1 - 1, tid, nth, [&](const int* c, int idx) {
           if (idx != 0) upd(c, idx);
         });
       }
-      __syncthreads();
+      gsync<W>();
     }
+}
+
+// level storage of one problem inside the CTA-resident MG
+struct MGLevels {
+  const MGArgs& a;
+  double2* smem;
+  int p;
+  double* ctab;   // class stencils per smoothing level (ORD 2, real operators) or nullptr
+  __device__ double2* X(int l) const {
+    if (l == 0) return a.x0.p + voff(a.x0, p, a.g[0].n);
+    return l >= a.lsm ? smem + a.sm_x[l] : a.xw[l] + (long)p * a.g[l].n;
+  }
+  __device__ double2* B(int l) const {
+    if (l == 0) return a.b0.p + voff(a.b0, p, a.g[0].n);
+    return l >= a.lsm ? smem + a.sm_b[l] : a.bw[l] + (long)p * a.g[l].n;
+  }
+  __device__ double2* R(int l) const { return a.rw[l] + (long)p * a.g[l].n; }
+  __device__ const double* CV(int l) const { return a.op.conv_sel == 1 ? a.g[l].conv : a.g[l].convT; }
+};
+
+// down-leg of level l: (x_l = 0 for l > 0), pre-smoothing, residual, restriction to b_{l+1}
+template <int DIM, int ORD, bool CONV, bool W>
+__device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int nth) {
+  constexpr int R = ORD == 2 ? 3 : 1;
+  constexpr int WR = 2 * R + 1;
+  const MGArgs& a = S.a;
+  const Grid g = a.g[l];
+  double2* xl = S.X(l);
+  const double2* bl = S.B(l);
+  if (l > 0) {
+    for (int i = tid; i < (int)g.n; i += nth) xl[i] = make_double2(0.0, 0.0);
+    gsync<W>();
+  }
+  const double* tabl = S.ctab ? S.ctab + l * ClassTab<DIM>::PER_LEVEL : nullptr;
+  cta_sweep<DIM, ORD, CONV, W>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl);
+  double2* rl = S.R(l);
+  const double* cvl = S.CV(l);
+  cta_all_unknowns<DIM, ORD>(g.n1, tid, nth, [&](const int* c, int i) {
+    double2 Ax;
+    if (ORD == 2 && !CONV && tabl != nullptr) {
+      double invD;
+      Ax = class_eval<DIM>(tabl, xl, c, g.n1, invD);
+    } else if (CONV) {
+      double2 D;
+      apply_op_conv<DIM, ORD>(g, cf, cvl, xl, c, i, Ax, D);
+    } else {
+      double D;
+      apply_op_real<DIM, ORD>(g, cf.a.x, cf.b.x, xl, c, i, Ax, D);
+    }
+    rl[i] = csub(bl[i], Ax);
+  });
+  gsync<W>();
+  const Grid gc = a.g[l + 1];
+  const Transfer t = a.t[l];
+  const int o7 = ORD == 2 ? 0 : 2;
+  double2* bn = S.B(l + 1);
+  for (int I = tid; I < (int)gc.n; I += nth) {
+    int c[DIM];
+    coords<DIM>(I, gc.n1, c);
+    if (masked<DIM, ORD>(c, I, gc.n1)) {
+      bn[I] = make_double2(0.0, 0.0);
+      continue;
+    }
+    double w[DIM][WR];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d)
+#pragma unroll
+      for (int o = 0; o < WR; ++o) w[d][o] = __ldg(t.tR + c[d] * 7 + o7 + o);
+    double2 acc = make_double2(0.0, 0.0);
+    const int n1 = g.n1;
+    if constexpr (DIM == 2) {
+      for (int ob = 0; ob < WR; ++ob) {
+        if (w[1][ob] == 0.0) continue;
+        const double2* rrow = rl + (2 * c[1] + ob - R) * n1 + 2 * c[0] - R;
+        for (int oa = 0; oa < WR; ++oa)
+          if (w[0][oa] != 0.0) acc = cfma(w[1][ob] * w[0][oa], rrow[oa], acc);
+      }
+    } else {
+      for (int oc = 0; oc < WR; ++oc) {
+        if (w[2][oc] == 0.0) continue;
+        for (int ob = 0; ob < WR; ++ob) {
+          if (w[1][ob] == 0.0) continue;
+          const double2* rrow = rl + ((2 * c[2] + oc - R) * n1 + 2 * c[1] + ob - R) * n1 + 2 * c[0] - R;
+          for (int oa = 0; oa < WR; ++oa)
+            if (w[0][oa] != 0.0) acc = cfma(w[2][oc] * w[1][ob] * w[0][oa], rrow[oa], acc);
+        }
+      }
+    }
+    bn[I] = acc;
+  }
+  gsync<W>();
+}
+
+// coarsest level: dense inverse (masked entries of the coarsest iterate read as 0 in the prolongation)
+template <int DIM, int ORD, bool W>
+__device__ void mg_coarse(const MGLevels& S, int tid, int nth) {
+  const MGArgs& a = S.a;
+  const int L = a.nlev;
+  double2* xL = S.X(L - 1);
+  const double2* bL = S.B(L - 1);
+  for (int i = tid; i < (int)a.g[L - 1].n; i += nth) xL[i] = make_double2(0.0, 0.0);
+  gsync<W>();
+  const double2* A = a.inv + (long)(S.p / a.inv_pg) * a.nu * a.nu;
+  for (int i = tid; i < a.nu; i += nth) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int j = 0; j < a.nu; ++j) acc = cadd(acc, cmul(A[(long)i * a.nu + j], bL[a.unk[j]]));
+    xL[a.unk[i]] = acc;
+  }
+  gsync<W>();
+}
+
+// up-leg of level l: prolongate x_{l+1} and correct, post-smoothing
+template <int DIM, int ORD, bool CONV, bool W>
+__device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth) {
+  constexpr int NW = ORD == 2 ? 3 : 2;
+  const MGArgs& a = S.a;
+  const Grid g = a.g[l];
+  const Grid gc = a.g[l + 1];
+  const Transfer t = a.t[l];
+  double2* xl = S.X(l);
+  const double2* xc = S.X(l + 1);
+  cta_all_unknowns<DIM, ORD>(g.n1, tid, nth, [&](const int* c, int i) {
+    int base[DIM];
+    double w[DIM][NW];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      base[d] = (int)__ldg(t.tP + c[d] * 4);
+#pragma unroll
+      for (int o = 0; o < NW; ++o) w[d][o] = __ldg(t.tP + c[d] * 4 + 1 + o);
+    }
+    const int n1 = gc.n1;
+    double2 acc = make_double2(0.0, 0.0);
+    if constexpr (DIM == 2) {
+#pragma unroll
+      for (int ob = 0; ob < NW; ++ob)
+#pragma unroll
+        for (int oa = 0; oa < NW; ++oa) {
+          const double ww = w[1][ob] * w[0][oa];
+          if (ww != 0.0) acc = cfma(ww, xc[(base[1] + ob) * n1 + base[0] + oa], acc);
+        }
+    } else {
+#pragma unroll
+      for (int oc = 0; oc < NW; ++oc)
+#pragma unroll
+        for (int ob = 0; ob < NW; ++ob)
+#pragma unroll
+          for (int oa = 0; oa < NW; ++oa) {
+            const double ww = w[2][oc] * w[1][ob] * w[0][oa];
+            if (ww != 0.0) acc = cfma(ww, xc[((base[2] + oc) * n1 + base[1] + ob) * n1 + base[0] + oa], acc);
+          }
+    }
+    xl[i] = cadd(xl[i], acc);
+  });
+  gsync<W>();
+  const double* tabl = S.ctab ? S.ctab + l * ClassTab<DIM>::PER_LEVEL : nullptr;
+  cta_sweep<DIM, ORD, CONV, W>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl);
 }
 
 template <int DIM, int ORD, bool CONV>
 __global__ void __launch_bounds__(MG_THREADS, 1) k_mg_cta(MGArgs a) {
   extern __shared__ double2 smem[];
-  constexpr int R = ORD == 2 ? 3 : 1;
-  constexpr int WR = 2 * R + 1;
-  constexpr int NW = ORD == 2 ? 3 : 2;
   const int p = blockIdx.x;
   const int L = a.nlev;
-  // level pointers of this problem; coarse levels that fit live in shared memory (generic pointers)
-  auto X = [&](int l) -> double2* {
-    if (l == 0) return a.x0.p + voff(a.x0, p, a.g[0].n);
-    return l >= a.lsm ? smem + a.sm_x[l] : a.xw[l] + (long)p * a.g[l].n;
-  };
-  auto B = [&](int l) -> double2* {
-    if (l == 0) return a.b0.p + voff(a.b0, p, a.g[0].n);
-    return l >= a.lsm ? smem + a.sm_b[l] : a.bw[l] + (long)p * a.g[l].n;
-  };
-  auto Rr = [&](int l) -> double2* { return a.rw[l] + (long)p * a.g[l].n; };
   const Coef cf = a.op.coef[p / a.op.per_group];
-  auto CV = [&](int l) -> const double* { return a.op.conv_sel == 1 ? a.g[l].conv : a.g[l].convT; };
-  for (int i = threadIdx.x; i < (int)a.g[0].n; i += blockDim.x) X(0)[i] = make_double2(0.0, 0.0);
+  const int tid = threadIdx.x, nth = blockDim.x;
+  // class stencils of every smoothing level (real Q2 operators) at the start of dynamic smem
+  double* ctab = nullptr;
+  if (ORD == 2 && !CONV && a.use_ctab) {
+    ctab = reinterpret_cast<double*>(smem);
+    for (int l = 0; l < L - 1; ++l)
+      build_class_tab<DIM>(a.g[l], cf.a.x, cf.b.x, ctab + l * ClassTab<DIM>::PER_LEVEL, tid, nth);
+    __syncthreads();
+  }
+  const MGLevels S{a, smem, p, ctab};
+  const int lw = a.lwarp;   // levels >= lw run inside warp 0
+  double2* x0 = S.X(0);
+  for (int i = tid; i < (int)a.g[0].n; i += nth) x0[i] = make_double2(0.0, 0.0);
   __syncthreads();
   for (int cyc = 0; cyc < a.cycles; ++cyc) {
-    // ---- down: smooth, residual, restrict
-    for (int l = 0; l < L - 1; ++l) {
-      const Grid g = a.g[l];
-      if (l > 0) {
-        for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) X(l)[i] = make_double2(0.0, 0.0);
-        __syncthreads();
-      }
-      cta_sweep<DIM, ORD, CONV>(g, cf, CV(l), X(l), B(l), a.pre, false, a.omega);
-      {
-        double2* rl = Rr(l);
-        const double2* xl = X(l);
-        const double2* bl = B(l);
-        const double* cvl = CV(l);
-        cta_all_unknowns<DIM, ORD>(g.n1, [&](const int* c, int i) {
-          double2 Ax;
-          if (CONV) {
-            double2 D;
-            apply_op_conv<DIM, ORD>(g, cf, cvl, xl, c, i, Ax, D);
-          } else {
-            double D;
-            apply_op_real<DIM, ORD>(g, cf.a.x, cf.b.x, xl, c, i, Ax, D);
-          }
-          rl[i] = csub(bl[i], Ax);
-        });
+    for (int l = 0; l < lw && l < L - 1; ++l) mg_down<DIM, ORD, CONV, false>(S, cf, l, tid, nth);
+    if (lw < L) {
+      if (tid < 32) {
+        for (int l = lw; l < L - 1; ++l) mg_down<DIM, ORD, CONV, true>(S, cf, l, tid, 32);
+        mg_coarse<DIM, ORD, true>(S, tid, 32);
+        for (int l = L - 2; l >= lw; --l) mg_up<DIM, ORD, CONV, true>(S, cf, l, tid, 32);
       }
       __syncthreads();
-      const Grid gc = a.g[l + 1];
-      const Transfer t = a.t[l];
-      const int o7 = ORD == 2 ? 0 : 2;
-      for (int I = threadIdx.x; I < (int)gc.n; I += blockDim.x) {
-        int c[DIM];
-        coords<DIM>(I, gc.n1, c);
-        if (masked<DIM, ORD>(c, I, gc.n1)) {
-          B(l + 1)[I] = make_double2(0.0, 0.0);
-          continue;
-        }
-        double w[DIM][WR];
-#pragma unroll
-        for (int d = 0; d < DIM; ++d)
-#pragma unroll
-          for (int o = 0; o < WR; ++o) w[d][o] = __ldg(t.tR + c[d] * 7 + o7 + o);
-        double2 acc = make_double2(0.0, 0.0);
-        const int n1 = g.n1;
-        if constexpr (DIM == 2) {
-          for (int ob = 0; ob < WR; ++ob) {
-            if (w[1][ob] == 0.0) continue;
-            const int jj = 2 * c[1] + ob - R;
-            for (int oa = 0; oa < WR; ++oa) {
-              if (w[0][oa] == 0.0) continue;
-              acc = cfma(w[1][ob] * w[0][oa], Rr(l)[jj * n1 + 2 * c[0] + oa - R], acc);
-            }
-          }
-        } else {
-          for (int oc = 0; oc < WR; ++oc) {
-            if (w[2][oc] == 0.0) continue;
-            const int kk = 2 * c[2] + oc - R;
-            for (int ob = 0; ob < WR; ++ob) {
-              if (w[1][ob] == 0.0) continue;
-              const int jj = 2 * c[1] + ob - R;
-              for (int oa = 0; oa < WR; ++oa) {
-                if (w[0][oa] == 0.0) continue;
-                acc = cfma(w[2][oc] * w[1][ob] * w[0][oa], Rr(l)[(kk * n1 + jj) * n1 + 2 * c[0] + oa - R], acc);
-              }
-            }
-          }
-        }
-        B(l + 1)[I] = acc;
-      }
-      __syncthreads();
+    } else {
+      mg_coarse<DIM, ORD, false>(S, tid, nth);
     }
-    // ---- coarsest level: dense inverse
-    {
-      // masked (boundary / pinned) entries of the coarsest iterate must read as 0 in the prolongation
-      for (int i = threadIdx.x; i < (int)a.g[L - 1].n; i += blockDim.x) X(L - 1)[i] = make_double2(0.0, 0.0);
-      __syncthreads();
-      const double2* A = a.inv + (long)(p / a.inv_pg) * a.nu * a.nu;
-      for (int i = threadIdx.x; i < a.nu; i += blockDim.x) {
-        double2 acc = make_double2(0.0, 0.0);
-        for (int j = 0; j < a.nu; ++j) acc = cadd(acc, cmul(A[(long)i * a.nu + j], B(L - 1)[a.unk[j]]));
-        X(L - 1)[a.unk[i]] = acc;
-      }
-      __syncthreads();
-    }
-    // ---- up: prolongate + correct, smooth
-    for (int l = L - 2; l >= 0; --l) {
-      const Grid g = a.g[l];
-      const Grid gc = a.g[l + 1];
-      const Transfer t = a.t[l];
-      for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) {
-        int c[DIM];
-        coords<DIM>(i, g.n1, c);
-        if (masked<DIM, ORD>(c, i, g.n1)) continue;
-        int base[DIM];
-        double w[DIM][NW];
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) {
-          base[d] = (int)__ldg(t.tP + c[d] * 4);
-#pragma unroll
-          for (int o = 0; o < NW; ++o) w[d][o] = __ldg(t.tP + c[d] * 4 + 1 + o);
-        }
-        const int n1 = gc.n1;
-        const double2* xc = X(l + 1);
-        double2 acc = make_double2(0.0, 0.0);
-        if constexpr (DIM == 2) {
-#pragma unroll
-          for (int ob = 0; ob < NW; ++ob)
-#pragma unroll
-            for (int oa = 0; oa < NW; ++oa) {
-              const double ww = w[1][ob] * w[0][oa];
-              if (ww != 0.0) acc = cfma(ww, xc[(base[1] + ob) * n1 + base[0] + oa], acc);
-            }
-        } else {
-#pragma unroll
-          for (int oc = 0; oc < NW; ++oc)
-#pragma unroll
-            for (int ob = 0; ob < NW; ++ob)
-#pragma unroll
-              for (int oa = 0; oa < NW; ++oa) {
-                const double ww = w[2][oc] * w[1][ob] * w[0][oa];
-                if (ww != 0.0)
-                  acc = cfma(ww, xc[((base[2] + oc) * n1 + base[1] + ob) * n1 + base[0] + oa], acc);
-              }
-        }
-        X(l)[i] = cadd(X(l)[i], acc);
-      }
-      __syncthreads();
-      cta_sweep<DIM, ORD, CONV>(g, cf, CV(l), X(l), B(l), a.post, true, a.omega);
-    }
+    for (int l = (lw < L ? lw : L - 1) - 1; l >= 0; --l) mg_up<DIM, ORD, CONV, false>(S, cf, l, tid, nth);
   }
 }
 
@@ -922,7 +1059,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) k_cheb_cta(Grid g, View bv, Vie
     const double c1 = rho1 * rho, c2 = 2.0 * rho1 / delta;
     const double2* dold = d0;
     double2* dnew = d1;
-    cta_all_unknowns<DIM, ORD>(g.n1, [&](const int* c, int i) {
+    cta_all_unknowns<DIM, ORD>(g.n1, threadIdx.x, blockDim.x, [&](const int* c, int i) {
       double2 Mx, Kx, Cx;
       double dM, dK, dC;
       apply_MKC<DIM, ORD, false>(g, nullptr, dold, c, i, Mx, Kx, Cx, dM, dK, dC);
@@ -1098,13 +1235,13 @@ __device__ __forceinline__ void cta_sweep_real(const Grid& g, double ca, double 
             s0[a] = res[a] + 3 * ((cls >> (a - 1)) & 1);
             st[a] = 6;
           }
-          cta_visit<DIM>(g.n1, s0, st, 1, g.n1 - 2, upd);
+          cta_visit<DIM>(g.n1, s0, st, 1, g.n1 - 2, threadIdx.x, blockDim.x, upd);
         }
       } else {
         int st[DIM];
 #pragma unroll
         for (int a = 0; a < DIM; ++a) st[a] = 2;
-        cta_visit<DIM>(g.n1, res, st, 0, g.n1 - 1, [&](const int* c, int idx) {
+        cta_visit<DIM>(g.n1, res, st, 0, g.n1 - 1, threadIdx.x, blockDim.x, [&](const int* c, int idx) {
           if (idx != 0) upd(c, idx);
         });
       }
@@ -1147,7 +1284,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) k_mg_real(MGRealArgs a) {
         }
         cta_sweep_real<DIM, ORD>(g, ca, cb, xl, bl, bs, a.pre, false, a.omega);
         double* rl = Rr(l);
-        cta_all_unknowns<DIM, ORD>(g.n1, [&](const int* c, int i) {
+        cta_all_unknowns<DIM, ORD>(g.n1, threadIdx.x, blockDim.x, [&](const int* c, int i) {
           double Ax, D;
           apply_real<DIM, ORD>(g, ca, cb, xl, c, Ax, D);
           rl[i] = bl[(long)i * bs] - Ax;
@@ -1214,7 +1351,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) k_mg_real(MGRealArgs a) {
         const Transfer t = a.t[l];
         double* xl = X(l);
         const double* xcl = X(l + 1);
-        cta_all_unknowns<DIM, ORD>(g.n1, [&](const int* c, int i) {
+        cta_all_unknowns<DIM, ORD>(g.n1, threadIdx.x, blockDim.x, [&](const int* c, int i) {
           int base[DIM];
           double w[DIM][NW];
 #pragma unroll
