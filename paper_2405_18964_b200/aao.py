@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libaao.so")
+LIB_PATH = os.environ.get("AAO_LIB", os.path.join(_HERE, "libaao.so"))
 _lib = None
 
 AAO_STOKES, AAO_OSEEN = 0, 1

@@ -15,6 +15,9 @@ namespace aao {
 #ifndef MG_THREADS
 #define MG_THREADS 512
 #endif
+#ifndef MG_THREADS_TAB
+#define MG_THREADS_TAB 512
+#endif
 
 // ---------------------------------------------------------------- complex helpers
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -784,10 +787,10 @@ __device__ __forceinline__ void cta_all_unknowns(int n1, int tid, int nth, F&& f
   }
 }
 
-template <int DIM, int ORD, bool CONV, bool W>
+template <int DIM, int ORD, bool CONV, bool W, bool TAB>
 __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
                                           const double2* b, int sweeps, bool reverse, double omega, int tid, int nth,
-                                          const double* tabl = nullptr) {
+                                          const double* tabl) {
   constexpr int C1 = ORD == 2 ? 3 : 2;
   constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
   for (int sw = 0; sw < sweeps; ++sw)
@@ -801,7 +804,7 @@ __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const d
         col /= C1;
       }
       auto upd = [&](const int* c, int idx) {
-        if (ORD == 2 && !CONV && tabl != nullptr) {
+        if constexpr (TAB) {
           double invD;
           const double2 Ax = class_eval<DIM>(tabl, x, c, g.n1, invD);
           x[idx] = cadd(x[idx], cscale(omega * invD, csub(b[idx], Ax)));
@@ -854,7 +857,7 @@ struct MGLevels {
 };
 
 // down-leg of level l: (x_l = 0 for l > 0), pre-smoothing, residual, restriction to b_{l+1}
-template <int DIM, int ORD, bool CONV, bool W>
+template <int DIM, int ORD, bool CONV, bool W, bool TAB>
 __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int nth) {
   constexpr int R = ORD == 2 ? 3 : 1;
   constexpr int WR = 2 * R + 1;
@@ -867,12 +870,12 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
     gsync<W>();
   }
   const double* tabl = S.ctab ? S.ctab + l * ClassTab<DIM>::PER_LEVEL : nullptr;
-  cta_sweep<DIM, ORD, CONV, W>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl);
+  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl);
   double2* rl = S.R(l);
   const double* cvl = S.CV(l);
   cta_all_unknowns<DIM, ORD>(g.n1, tid, nth, [&](const int* c, int i) {
     double2 Ax;
-    if (ORD == 2 && !CONV && tabl != nullptr) {
+    if constexpr (TAB) {
       double invD;
       Ax = class_eval<DIM>(tabl, xl, c, g.n1, invD);
     } else if (CONV) {
@@ -945,7 +948,7 @@ __device__ void mg_coarse(const MGLevels& S, int tid, int nth) {
 }
 
 // up-leg of level l: prolongate x_{l+1} and correct, post-smoothing
-template <int DIM, int ORD, bool CONV, bool W>
+template <int DIM, int ORD, bool CONV, bool W, bool TAB>
 __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth) {
   constexpr int NW = ORD == 2 ? 3 : 2;
   const MGArgs& a = S.a;
@@ -988,11 +991,11 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
   });
   gsync<W>();
   const double* tabl = S.ctab ? S.ctab + l * ClassTab<DIM>::PER_LEVEL : nullptr;
-  cta_sweep<DIM, ORD, CONV, W>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl);
+  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl);
 }
 
-template <int DIM, int ORD, bool CONV>
-__global__ void __launch_bounds__(MG_THREADS, 1) k_mg_cta(MGArgs a) {
+template <int DIM, int ORD, bool CONV, bool TAB>
+__global__ void __launch_bounds__(TAB ? MG_THREADS_TAB : MG_THREADS, 1) k_mg_cta(MGArgs a) {
   extern __shared__ double2 smem[];
   const int p = blockIdx.x;
   const int L = a.nlev;
@@ -1000,7 +1003,7 @@ __global__ void __launch_bounds__(MG_THREADS, 1) k_mg_cta(MGArgs a) {
   const int tid = threadIdx.x, nth = blockDim.x;
   // class stencils of every smoothing level (real Q2 operators) at the start of dynamic smem
   double* ctab = nullptr;
-  if (ORD == 2 && !CONV && a.use_ctab) {
+  if (TAB) {
     ctab = reinterpret_cast<double*>(smem);
     for (int l = 0; l < L - 1; ++l)
       build_class_tab<DIM>(a.g[l], cf.a.x, cf.b.x, ctab + l * ClassTab<DIM>::PER_LEVEL, tid, nth);
@@ -1012,18 +1015,18 @@ __global__ void __launch_bounds__(MG_THREADS, 1) k_mg_cta(MGArgs a) {
   for (int i = tid; i < (int)a.g[0].n; i += nth) x0[i] = make_double2(0.0, 0.0);
   __syncthreads();
   for (int cyc = 0; cyc < a.cycles; ++cyc) {
-    for (int l = 0; l < lw && l < L - 1; ++l) mg_down<DIM, ORD, CONV, false>(S, cf, l, tid, nth);
+    for (int l = 0; l < lw && l < L - 1; ++l) mg_down<DIM, ORD, CONV, false, TAB>(S, cf, l, tid, nth);
     if (lw < L) {
       if (tid < 32) {
-        for (int l = lw; l < L - 1; ++l) mg_down<DIM, ORD, CONV, true>(S, cf, l, tid, 32);
+        for (int l = lw; l < L - 1; ++l) mg_down<DIM, ORD, CONV, true, TAB>(S, cf, l, tid, 32);
         mg_coarse<DIM, ORD, true>(S, tid, 32);
-        for (int l = L - 2; l >= lw; --l) mg_up<DIM, ORD, CONV, true>(S, cf, l, tid, 32);
+        for (int l = L - 2; l >= lw; --l) mg_up<DIM, ORD, CONV, true, TAB>(S, cf, l, tid, 32);
       }
       __syncthreads();
     } else {
       mg_coarse<DIM, ORD, false>(S, tid, nth);
     }
-    for (int l = (lw < L ? lw : L - 1) - 1; l >= 0; --l) mg_up<DIM, ORD, CONV, false>(S, cf, l, tid, nth);
+    for (int l = (lw < L ? lw : L - 1) - 1; l >= 0; --l) mg_up<DIM, ORD, CONV, false, TAB>(S, cf, l, tid, nth);
   }
 }
 
@@ -1512,14 +1515,18 @@ template <int DIM, int ORD>
 static void mgcta_t(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_mg_cta<DIM, ORD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_mg_cta<DIM, ORD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_mg_cta<DIM, ORD, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_mg_cta<DIM, ORD, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (ORD == 2)
+      cudaFuncSetAttribute(k_mg_cta<DIM, ORD, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  if (a.op.conv_sel == 0)
-    k_mg_cta<DIM, ORD, false><<<nprob, MG_THREADS, smem, s>>>(a);
+  if (a.op.conv_sel != 0)
+    k_mg_cta<DIM, ORD, true, false><<<nprob, MG_THREADS, smem, s>>>(a);
+  else if (ORD == 2 && a.use_ctab)
+    k_mg_cta<DIM, ORD, false, (ORD == 2)><<<nprob, MG_THREADS_TAB, smem, s>>>(a);
   else
-    k_mg_cta<DIM, ORD, true><<<nprob, MG_THREADS, smem, s>>>(a);
+    k_mg_cta<DIM, ORD, false, false><<<nprob, MG_THREADS, smem, s>>>(a);
 }
 void launch_mg_cta(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
   SWITCH_DO(a.g[0], mgcta_t, a, nprob, smem, s);
