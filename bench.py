@@ -92,6 +92,22 @@ def rank_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def aggregate_replicas(ms, iterations, world, device="cuda"):
+    """Whole-job numbers over independent replicas: time = MAX over ranks, work = SUM over ranks.
+
+    Returns (max_ms, total_iterations).  World size 1 needs no process group.
+    """
+    if world == 1:
+        return float(ms), float(iterations)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    it = torch.tensor([float(iterations)], dtype=torch.float64, device=device)
+    dist.all_reduce(it, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(it.item())
+
+
 # ---------------------------------------------------------------------------------------------
 def oracle_iteration_sample(cfg, reps, warm):
     """The CPU oracle as it stands, timed on one GMRES iteration's work: precond_apply (all n_b
@@ -193,16 +209,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     clocks = sampler.stop()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        it_t = torch.tensor([its_total], device="cuda", dtype=torch.float64)
-        dist.all_reduce(it_t)
-        its_all = float(it_t.item())
-    else:
-        its_all = float(its_total)
+    ms, its_all = aggregate_replicas(e0.elapsed_time(e1), its_total, world)
     ms_per_step = ms / args.steps
     value = cfg.n_dofs * its_all / (ms / 1e3)
 
@@ -264,12 +271,8 @@ def run_ours(args):
         _, info_e, _, _ = ctx.gmres_solve_host(bh, xh)
         its_e2e += info_e["iterations"]
     torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = world * cfg.n_dofs * its_e2e / e2e_s
+    e2e_s, its_e2e_all = aggregate_replicas(time.perf_counter() - t0, its_e2e, world)
+    e2e_value = cfg.n_dofs * its_e2e_all / e2e_s
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

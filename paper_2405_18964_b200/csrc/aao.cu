@@ -806,9 +806,10 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   static const bool no_ctab = std::getenv("AAO_NO_CTAB") != nullptr;
   size_t tab_bytes = 0;
   a.use_ctab = 0;
-  if (!no_ctab && S.order == 2 && op.conv_sel == 0 && a.nlev >= 2 && a.g[a.nlev - 2].n1 >= 9) {
+  if (!no_ctab && S.order == 2 && a.nlev >= 2 && a.g[a.nlev - 2].n1 >= 9) {
     a.use_ctab = 1;
-    const size_t per = (size_t)(1 << c.dim) * ((c.dim == 2 ? 25 : 125) + 1);
+    const size_t nt = c.dim == 2 ? 25 : 125;
+    const size_t per = (size_t)(1 << c.dim) * (op.conv_sel == 0 ? (nt + 1) : 2 * nt);
     tab_bytes = (a.nlev - 1) * per * sizeof(double);
     tab_bytes = (tab_bytes + 15) / 16 * 16;
   }

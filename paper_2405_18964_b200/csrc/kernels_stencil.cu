@@ -640,6 +640,71 @@ __device__ void build_class_tab(const Grid& g, double ca, double cb, double* tab
   }
 }
 
+// complex coefficients (Oseen Q_k = a M + b K + c N): class table of a M + b K (double2 per tap);
+// the convection part is per node (stored stencil), accumulated separately and scaled by c.
+template <int DIM>
+__device__ void build_class_tab_c(const Grid& g, double2 ca, double2 cb, double2* tab, int tid, int nth) {
+  using CT = ClassTab<DIM>;
+  for (int e = tid; e < CT::NCL * CT::NT; e += nth) {
+    const int cls = e / CT::NT, tap = e % CT::NT;
+    const int oa = tap % 5, ob = (tap / 5) % 5, oc = tap / 25;
+    const int rx = (cls & 1) ? 3 : 4, ry = ((cls >> 1) & 1) ? 3 : 4, rz = ((cls >> 2) & 1) ? 3 : 4;
+    const double mx = g.tM[rx * 5 + oa], kx = g.tK[rx * 5 + oa];
+    const double my = g.tM[ry * 5 + ob], ky = g.tK[ry * 5 + ob];
+    double mz = 1.0, kz = 0.0;
+    if (DIM == 3) {
+      mz = g.tM[rz * 5 + oc];
+      kz = g.tK[rz * 5 + oc];
+    }
+    const double m = mz * my * mx;
+    const double k = kz * my * mx + mz * ky * mx + mz * my * kx;
+    tab[cls * CT::NT + tap] = cadd(cscale(m, ca), cscale(k, cb));
+  }
+}
+
+template <int DIM, int PY, int PZ>
+__device__ __forceinline__ void class_eval_conv_rows(const double2* T, const double* cvr, const double2* x,
+                                                     const int* c, int n1, double2& acc, double2& nacc) {
+  constexpr int AY0 = PY ? 1 : 0, AY1 = PY ? 4 : 5;
+  constexpr int AZ0 = DIM == 3 ? (PZ ? 1 : 0) : 2, AZ1 = DIM == 3 ? (PZ ? 4 : 5) : 3;
+  const int xl = c[0] >= 2 ? c[0] - 2 : c[0], xr = c[0] + 2 <= n1 - 1 ? c[0] + 2 : c[0];
+#pragma unroll
+  for (int oc = AZ0; oc < AZ1; ++oc) {
+    const int zrow = DIM == 3 ? (c[2] + oc - 2) * n1 : 0;
+#pragma unroll
+    for (int ob = AY0; ob < AY1; ++ob) {
+      const double2* row = x + (zrow + c[1] + ob - 2) * n1;
+      const int t0 = ((DIM == 3 ? oc * 5 : 0) + ob) * 5;
+#pragma unroll
+      for (int oa = 0; oa < 5; ++oa) {
+        const double2 v = row[oa == 0 ? xl : (oa == 4 ? xr : c[0] + oa - 2)];
+        acc = cadd(acc, cmul(T[t0 + oa], v));
+        nacc = cfma(__ldg(cvr + t0 + oa), v, nacc);
+      }
+    }
+  }
+}
+
+template <int DIM>
+__device__ __forceinline__ double2 class_eval_conv(const double2* tabl, const double* cv, double2 cc,
+                                                   const double2* x, const int* c, int idx, int n1, double2& D) {
+  using CT = ClassTab<DIM>;
+  const int cls = (c[0] & 1) | ((c[1] & 1) << 1) | (DIM == 3 ? ((c[2] & 1) << 2) : 0);
+  const double2* T = tabl + cls * CT::NT;
+  const double* cvr = cv + (long)idx * CT::NT;
+  double2 acc = make_double2(0.0, 0.0), nacc = acc;
+  const int ycls = (c[1] & 1) | (DIM == 3 ? ((c[2] & 1) << 1) : 0);
+  switch (ycls) {
+    case 0: class_eval_conv_rows<DIM, 0, 0>(T, cvr, x, c, n1, acc, nacc); break;
+    case 1: class_eval_conv_rows<DIM, 1, 0>(T, cvr, x, c, n1, acc, nacc); break;
+    case 2: class_eval_conv_rows<DIM, 0, 1>(T, cvr, x, c, n1, acc, nacc); break;
+    default: class_eval_conv_rows<DIM, 1, 1>(T, cvr, x, c, n1, acc, nacc); break;
+  }
+  const int centre = DIM == 2 ? 12 : 62;
+  D = cadd(T[centre], cscale(__ldg(cvr + centre), cc));
+  return cadd(acc, cmul(cc, nacc));
+}
+
 // (A x)_i with the class stencil; returns 1/A_ii in invD.  Rows with zero taps for odd y/z are skipped.
 template <int DIM, int PY, int PZ>
 __device__ __forceinline__ double2 class_eval_rows(const double* T, const double2* x, const int* c, int n1) {
@@ -759,6 +824,44 @@ __device__ __forceinline__ void cta_visit(int n1, const int* s0, const int* sta,
   }
 }
 
+// Same visit, two nodes per thread per round (t and t + nth): f2(c, idx, c2, idx2, has2) lets the
+// caller issue the loads of both before either store (colour steps: no same-colour coupling).
+template <int DIM, class F2>
+__device__ __forceinline__ void cta_visit2(int n1, const int* s0, const int* sta, int lo, int hi, int tid, int nth,
+                                           F2&& f2) {
+  int cnt[DIM], start[DIM], stv[DIM];
+  int total = 1;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    int s = s0[a];
+    while (s < lo) s += sta[a];
+    start[a] = s;
+    stv[a] = sta[a];
+    cnt[a] = s > hi ? 0 : (hi - s) / sta[a] + 1;
+    total *= cnt[a];
+  }
+  if (total == 0) return;
+  auto node = [&](int t, int* c) {
+    const unsigned q = (unsigned)t / (unsigned)cnt[0];
+    c[0] = start[0] + stv[0] * (int)((unsigned)t - q * (unsigned)cnt[0]);
+    if (DIM == 2) {
+      c[1] = start[1] + stv[1] * (int)q;
+    } else {
+      const unsigned q2 = q / (unsigned)cnt[1];
+      c[1] = start[1] + stv[1] * (int)(q - q2 * (unsigned)cnt[1]);
+      c[2] = start[2] + stv[2] * (int)q2;
+    }
+    return DIM == 2 ? c[1] * n1 + c[0] : (c[2] * n1 + c[1]) * n1 + c[0];
+  };
+  for (int t = tid; t < total; t += 2 * nth) {
+    int c[DIM], c2[DIM];
+    const int idx = node(t, c);
+    const bool has2 = t + nth < total;
+    const int idx2 = node(has2 ? t + nth : t, c2);
+    f2(c, idx, c2, idx2, has2);
+  }
+}
+
 // all unknowns of a level: Q2 in y/z parity classes (uniform taps per warp), Q1 in one pass
 template <int DIM, int ORD, class F>
 __device__ __forceinline__ void cta_all_unknowns(int n1, int tid, int nth, F&& f) {
@@ -804,7 +907,11 @@ __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const d
         col /= C1;
       }
       auto upd = [&](const int* c, int idx) {
-        if constexpr (TAB) {
+        if constexpr (TAB && CONV) {
+          double2 D;
+          const double2 Ax = class_eval_conv<DIM>(reinterpret_cast<const double2*>(tabl), cv, cf.c, x, c, idx, g.n1, D);
+          x[idx] = cadd(x[idx], cscale(omega, cdiv(csub(b[idx], Ax), D)));
+        } else if constexpr (TAB) {
           double invD;
           const double2 Ax = class_eval<DIM>(tabl, x, c, g.n1, invD);
           x[idx] = cadd(x[idx], cscale(omega * invD, csub(b[idx], Ax)));
@@ -824,7 +931,20 @@ __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const d
             s0[a] = res[a] + 3 * ((cls >> (a - 1)) & 1);
             st[a] = 6;
           }
-          cta_visit<DIM>(g.n1, s0, st, 1, g.n1 - 2, tid, nth, upd);
+          if constexpr (TAB && !CONV && false) {   // 2 nodes per thread: measured slower (2.82 vs 2.40 ms, c2)
+            cta_visit2<DIM>(g.n1, s0, st, 1, g.n1 - 2, tid, nth,
+                            [&](const int* c, int idx, const int* c2, int idx2, bool has2) {
+                              double iA, iB;
+                              const double2 A1 = class_eval<DIM>(tabl, x, c, g.n1, iA);
+                              const double2 A2 = class_eval<DIM>(tabl, x, c2, g.n1, iB);
+                              const double2 b1 = b[idx], b2 = b[idx2];
+                              const double2 x1 = x[idx], x2 = x[idx2];
+                              x[idx] = cadd(x1, cscale(omega * iA, csub(b1, A1)));
+                              if (has2) x[idx2] = cadd(x2, cscale(omega * iB, csub(b2, A2)));
+                            });
+          } else {
+            cta_visit<DIM>(g.n1, s0, st, 1, g.n1 - 2, tid, nth, upd);
+          }
         }
       } else {
         int st[DIM];
@@ -869,13 +989,17 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
     for (int i = tid; i < (int)g.n; i += nth) xl[i] = make_double2(0.0, 0.0);
     gsync<W>();
   }
-  const double* tabl = S.ctab ? S.ctab + l * ClassTab<DIM>::PER_LEVEL : nullptr;
+  const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
+                                                       : ClassTab<DIM>::PER_LEVEL) : nullptr;
   cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl);
   double2* rl = S.R(l);
   const double* cvl = S.CV(l);
   cta_all_unknowns<DIM, ORD>(g.n1, tid, nth, [&](const int* c, int i) {
     double2 Ax;
-    if constexpr (TAB) {
+    if constexpr (TAB && CONV) {
+      double2 D;
+      Ax = class_eval_conv<DIM>(reinterpret_cast<const double2*>(tabl), cvl, cf.c, xl, c, i, g.n1, D);
+    } else if constexpr (TAB) {
       double invD;
       Ax = class_eval<DIM>(tabl, xl, c, g.n1, invD);
     } else if (CONV) {
@@ -990,7 +1114,8 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
     xl[i] = cadd(xl[i], acc);
   });
   gsync<W>();
-  const double* tabl = S.ctab ? S.ctab + l * ClassTab<DIM>::PER_LEVEL : nullptr;
+  const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
+                                                   : ClassTab<DIM>::PER_LEVEL) : nullptr;
   cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl);
 }
 
@@ -1005,8 +1130,13 @@ __global__ void __launch_bounds__(TAB ? MG_THREADS_TAB : MG_THREADS, 1) k_mg_cta
   double* ctab = nullptr;
   if (TAB) {
     ctab = reinterpret_cast<double*>(smem);
-    for (int l = 0; l < L - 1; ++l)
-      build_class_tab<DIM>(a.g[l], cf.a.x, cf.b.x, ctab + l * ClassTab<DIM>::PER_LEVEL, tid, nth);
+    for (int l = 0; l < L - 1; ++l) {
+      if (CONV)
+        build_class_tab_c<DIM>(a.g[l], cf.a, cf.b,
+                               reinterpret_cast<double2*>(ctab) + l * ClassTab<DIM>::NCL * ClassTab<DIM>::NT, tid, nth);
+      else
+        build_class_tab<DIM>(a.g[l], cf.a.x, cf.b.x, ctab + l * ClassTab<DIM>::PER_LEVEL, tid, nth);
+    }
     __syncthreads();
   }
   const MGLevels S{a, smem, p, ctab};
@@ -1041,6 +1171,13 @@ __global__ void __launch_bounds__(MG_THREADS, 1) k_cheb_cta(Grid g, View bv, Vie
   double2* d0 = d0w + (long)p * g.n;
   double2* d1 = d1w + (long)p * g.n;
   const double2 z = make_double2(0.0, 0.0);
+  // Q2 mass: class stencils (a = 1, b = 0) when the level has an interior vertex row (n1 >= 9)
+  __shared__ double mtab[ClassTab<DIM>::PER_LEVEL];
+  const bool tab = ORD == 2 && g.n1 >= 9;
+  if (tab) {
+    build_class_tab<DIM>(g, 1.0, 0.0, mtab, threadIdx.x, blockDim.x);
+    __syncthreads();
+  }
   for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) {
     int c[DIM];
     coords<DIM>(i, g.n1, c);
@@ -1063,14 +1200,21 @@ __global__ void __launch_bounds__(MG_THREADS, 1) k_cheb_cta(Grid g, View bv, Vie
     const double2* dold = d0;
     double2* dnew = d1;
     cta_all_unknowns<DIM, ORD>(g.n1, threadIdx.x, blockDim.x, [&](const int* c, int i) {
-      double2 Mx, Kx, Cx;
-      double dM, dK, dC;
-      apply_MKC<DIM, ORD, false>(g, nullptr, dold, c, i, Mx, Kx, Cx, dM, dK, dC);
+      double2 Mx;
+      double invM;
+      if (ORD == 2 && tab) {
+        Mx = class_eval<DIM>(mtab, dold, c, g.n1, invM);
+      } else {
+        double2 Kx, Cx;
+        double dM, dK, dC;
+        apply_MKC<DIM, ORD, false>(g, nullptr, dold, c, i, Mx, Kx, Cx, dM, dK, dC);
+        invM = 1.0 / dM;
+      }
       const double2 d = dold[i];
       x[i] = cadd(x[i], d);
       const double2 rr = csub(r[i], Mx);
       r[i] = rr;
-      dnew[i] = cadd(cscale(c1, d), cscale(c2, cscale(1.0 / dM, rr)));
+      dnew[i] = cadd(cscale(c1, d), cscale(c2, cscale(invM, rr)));
     });
     __syncthreads();
     double2* tmp = d0;
@@ -1517,11 +1661,15 @@ static void mgcta_t(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
   if (!attr) {
     cudaFuncSetAttribute(k_mg_cta<DIM, ORD, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_mg_cta<DIM, ORD, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    if (ORD == 2)
+    if (ORD == 2) {
       cudaFuncSetAttribute(k_mg_cta<DIM, ORD, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      cudaFuncSetAttribute(k_mg_cta<DIM, ORD, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    }
     attr = true;
   }
-  if (a.op.conv_sel != 0)
+  if (a.op.conv_sel != 0 && ORD == 2 && a.use_ctab)
+    k_mg_cta<DIM, ORD, true, (ORD == 2)><<<nprob, MG_THREADS_TAB, smem, s>>>(a);
+  else if (a.op.conv_sel != 0)
     k_mg_cta<DIM, ORD, true, false><<<nprob, MG_THREADS, smem, s>>>(a);
   else if (ORD == 2 && a.use_ctab)
     k_mg_cta<DIM, ORD, false, (ORD == 2)><<<nprob, MG_THREADS_TAB, smem, s>>>(a);
