@@ -70,7 +70,15 @@ typedef struct {
   int cheb_iters;        /* Chebyshev semi-iterations (10)                      */
   int uzawa_iters;       /* Uzawa iterations, Oseen (6)                         */
   double uzawa_mu;       /* Uzawa parameter mu (3/4)                            */
+  int pmode;             /* aao_pmode: AAO_PRECOND_LINEAR (Algorithm 1, default) or
+                            AAO_PRECOND_NONLINEAR (Algorithm 2: per-frequency inner
+                            GMRES to inner_eps; aao_gmres_solve then runs FGMRES)  */
+  double inner_eps;      /* inner relative tolerance (1e-2)                      */
+  int inner_maxit;       /* inner iteration cap = inner Krylov basis size (reading: 60;
+                            reduced at create if the basis does not fit in memory)     */
 } aao_config;
+
+typedef enum { AAO_PRECOND_LINEAR = 0, AAO_PRECOND_NONLINEAR = 1 } aao_pmode;
 
 /* Fill *cfg with the paper's defaults (4 V-cycles, 2/2 sweeps, omega 1, 10 Chebyshev,
    6 Uzawa, mu 3/4); geometry / time / beta / nu must still be set by the caller. */
@@ -91,12 +99,16 @@ typedef struct {
   double true_relres;    /* ||b - A x|| / ||b|| recomputed at exit                           */
   int precond_applies;   /* including the x-update application per cycle                    */
   double ms_total;       /* wall time of the solve (host clock around device work)           */
+  long inner_its_total;  /* nonlinear mode: inner GMRES iterations summed over frequencies and
+                            preconditioner applications of this solve                        */
+  int inner_its_max;     /* nonlinear mode: largest inner iteration count of one frequency    */
 } aao_info;
 
 /* Assemble operators and per-frequency data, allocate all device workspace (step A9).
    Rejects with AAO_ERR_CONFIG: dim not in {2,3}; n_cells not a power of 2 or < 4;
    n_t < 3; T, beta, nu <= 0; Oseen without wind_q2; mg_cycles < 1; cheb_iters < 1;
-   uzawa_iters < 1; uzawa_mu <= 0.  Ownership of *out passes to the caller
+   uzawa_iters < 1; uzawa_mu <= 0; pmode not in {0,1}; nonlinear with inner_eps not in (0,1)
+   or inner_maxit < 1.  Ownership of *out passes to the caller
    (release with aao_destroy).  Runs on the current CUDA device. */
 aao_status aao_create(const aao_config* cfg, aao_ctx** out);
 void aao_destroy(aao_ctx* ctx);
@@ -118,10 +130,12 @@ aao_status aao_build_rhs(aao_ctx* ctx, const double* vd_q2, double* b, void* str
 aao_status aao_kkt_apply(aao_ctx* ctx, const double* x, double* y, void* stream);
 
 /* z = Pbar_C^{-1} r, Algorithm 1 (steps A3-A8).  Device pointers, r != z.
-   A fixed linear map (fixed-count inner solvers). */
+   A fixed linear map (fixed-count inner solvers).  With pmode = AAO_PRECOND_NONLINEAR:
+   Algorithm 2 (a nonlinear map; synchronises the stream once per inner iteration). */
 aao_status aao_precond_apply(aao_ctx* ctx, const double* r, double* z, void* stream);
 
-/* Restarted right-preconditioned GMRES(m), MGS + Givens (step A1).
+/* Restarted right-preconditioned GMRES(m), MGS + Givens (step A1); flexible GMRES (FGMRES,
+   storing the preconditioned basis) when pmode = AAO_PRECOND_NONLINEAR.
    b, x: DEVICE; x is the initial guess on input (pass zeros for x0 = 0) and the
    solution on output.  hist: HOST, may be NULL; receives |g_{k+1}|/||b|| per
    iteration (up to hist_cap entries).  Synchronises `stream` before returning;
@@ -140,6 +154,10 @@ aao_status aao_gmres_solve_host(aao_ctx* ctx, const double* b_host, double* x_ho
    (Stokes) or after Algorithm 3 (Oseen), to HOST memory `out` as complex128
    pairs (re, im): [half 0..1][n_v + n_p] in the field order above.  Synchronises. */
 aao_status aao_debug_freq_block(aao_ctx* ctx, int k, double* out, void* stream);
+
+/* Nonlinear mode: inner GMRES iteration counts of the last aao_precond_apply, one per stored
+   frequency k < n_f (HOST out, up to cap entries); returns the number written (>= 0) or an error. */
+int aao_last_inner_iterations(const aao_ctx* ctx, int* out, int cap);
 
 /* Per-phase device timings of the last aao_precond_apply, milliseconds
    (fft_fwd, velocity block solves, pressure block solves, fft_inv); requires

@@ -26,7 +26,8 @@ class Config(ctypes.Structure):
                 ("beta", ctypes.c_double), ("nu", ctypes.c_double), ("problem", ctypes.c_int),
                 ("wind_q2", ctypes.POINTER(ctypes.c_double)), ("mg_cycles", ctypes.c_int),
                 ("pre_sweeps", ctypes.c_int), ("post_sweeps", ctypes.c_int), ("omega", ctypes.c_double),
-                ("cheb_iters", ctypes.c_int), ("uzawa_iters", ctypes.c_int), ("uzawa_mu", ctypes.c_double)]
+                ("cheb_iters", ctypes.c_int), ("uzawa_iters", ctypes.c_int), ("uzawa_mu", ctypes.c_double),
+                ("pmode", ctypes.c_int), ("inner_eps", ctypes.c_double), ("inner_maxit", ctypes.c_int)]
 
 
 class Krylov(ctypes.Structure):
@@ -37,7 +38,7 @@ class Info(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int), ("restarts", ctypes.c_int), ("converged", ctypes.c_int),
                 ("breakdown", ctypes.c_int), ("final_relres", ctypes.c_double),
                 ("true_relres", ctypes.c_double), ("precond_applies", ctypes.c_int),
-                ("ms_total", ctypes.c_double)]
+                ("ms_total", ctypes.c_double), ("inner_its_total", ctypes.c_long), ("inner_its_max", ctypes.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -46,7 +47,8 @@ class Info(ctypes.Structure):
 EXPORTS = ["aao_config_defaults", "aao_create", "aao_destroy", "aao_last_error", "aao_vector_len",
            "aao_device_bytes", "aao_pack", "aao_build_rhs", "aao_kkt_apply", "aao_precond_apply",
            "aao_gmres_solve", "aao_gmres_solve_host", "aao_debug_freq_block", "aao_set_timing",
-           "aao_last_phase_ms", "aao_last_launch_count", "aao_profile_smoother", "aao_profile_read"]
+           "aao_last_phase_ms", "aao_last_launch_count", "aao_profile_smoother", "aao_profile_read",
+           "aao_last_inner_iterations"]
 
 
 def load(path: str = LIB_PATH):
@@ -87,6 +89,8 @@ def load(path: str = LIB_PATH):
     L.aao_profile_smoother.restype = st
     L.aao_profile_read.argtypes = [vp, dp]
     L.aao_profile_read.restype = st
+    L.aao_last_inner_iterations.argtypes = [vp, ctypes.POINTER(ctypes.c_int), i]
+    L.aao_last_inner_iterations.restype = ctypes.c_int
     L.aao_last_launch_count.argtypes = [vp]
     L.aao_last_launch_count.restype = ctypes.c_long
     _lib = L
@@ -106,7 +110,7 @@ class Context:
 
     def __init__(self, dim, n_cells, x_lo, x_hi, n_t, T, beta, nu, problem="stokes", wind_q2=None,
                  mg_cycles=4, pre_sweeps=2, post_sweeps=2, omega=1.0, cheb_iters=10, uzawa_iters=6,
-                 uzawa_mu=0.75):
+                 uzawa_mu=0.75, nonlinear=False, inner_eps=1e-2, inner_maxit=60):
         import torch
         if not torch.cuda.is_available():
             raise AAOError("no CUDA device: the aao hot path has no CPU fallback")
@@ -123,6 +127,8 @@ class Context:
             cfg.wind_q2 = self._wind.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         cfg.mg_cycles, cfg.pre_sweeps, cfg.post_sweeps, cfg.omega = mg_cycles, pre_sweeps, post_sweeps, omega
         cfg.cheb_iters, cfg.uzawa_iters, cfg.uzawa_mu = cheb_iters, uzawa_iters, uzawa_mu
+        cfg.pmode, cfg.inner_eps, cfg.inner_maxit = (1 if nonlinear else 0), inner_eps, inner_maxit
+        self.nonlinear = bool(nonlinear)
         h = ctypes.c_void_p()
         rc = L.aao_create(ctypes.byref(cfg), ctypes.byref(h))
         if rc != 0:
@@ -250,6 +256,12 @@ class Context:
         out = (ctypes.c_double * 3)()
         self._check(self.L.aao_profile_read(self.h, out), "profile_read")
         return out[0], out[1], int(out[2])
+
+    def last_inner_iterations(self):
+        """Nonlinear mode: inner GMRES iterations per stored frequency of the last precond_apply."""
+        buf = (ctypes.c_int * self.n_f)()
+        n = self._check(self.L.aao_last_inner_iterations(self.h, buf, self.n_f), "last_inner_iterations")
+        return list(buf[:n])
 
     def last_launch_count(self):
         return int(self.L.aao_last_launch_count(self.h))

@@ -5,7 +5,8 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["csrc/aao.cu", "csrc/kernels_stencil.cu", "csrc/kernels_time.cu", "csrc/kernels_blas.cu"]
+SOURCES = ["csrc/aao.cu", "csrc/kernels_stencil.cu", "csrc/kernels_time.cu", "csrc/kernels_blas.cu",
+           "csrc/kernels_freq.cu"]
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-warn-spills"]
 

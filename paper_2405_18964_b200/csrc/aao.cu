@@ -582,6 +582,7 @@ void setup(Ctx& c, const aao_config& cfg) {
   };
   c.coefKp = upload(c, std::vector<Coef>{coef(0.0, 1.0, 0.0)});
   c.coefMass = upload(c, std::vector<Coef>{coef(1.0, 0.0, 0.0)});
+  c.coefNegMass = upload(c, std::vector<Coef>{coef(-1.0, 0.0, 0.0)});
   c.invKp = upload(c, inv_of(1, 0.0, 1.0, 0.0, nullptr, unk_p));
   if (!c.oseen) {
     std::vector<Coef> cw(n_f);
@@ -594,6 +595,9 @@ void setup(Ctx& c, const aao_config& cfg) {
     }
     c.coefW = upload(c, cw);
     c.invW = upload(c, iw);
+    std::vector<Coef> zx(n_f);
+    for (int k = 0; k < n_f; ++k) zx[k] = coef(c.fch[k].c1, c.fch[k].c2 * nu, 0.0);   // X = c1 M + c2 L
+    c.coefZX = upload(c, zx);
   } else {
     // Q_k = d_k M + tau L + (tau/sqrt(beta)) M, L = nu K + N; Q_k^H uses N^T
     std::vector<Coef> cq(n_f), cqh(n_f), u2(n_f), u3(n_f), s2(n_f), s3(n_f);
@@ -668,6 +672,30 @@ void setup(Ctx& c, const aao_config& cfg) {
         CK(cudaMemset(S.b[l], 0, n * sizeof(double2)));
       }
     }
+  }
+  // Algorithm 2 workspace: inner Krylov basis V_0..V_m plus Zt, U (frequency vectors)
+  if (cfg.pmode == AAO_PRECOND_NONLINEAR) {
+    c.nonlinear = true;
+    c.inner_eps = cfg.inner_eps;
+    const size_t fvec = (size_t)(fv + fp) * sizeof(double2);
+    size_t freeb = 0, totb = 0;
+    CK(cudaMemGetInfo(&freeb, &totb));
+    const long fit = (long)((freeb * 0.6) / fvec) - 3;
+    int m = std::min<long>(cfg.inner_maxit, std::max<long>(fit, 1));
+    c.inner_maxit = m;
+    c.nlV.resize(m + 3);
+    for (int j = 0; j < m + 3; ++j) {
+      c.nlV[j].v = dalloc<double2>(c, fv);
+      c.nlV[j].p = dalloc<double2>(c, fp);
+      CK(cudaMemset(c.nlV[j].v, 0, fv * sizeof(double2)));
+      CK(cudaMemset(c.nlV[j].p, 0, fp * sizeof(double2)));
+    }
+    c.nlVdev = upload(c, std::vector<FVec>(c.nlV.begin(), c.nlV.begin() + m + 1));
+    c.nlH = dalloc<double2>(c, (size_t)(m + 2) * n_f);
+    c.nlPart = dalloc<double2>(c, fdot_partial_len(n_f));
+    c.nlY = dalloc<double2>(c, (size_t)n_f * (m + 1));
+    c.nlFrozen = dalloc<int>(c, n_f);
+    if (!c.oseen && !c.Xv) c.Xv = dalloc<double2>(c, fv);
   }
   CK(cudaMemset(c.Fv, 0, fv * sizeof(double2)));
   CK(cudaMemset(c.Fp, 0, fp * sizeof(double2)));
@@ -953,35 +981,41 @@ void cheb_solve(Ctx& c, const Grid& g, View b, View x, int nprob, double scale, 
   launch_counter() += c.cfg.cheb_iters + 1;
 }
 
-void precond_stokes(Ctx& c, cudaStream_t s) {
+// Stokes block solves P~_k^{-1} without the T transforms, on the frequency vector `in`
+// (velocity slots -> outV; pressure slots: K_p-MG -> outPA, M_p-Chebyshev -> outPB)
+void stokes_blocks(Ctx& c, FVec in, double2* outV, double2* outPA, double2* outPB, cudaStream_t s) {
   const int dim = c.dim, n_f = c.n_f;
   const Grid& gv = c.vel.grids[0];
   const Grid& gp = c.pres.grids[0];
   // x1 = MG(W; s1), x2 = MG(W; s2) per velocity component
   OpSel opW{c.coefW, 2 * dim, 0};
   // pressure slots on the side stream (independent of the velocity slots): K_p^{-1} by MG and
-  // M_p^{-1} by Chebyshev, combined in the inverse transform
+  // M_p^{-1} by Chebyshev, combined later
   static const bool one_stream = std::getenv("AAO_ONE_STREAM") != nullptr;
   cudaStream_t sp = one_stream ? s : c.s2;
   cudaEventRecord(c.ev_fork, s);
   cudaStreamWaitEvent(sp, c.ev_fork, 0);
   OpSel opKp{c.coefKp, 1 << 30, 0};
-  mg_solve(c, c.pres, opKp, c.invKp, 1 << 30, contig(c.XpA, gp.n), contig(c.Fp, gp.n), 2 * n_f, sp);
-  cheb_solve(c, gp, contig(c.Fp, gp.n), contig(c.XpB, gp.n), 2 * n_f, 1.0, sp);
+  mg_solve(c, c.pres, opKp, c.invKp, 1 << 30, contig(outPA, gp.n), contig(in.p, gp.n), 2 * n_f, sp);
+  cheb_solve(c, gp, contig(in.p, gp.n), contig(outPB, gp.n), 2 * n_f, 1.0, sp);
   cudaEventRecord(c.ev_join, sp);
-  mg_solve(c, c.vel, opW, c.invW, 2 * dim, contig(c.Xv, gv.n), contig(c.Fv, gv.n), n_f * 2 * dim, s);
+  mg_solve(c, c.vel, opW, c.invW, 2 * dim, contig(outV, gv.n), contig(in.v, gv.n), n_f * 2 * dim, s);
   if (c.timing) cudaEventRecord(c.ev[2], s);
   cudaStreamWaitEvent(s, c.ev_join, 0);
 }
 
-void precond_oseen(Ctx& c, cudaStream_t s) {
+void precond_stokes(Ctx& c, cudaStream_t s) { stokes_blocks(c, FVec{c.Fv, c.Fp}, c.Xv, c.XpA, c.XpB, s); }
+
+// Oseen block solves (P~_k^(UZ))^{-1} (Algorithm 3) on the frequency vector `in`: outputs X1, X2
+// (velocity slots, [k][comp][node]) and XpA (pressure slots, to be scaled by -1/tau)
+void oseen_blocks(Ctx& c, FVec in, cudaStream_t s) {
   const int dim = c.dim, n_f = c.n_f;
   const Grid& gv = c.vel.grids[0];
   const Grid& gp = c.pres.grids[0];
   const long nv = gv.n, np = gp.n;
   const int nprob = n_f * dim;
   const double tau = c.tau, mu = c.cfg.uzawa_mu;
-  View B1{c.Fv, dim, 2L * dim * nv}, B2{c.Fv + (long)dim * nv, dim, 2L * dim * nv};
+  View B1{in.v, dim, 2L * dim * nv}, B2{in.v + (long)dim * nv, dim, 2L * dim * nv};
   View X1 = contig(c.X1, nv), X2 = contig(c.X2, nv), T1 = contig(c.T1, nv), T2 = contig(c.T2, nv),
        T3 = contig(c.T3, nv);
   OpSel U1{c.coefU1, 1 << 30, 0}, U2{c.coefU2, dim, 2}, U3{c.coefU3, dim, 1}, U4{c.coefU4, 1 << 30, 0};
@@ -1009,7 +1043,7 @@ void precond_oseen(Ctx& c, cudaStream_t s) {
   if (c.timing) cudaEventRecord(c.ev[2], s);
   // (y3, y4) = -S_hat^{-1}((r3, r4) - tau (B y2, B y1))   (Algorithm 3)
   View Xv2{c.X2, dim, (long)dim * nv}, Xv1{c.X1, dim, (long)dim * nv};
-  View P3{c.Fp, 1, 2 * np}, P4{c.Fp + np, 1, 2 * np};
+  View P3{in.p, 1, 2 * np}, P4{in.p + np, 1, 2 * np};
   View Q3{c.Qp, 1, 2 * np}, Q4{c.Qp + np, 1, 2 * np};
   launch_Bv(gv, gp, c.tPm, c.tGm, Xv2, P3, Q3, 1.0, -tau, n_f, s);
   launch_Bv(gv, gp, c.tPm, c.tGm, Xv1, P4, Q4, 1.0, -tau, n_f, s);
@@ -1027,7 +1061,161 @@ void precond_oseen(Ctx& c, cudaStream_t s) {
   mg_solve(c, c.pres, opKp, c.invKp, 1 << 30, contig(c.XpA, np), contig(c.Tp, np), 2 * n_f, s);
 }
 
+void precond_oseen(Ctx& c, cudaStream_t s) { oseen_blocks(c, FVec{c.Fv, c.Fp}, s); }
+
+// ------------------------------------------------------------------ Algorithm 2 (nonlinear)
+// P~ applied to a frequency vector: out = blkdiag-preconditioner(in)   (Stokes: P~_k^{-1} of P:416-426
+// without T transforms; Oseen: (P~_k^(UZ))^{-1}, Algorithm 3)
+void pt_apply(Ctx& c, FVec in, FVec out, cudaStream_t s) {
+  const long LP = 2L * c.n_p;
+  if (!c.oseen) {
+    stokes_blocks(c, in, out.v, c.XpA, c.XpB, s);
+    launch_combine_p(out.p, c.XpA, c.XpB, c.fc, c.nu, LP, c.n_f, s);
+  } else {
+    oseen_blocks(c, in, s);
+    launch_oseen_scatter(out, c.X1, c.X2, c.XpA, -1.0 / c.tau, (long)c.dim * c.n_s, LP, c.n_f, s);
+  }
+  ++launch_counter();
+}
+
+// y = A_k x per frequency: Z_k of P:392-397 (Stokes) or G_k of eq. (SubBlockG) (Oseen)
+void op_apply(Ctx& c, FVec x, FVec y, cudaStream_t s) {
+  const int dim = c.dim, n_f = c.n_f;
+  const Grid& gv = c.vel.grids[0];
+  const Grid& gp = c.pres.grids[0];
+  const long nv = gv.n, np = gp.n;
+  auto vh = [&](double2* base, int h) { return View{base + (long)h * dim * nv, dim, 2L * dim * nv}; };
+  auto ph = [&](double2* base, int h) { return View{base + (long)h * np, 1, 2 * np}; };
+  const int nprob = n_f * dim;
+  const View none{nullptr, 1, 0};
+  if (!c.oseen) {
+    // r1 = M x1 + X x2 + B^T x4 ; r2 = X x1 - M x2 + B^T x3 ; r3 = B x2 ; r4 = B x1,  X = c1 M + c2 nu K
+    OpSel Mass{c.coefMass, 1 << 30, 0}, NegMass{c.coefNegMass, 1 << 30, 0}, X{c.coefZX, dim, 0};
+    launch_lincomb(gv, vh(y.v, 0), 0.0, none, Mass, vh(x.v, 0), X, vh(x.v, 1), nprob, s);
+    launch_lincomb(gv, vh(y.v, 1), 0.0, none, X, vh(x.v, 0), NegMass, vh(x.v, 1), nprob, s);
+    launch_fBT(c, y, 0, x, 1, 1.0, s);
+    launch_fBT(c, y, 1, x, 0, 1.0, s);
+    launch_Bv(gv, gp, c.tPm, c.tGm, vh(x.v, 1), none, ph(y.p, 0), 0.0, 1.0, n_f, s);
+    launch_Bv(gv, gp, c.tPm, c.tGm, vh(x.v, 0), none, ph(y.p, 1), 0.0, 1.0, n_f, s);
+  } else {
+    // r1 = tau M x1 + (d^* M + tau L^T) x2 + tau B^T x4 ; r2 = (d M + tau L) x1 - tau/beta M x2 + tau B^T x3
+    // r3 = tau B x2 ; r4 = tau B x1
+    const double tau = c.tau;
+    OpSel G11{c.coefS1, 1 << 30, 0}, G12{c.coefS2, dim, 2}, G21{c.coefS3, dim, 1}, G22{c.coefS4, 1 << 30, 0};
+    launch_lincomb(gv, vh(y.v, 0), 0.0, none, G11, vh(x.v, 0), G12, vh(x.v, 1), nprob, s);
+    launch_lincomb(gv, vh(y.v, 1), 0.0, none, G21, vh(x.v, 0), G22, vh(x.v, 1), nprob, s);
+    launch_fBT(c, y, 0, x, 1, tau, s);
+    launch_fBT(c, y, 1, x, 0, tau, s);
+    launch_Bv(gv, gp, c.tPm, c.tGm, vh(x.v, 1), none, ph(y.p, 0), 0.0, tau, n_f, s);
+    launch_Bv(gv, gp, c.tPm, c.tGm, vh(x.v, 0), none, ph(y.p, 1), 0.0, tau, n_f, s);
+  }
+  launch_counter() += 6;
+}
+
+// Algorithm 2: z = F^{-1} T_r^{-1} GMRES_k(A_k, P~_k, T_l^{-1} (F r)_k, eps)  per frequency,
+// inner GMRES right-preconditioned, x0 = 0, MGS, no restart, |g_{j+1}| <= eps ||s_k|| (C.2 #20)
+void nl_precond_apply(Ctx& c, const double* r, double* z, cudaStream_t s) {
+  const int nf = c.n_f, m = c.inner_maxit;
+  const long LV = 2L * c.dim * c.n_s, LP = 2L * c.n_p;
+  launch_fft_fwd(c, r, s);
+  ++launch_counter();
+  FVec S0{c.Fv, c.Fp};
+  FVec* V = c.nlV.data();
+  FVec Zt = c.nlV[m + 1], U = c.nlV[m + 2];
+  std::vector<double2> hh((size_t)(m + 2) * nf);
+  std::vector<std::complex<double>> H((size_t)nf * (m + 1) * m), cs((size_t)nf * m), sn((size_t)nf * m),
+      g((size_t)nf * (m + 1));
+  std::vector<double> beta(nf);
+  std::vector<int> its(nf, 0), done(nf, 0);
+  // beta_k = ||s_k||, V_0 = s / beta_k
+  launch_fdot(S0, S0, LV, LP, nf, c.nlPart, c.nlH, 1, s);
+  CK(cudaMemcpyAsync(hh.data(), c.nlH, nf * sizeof(double2), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int k = 0; k < nf; ++k) {
+    beta[k] = hh[k].x;
+    done[k] = beta[k] == 0.0;
+    g[(size_t)k * (m + 1)] = beta[k];
+  }
+  CK(cudaMemcpyAsync(c.nlFrozen, done.data(), nf * sizeof(int), cudaMemcpyHostToDevice, s));
+  launch_fscale(V[0], S0, c.nlH, c.nlFrozen, LV, LP, nf, s);
+  launch_counter() += 3;
+  int jmax = 0;
+  for (int j = 0; j < m; ++j) {
+    bool all = true;
+    for (int k = 0; k < nf; ++k) all = all && done[k];
+    if (all) break;
+    pt_apply(c, V[j], Zt, s);
+    op_apply(c, Zt, V[j + 1], s);
+    for (int i = 0; i <= j; ++i) {                       // modified Gram-Schmidt, per frequency
+      launch_fdot(V[i], V[j + 1], LV, LP, nf, c.nlPart, c.nlH + (size_t)i * nf, 0, s);
+      launch_faxpy(V[j + 1], V[i], c.nlH + (size_t)i * nf, -1.0, LV, LP, nf, s);
+      launch_counter() += 3;
+    }
+    launch_fdot(V[j + 1], V[j + 1], LV, LP, nf, c.nlPart, c.nlH + (size_t)(j + 1) * nf, 1, s);
+    launch_counter() += 2;
+    CK(cudaMemcpyAsync(hh.data(), c.nlH, (size_t)(j + 2) * nf * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    jmax = j + 1;
+    for (int k = 0; k < nf; ++k) {
+      if (done[k]) continue;
+      std::complex<double>* Hk = &H[(size_t)k * (m + 1) * m];
+      for (int i = 0; i <= j + 1; ++i) Hk[(size_t)i * m + j] = std::complex<double>(hh[(size_t)i * nf + k].x, hh[(size_t)i * nf + k].y);
+      std::complex<double>* csk = &cs[(size_t)k * m];
+      std::complex<double>* snk = &sn[(size_t)k * m];
+      std::complex<double>* gk = &g[(size_t)k * (m + 1)];
+      for (int i = 0; i < j; ++i) {                      // previous complex Givens rotations
+        const std::complex<double> t = std::conj(csk[i]) * Hk[(size_t)i * m + j] + std::conj(snk[i]) * Hk[(size_t)(i + 1) * m + j];
+        Hk[(size_t)(i + 1) * m + j] = -snk[i] * Hk[(size_t)i * m + j] + csk[i] * Hk[(size_t)(i + 1) * m + j];
+        Hk[(size_t)i * m + j] = t;
+      }
+      const std::complex<double> a = Hk[(size_t)j * m + j], b = Hk[(size_t)(j + 1) * m + j];
+      const double den = std::sqrt(std::norm(a) + std::norm(b));
+      csk[j] = a / den;
+      snk[j] = b / den;
+      Hk[(size_t)j * m + j] = den;
+      Hk[(size_t)(j + 1) * m + j] = 0.0;
+      gk[j + 1] = -snk[j] * gk[j];
+      gk[j] = std::conj(csk[j]) * gk[j];
+      its[k] = j + 1;
+      if (std::abs(gk[j + 1]) <= c.inner_eps * beta[k] || std::abs(b) < 1e-14 * beta[k]) done[k] = 1;
+    }
+    CK(cudaMemcpyAsync(c.nlFrozen, done.data(), nf * sizeof(int), cudaMemcpyHostToDevice, s));
+    launch_fscale(V[j + 1], V[j + 1], c.nlH + (size_t)(j + 1) * nf, c.nlFrozen, LV, LP, nf, s);
+    ++launch_counter();
+  }
+  // y_k = H_k^{-1} g_k (its_k columns), u_k = sum_i y_k[i] V_i,k, x = P~(u)
+  std::vector<double2> Y((size_t)nf * std::max(jmax, 1), make_double2(0.0, 0.0));
+  c.inner_its = its;
+  for (int k = 0; k < nf; ++k) {
+    const int n = its[k];
+    const std::complex<double>* Hk = &H[(size_t)k * (m + 1) * m];
+    const std::complex<double>* gk = &g[(size_t)k * (m + 1)];
+    std::vector<std::complex<double>> y(n);
+    for (int i = n - 1; i >= 0; --i) {
+      std::complex<double> acc = gk[i];
+      for (int l = i + 1; l < n; ++l) acc -= Hk[(size_t)i * m + l] * y[l];
+      y[i] = acc / Hk[(size_t)i * m + i];
+    }
+    for (int i = 0; i < n; ++i) Y[(size_t)k * std::max(jmax, 1) + i] = make_double2(y[i].real(), y[i].imag());
+    c.inner_total += n;
+    c.inner_max = std::max(c.inner_max, n);
+  }
+  CK(cudaMemcpyAsync(c.nlY, Y.data(), Y.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+  launch_fmulti(U, c.nlVdev, c.nlY, std::max(jmax, 1), LV, LP, nf, s);
+  pt_apply(c, U, Zt, s);
+  c.debug_block_src_v = Zt.v;
+  c.debug_block_src_p = Zt.p;
+  launch_fft_inv_from(c, Zt, z, s);
+  launch_counter() += 2;
+  CK(cudaStreamSynchronize(s));   // host vectors H, g, Y go out of scope
+}
+
 void precond_apply(Ctx& c, const double* r, double* z, cudaStream_t s) {
+  if (c.nonlinear) {
+    nl_precond_apply(c, r, z, s);
+    return;
+  }
+  c.debug_block_src_v = c.debug_block_src_p = nullptr;
   if (c.timing) cudaEventRecord(c.ev[0], s);
   launch_fft_fwd(c, r, s);
   ++launch_counter();
@@ -1062,6 +1250,12 @@ void gmres_alloc(Ctx& c, int m) {
   std::vector<double*> ptr(m + 1);
   for (int i = 0; i <= m; ++i) ptr[i] = c.gV + (size_t)i * N;
   c.gVptr = upload(c, ptr);
+  if (c.nonlinear) {   // FGMRES stores the preconditioned vectors Z_k = P_k^{-1} v_k
+    c.gZ = dalloc<double>(c, (size_t)m * N);
+    std::vector<double*> zp(m);
+    for (int i = 0; i < m; ++i) zp[i] = c.gZ + (size_t)i * N;
+    c.gZptr = upload(c, zp);
+  }
   CK(cudaMallocHost(&c.hostH, sizeof(double) * (m + 2) * 2));
   c.gm_m = m;
 }
@@ -1082,6 +1276,8 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
   auto t0 = std::chrono::steady_clock::now();
   aao_info inf;
   std::memset(&inf, 0, sizeof(inf));
+  const long inner0 = c.inner_total;
+  c.inner_max = 0;
   const double bnorm = dot_host(c, b, b, 1, s);
   int nh = 0;
   if (bnorm == 0.0) {
@@ -1110,8 +1306,9 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
     for (int k = 0; k < m; ++k) {
       double* Vk = c.gV + (size_t)k * N;
       double* w = c.gV + (size_t)(k + 1) * N;
-      precond_apply(c, Vk, c.gz, s);
-      kkt_apply(c, c.gz, w, s);
+      double* zk = c.nonlinear ? c.gZ + (size_t)k * N : c.gz;
+      precond_apply(c, Vk, zk, s);
+      kkt_apply(c, zk, w, s);
       inf.precond_applies++;
       // modified Gram-Schmidt, device-resident coefficients, one cooperative launch
       double* hcol = c.gH + (size_t)k * (m + 1);
@@ -1164,10 +1361,15 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
       y[i] = acc / H[(size_t)i * m + i];
     }
     CK(cudaMemcpyAsync(c.gscal + 8, y.data(), sizeof(double) * kdone, cudaMemcpyHostToDevice, s));
-    launch_multi_axpy(c.gu, (const double* const*)c.gVptr, c.gscal + 8, kdone, N, s);
-    ++launch_counter();
-    precond_apply(c, c.gu, c.gz, s);
-    inf.precond_applies++;
+    if (c.nonlinear) {   // FGMRES: x += Z_k y
+      launch_multi_axpy(c.gz, (const double* const*)c.gZptr, c.gscal + 8, kdone, N, s);
+      ++launch_counter();
+    } else {             // GMRES: x += P^{-1}(V_k y)
+      launch_multi_axpy(c.gu, (const double* const*)c.gVptr, c.gscal + 8, kdone, N, s);
+      ++launch_counter();
+      precond_apply(c, c.gu, c.gz, s);
+      inf.precond_applies++;
+    }
     launch_axpy(x, c.gz, 1.0, N, s);
     kkt_apply(c, x, c.gz, s);
     launch_copy_sub(c.gr, b, c.gz, N, s);
@@ -1177,6 +1379,8 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
     inf.restarts++;
   }
   inf.iterations = it;
+  inf.inner_its_total = c.inner_total - inner0;
+  inf.inner_its_max = c.inner_max;
   inf.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (info) *info = inf;
   return inf.converged ? AAO_OK : AAO_NOT_CONVERGED;
@@ -1234,6 +1438,9 @@ void aao_config_defaults(aao_config* cfg) {
   cfg->cheb_iters = 10;
   cfg->uzawa_iters = 6;
   cfg->uzawa_mu = 0.75;
+  cfg->pmode = AAO_PRECOND_LINEAR;
+  cfg->inner_eps = 1e-2;
+  cfg->inner_maxit = 60;
 }
 
 aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
@@ -1244,7 +1451,9 @@ aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
   if ((cfg->dim != 2 && cfg->dim != 3) || !pow2 || cfg->n_t < 3 || !(cfg->T > 0) || !(cfg->beta > 0) ||
       !(cfg->nu > 0) || !(cfg->x_hi > cfg->x_lo) || (cfg->problem != AAO_STOKES && cfg->problem != AAO_OSEEN) ||
       (cfg->problem == AAO_OSEEN && cfg->wind_q2 == nullptr) || cfg->mg_cycles < 1 || cfg->cheb_iters < 1 ||
-      cfg->uzawa_iters < 1 || !(cfg->uzawa_mu > 0) || cfg->pre_sweeps < 0 || cfg->post_sweeps < 0)
+      cfg->uzawa_iters < 1 || !(cfg->uzawa_mu > 0) || cfg->pre_sweeps < 0 || cfg->post_sweeps < 0 ||
+      (cfg->pmode != AAO_PRECOND_LINEAR && cfg->pmode != AAO_PRECOND_NONLINEAR) ||
+      (cfg->pmode == AAO_PRECOND_NONLINEAR && (!(cfg->inner_eps > 0) || !(cfg->inner_eps < 1) || cfg->inner_maxit < 1)))
     return AAO_ERR_CONFIG;
   aao_ctx* ctx = new aao_ctx();
   try {
@@ -1356,6 +1565,13 @@ aao_status aao_debug_freq_block(aao_ctx* ctx, int k, double* out, void* stream) 
     cudaFree(tmp);
   });
   return AAO_OK;
+}
+
+int aao_last_inner_iterations(const aao_ctx* ctx, int* out, int cap) {
+  if (!ctx || !out || cap < 0) return AAO_ERR_SHAPE;
+  const int n = std::min<int>(cap, (int)ctx->c.inner_its.size());
+  for (int i = 0; i < n; ++i) out[i] = ctx->c.inner_its[i];
+  return n;
 }
 
 aao_status aao_set_timing(aao_ctx* ctx, int on) {

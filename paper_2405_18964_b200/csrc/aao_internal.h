@@ -78,6 +78,12 @@ struct MGArgs {
   long sm_x[MG_MAXL], sm_b[MG_MAXL];
 };
 
+// a frequency vector: velocity part [k][half][comp][node] and pressure part [k][half][node] (complex)
+struct FVec {
+  double2* v;
+  double2* p;
+};
+
 struct MGSpace {       // an MG hierarchy for one space, with batch workspace
   int order;
   int nlev;
@@ -113,11 +119,27 @@ struct Ctx {
   double2 *Cr = nullptr, *Cd0 = nullptr, *Cd1 = nullptr;
   // operator coefficient tables (device)
   Coef *coefW = nullptr, *coefKp = nullptr, *coefMass = nullptr;
+  Coef *coefZX = nullptr, *coefNegMass = nullptr;  // Z_k apply (Algorithm 2, Stokes)
   Coef *coefQ = nullptr, *coefQH = nullptr;        // MG operators Q_k, Q_k^H (per k)
   Coef *coefU1 = nullptr, *coefU2 = nullptr, *coefU3 = nullptr, *coefU4 = nullptr;  // Uzawa combos
   Coef *coefS1 = nullptr, *coefS2 = nullptr, *coefS3 = nullptr, *coefS4 = nullptr;  // Schur combos
   // coarse-grid inverses
   double2 *invW = nullptr, *invKp = nullptr, *invQ = nullptr, *invQH = nullptr;
+  // nonlinear preconditioner (Algorithm 2): batched inner GMRES per frequency
+  bool nonlinear = false;
+  double inner_eps = 1e-2;
+  int inner_maxit = 0;                   // basis size actually allocated
+  std::vector<FVec> nlV;                 // basis V_0..V_m (device), then Zt, U
+  FVec* nlVdev = nullptr;                // device copy of the basis descriptors
+  double2 *nlH = nullptr, *nlPart = nullptr, *nlY = nullptr;
+  int* nlFrozen = nullptr;
+  std::vector<int> inner_its;            // per frequency, last application
+  long inner_total = 0;
+  int inner_max = 0;
+  double2* debug_block_src_v = nullptr;  // frequency vector of the last NL solution (debug block)
+  double2* debug_block_src_p = nullptr;
+  double* gZ = nullptr;                  // FGMRES preconditioned basis
+  double** gZptr = nullptr;
   // GMRES workspace (allocated on first solve)
   int gm_m = 0;
   double *gV = nullptr, *gz = nullptr, *gw = nullptr, *gu = nullptr, *gr = nullptr;
@@ -199,6 +221,19 @@ void launch_kkt(const Ctx& c, const double* x, double* y, cudaStream_t s);
 void launch_mask_copy(const Ctx& c, const double* in, double* out, cudaStream_t s);
 void launch_rhs(const Ctx& c, const double* vd, double* b, cudaStream_t s);
 void launch_debug_block(const Ctx& c, int k, double2* out, cudaStream_t s);
+
+// frequency-vector kernels (kernels_freq.cu)
+void launch_fdot(FVec a, FVec b, long LV, long LP, int nf, double2* partial, double2* out, int mode, cudaStream_t s);
+size_t fdot_partial_len(int nf);
+void launch_faxpy(FVec y, FVec x, const double2* coef, double sign, long LV, long LP, int nf, cudaStream_t s);
+void launch_fscale(FVec y, FVec x, const double2* den, const int* frozen, long LV, long LP, int nf, cudaStream_t s);
+void launch_fmulti(FVec u, const FVec* V, const double2* Y, int m, long LV, long LP, int nf, cudaStream_t s);
+void launch_combine_p(double2* out, const double2* A, const double2* B, const FreqConst* fc, double nu, long LP, int nf,
+                      cudaStream_t s);
+void launch_oseen_scatter(FVec out, const double2* X1, const double2* X2, const double2* XpA, double pscale,
+                          long ncomp_nodes, long LP, int nf, cudaStream_t s);
+void launch_fBT(const Ctx& c, FVec out, int h, FVec q, int qh, double sc, cudaStream_t s);
+void launch_fft_inv_from(const Ctx& c, FVec x, double* z, cudaStream_t s);   // T_r^{-1} (Stokes) + inverse DFT of x
 
 // blas (kernels_blas.cu): deterministic two-stage reductions
 void launch_dot(const double* x, const double* y, long n, double* partial, int nblk, double* out,

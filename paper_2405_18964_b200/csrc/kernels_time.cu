@@ -69,12 +69,15 @@ __device__ __forceinline__ void slot_values(const Geo& G, const InvSrc& S, const
     const double2 a0 = S.pA[k * S.pstride + node];
     const double2 a1 = S.pA[k * S.pstride + S.phoff + node];
     if (S.stokes) {
-      // x3 = (1+c1) K_p^{-1} s3 + nu c2 M_p^{-1} s3, same for x4
-      const double2 b0 = S.pB[k * S.pstride + node];
-      const double2 b1 = S.pB[k * S.pstride + S.phoff + node];
-      const double ca = 1.0 + f.c1, cb = G.nu * f.c2;
-      const double2 x3 = make_double2(ca * a0.x + cb * b0.x, ca * a0.y + cb * b0.y);
-      const double2 x4 = make_double2(ca * a1.x + cb * b1.x, ca * a1.y + cb * b1.y);
+      // x3 = (1+c1) K_p^{-1} s3 + nu c2 M_p^{-1} s3, same for x4 (pB == nullptr: already combined)
+      double2 x3 = a0, x4 = a1;
+      if (S.pB) {
+        const double2 b0 = S.pB[k * S.pstride + node];
+        const double2 b1 = S.pB[k * S.pstride + S.phoff + node];
+        const double ca = 1.0 + f.c1, cb = G.nu * f.c2;
+        x3 = make_double2(ca * a0.x + cb * b0.x, ca * a0.y + cb * b0.y);
+        x4 = make_double2(ca * a1.x + cb * b1.x, ca * a1.y + cb * b1.y);
+      }
       // T_r^{-1}: y4 = x4 / sqrt(tau); y3 = (x3 + i (dc c2 / sqrt(tau)) y4) / (sqrt(tau) c2)
       const double2 yy4 = make_double2(x4.x / st, x4.y / st);
       const double a = f.dc * f.c2 / st, den = st * f.c2;
@@ -632,8 +635,32 @@ void launch_fft_inv(const Ctx& c, double* z, cudaStream_t s) {
   k_fft_inv<<<grd, blk, si, s>>>(geo_of(c), src_of(c), z, c.fc, c.tw, TD);
 }
 
+InvSrc src_of_fvec(const Ctx& c, FVec x) {
+  InvSrc S;
+  S.v1 = x.v;
+  S.v2 = x.v + (long)c.dim * c.n_s;
+  S.vstride = 2L * c.dim * c.n_s;
+  S.pA = x.p;
+  S.pB = nullptr;
+  S.pstride = 2L * c.n_p;
+  S.phoff = c.n_p;
+  S.stokes = c.oseen ? 0 : 1;
+  S.pscale = 1.0;
+  return S;
+}
+
 void launch_debug_block(const Ctx& c, int k, double2* out, cudaStream_t s) {
-  k_debug_block<<<(unsigned)((c.nblk + 255) / 256), 256, 0, s>>>(geo_of(c), src_of(c), c.fc, k, out);
+  const InvSrc S = c.debug_block_src_v ? src_of_fvec(c, FVec{c.debug_block_src_v, c.debug_block_src_p}) : src_of(c);
+  k_debug_block<<<(unsigned)((c.nblk + 255) / 256), 256, 0, s>>>(geo_of(c), S, c.fc, k, out);
+}
+
+void launch_fft_inv_from(const Ctx& c, FVec x, double* z, cudaStream_t s) {
+  size_t sf, si;
+  const int TD = tile_width(c.n_b, c.n_f, &sf, &si);
+  cudaFuncSetAttribute(k_fft_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)si);
+  dim3 blk(TD, 256 / TD);
+  dim3 grd((unsigned)((c.nblk + TD - 1) / TD));
+  k_fft_inv<<<grd, blk, si, s>>>(geo_of(c), src_of_fvec(c, x), z, c.fc, c.tw, TD);
 }
 
 void launch_kkt(const Ctx& c, const double* x, double* y, cudaStream_t s) {

@@ -17,6 +17,7 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 from oracle import gmres, kkt, precond  # noqa: E402
+from oracle.nonlinear import OracleNonlinearPreconditioner, fgmres  # noqa: E402
 from oracle.problem import Problem  # noqa: E402
 
 CASES = {
@@ -26,6 +27,10 @@ CASES = {
     "oseen_small": synth.small_config("oseen_small", 2, 8, 8, problem="oseen", lo=-1.0, hi=1.0,
                                       beta=1e-3, nu=1.0 / 20.0, index=3),
     "stokes3d_small": synth.small_config("stokes3d_small", 3, 4, 6, beta=1e-3, nu=1e-2, index=5),
+    # Algorithm 2 + FGMRES(10) (NEXT-1), eps = 1e-2
+    "nl_stokes_small": synth.small_config("nl_stokes_small", 2, 8, 10, beta=1e-2, nu=1e-2, index=1),
+    "nl_oseen_small": synth.small_config("nl_oseen_small", 2, 8, 8, problem="oseen", lo=-1.0, hi=1.0,
+                                         beta=1e-3, nu=1.0 / 20.0, index=3),
 }
 
 
@@ -33,9 +38,13 @@ def run(name):
     cfg = CASES[name]
     t0 = time.time()
     prob = Problem(cfg, synth.wind(cfg))
-    pc = precond.OraclePreconditioner(prob)
     b = kkt.build_rhs(prob, synth.desired_state(cfg))
-    x, hist, info = gmres.gmres(lambda v: kkt.kkt_apply(prob, v), pc.apply, b, tol=1e-6, restart=30)
+    if name.startswith("nl_"):
+        pc = OracleNonlinearPreconditioner(prob, inner_eps=1e-2, inner_maxit=60)
+        x, hist, info = fgmres(lambda v: kkt.kkt_apply(prob, v), pc.apply, b, tol=1e-6, restart=10)
+    else:
+        pc = precond.OraclePreconditioner(prob)
+        x, hist, info = gmres.gmres(lambda v: kkt.kkt_apply(prob, v), pc.apply, b, tol=1e-6, restart=30)
     out = dict(case=name, config=cfg.__dict__, iterations=info["iterations"], restarts=info["restarts"],
                converged=info["converged"], true_relres=[float(v) for v in info["true_relres"]],
                hist=[float(h) for h in hist], oracle_seconds=time.time() - t0,

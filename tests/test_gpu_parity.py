@@ -220,3 +220,46 @@ def test_per_level_launch_mode_matches_oracle(cfg, monkeypatch):
     r = synth.probe_vector(cfg)
     z = ctx.precond_apply(torch.from_numpy(r).cuda()).cpu().numpy()
     assert rel(z, pc.apply(r)) <= PRECOND_TOL
+
+
+# ---------------------------------------------------------------------------- Algorithm 2 (NEXT-1)
+NL_CASES = [
+    synth.small_config("nl_s2d", 2, 8, 10, beta=1e-2, nu=1e-2),
+    synth.small_config("nl_o2d", 2, 8, 8, problem="oseen", lo=-1.0, hi=1.0, beta=1e-3, nu=1 / 20, index=3),
+    synth.small_config("nl_s3d", 3, 4, 6, beta=1e-3, nu=1e-2, index=5),
+]
+
+
+@pytest.mark.parametrize("cfg", NL_CASES, ids=lambda c: c.name)
+def test_nonlinear_precond_parity(cfg):
+    """Algorithm 2 (inner GMRES per frequency to eps = 1e-2): same inner iteration counts per frequency
+    and <= 1e-10 agreement of the (nonlinear) preconditioner application (SURVEY C.2 #28)."""
+    torch = _torch()
+    from oracle.nonlinear import OracleNonlinearPreconditioner
+    from oracle.problem import Problem
+    from paper_2405_18964_b200 import Context
+    prob = Problem(cfg, synth.wind(cfg))
+    pc = OracleNonlinearPreconditioner(prob, inner_eps=1e-2, inner_maxit=60, cache_blocks=False)
+    ctx = Context.from_config(cfg, synth.wind(cfg), nonlinear=True, inner_eps=1e-2, inner_maxit=60)
+    r = synth.probe_vector(cfg)
+    z = ctx.precond_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    zo = pc.apply(r)
+    gpu_its = ctx.last_inner_iterations()
+    assert gpu_its == [pc.last_inner[k] for k in range(cfg.n_f)]
+    assert rel(z, zo) <= PRECOND_TOL
+
+
+@pytest.mark.parametrize("name", ["nl_stokes_small", "nl_oseen_small"])
+def test_fgmres_nonlinear_history_parity(name):
+    torch = _torch()
+    from paper_2405_18964_b200 import Context
+    ref = _golden(name)
+    c = ref["config"]
+    cfg = synth.small_config(name, c["dim"], c["n_cells"], c["n_t"], problem=c["problem"], beta=c["beta"],
+                             nu=c["nu"], lo=c["x_lo"], hi=c["x_hi"], index=c["index"])
+    ctx = Context.from_config(cfg, synth.wind(cfg), nonlinear=True, inner_eps=1e-2, inner_maxit=60)
+    b = ctx.build_rhs(synth.desired_state(cfg))
+    x, info, hist, rc = ctx.gmres_solve(b, tol=1e-6, restart=10)
+    assert abs(info["iterations"] - ref["iterations"]) <= 1 and info["converged"] == 1
+    n = min(len(hist), len(ref["hist"]))
+    assert np.max(np.abs(np.array(hist[:n]) - np.array(ref["hist"][:n])) / np.array(ref["hist"][:n])) <= 1e-8
