@@ -274,6 +274,24 @@ def run_ours(args):
     e2e_s, its_e2e_all = aggregate_replicas(time.perf_counter() - t0, its_e2e, world)
     e2e_value = cfg.n_dofs * its_e2e_all / e2e_s
 
+    # ---------------- NEXT-1: Algorithm 2 + FGMRES(10) on the same workload (reported, not the value)
+    nl = None
+    if not args.no_nonlinear:
+        ctx_nl = Context.from_config(cfg, synth.wind(cfg), nonlinear=True, inner_eps=1e-2, inner_maxit=60)
+        b_nl = ctx_nl.build_rhs(synth.desired_state(cfg))
+        ctx_nl.gmres_solve(b_nl, tol=1e-6, restart=10)          # warm-up
+        torch.cuda.synchronize()
+        e0.record(stream)
+        _, info_nl, _, _ = ctx_nl.gmres_solve(b_nl, tol=1e-6, restart=10)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_nl = e0.elapsed_time(e1) / 1e3
+        nl = {"solver": "Algorithm 2 (inner GMRES per frequency, eps 1e-2) + FGMRES(10), tol 1e-6",
+              "fgmres_iterations": info_nl["iterations"], "converged": info_nl["converged"],
+              "inner_avg_per_frequency": info_nl["inner_its_total"] / max(1, info_nl["precond_applies"] * cfg.n_f),
+              "solve_s": t_nl, "dofs_x_outer_its_per_s": cfg.n_dofs * info_nl["iterations"] / t_nl}
+        ctx_nl.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         times, cores = oracle_iteration_sample(cfg, 1, 0)
@@ -299,6 +317,7 @@ def run_ours(args):
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * cfg.n_dofs,
                         "d2h_bytes_per_step": 8 * cfg.n_dofs},
                 "gpu_launches": launches_per_step * args.steps, "launches_per_precond": precond_launches,
+                "nonlinear": nl,
                 "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -314,6 +333,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nonlinear", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
