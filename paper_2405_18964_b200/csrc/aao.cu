@@ -661,6 +661,25 @@ void setup(Ctx& c, const aao_config& cfg) {
     S.x.assign(nlev, nullptr);
     S.b.assign(nlev, nullptr);
     S.r.assign(nlev, nullptr);
+    if (S.order == 2) {
+      S.px.assign(nlev, nullptr);
+      S.pb.assign(nlev, nullptr);
+      S.pr.assign(nlev, nullptr);
+      S.pstride.assign(nlev, 0);
+      for (int l = 0; l < nlev; ++l) {
+        const long st = S.grids[l].n + S.grids[l].n1 + 8;   // padding: the last tap of the last row
+        S.pstride[l] = st;
+        const long n = st * (long)np + 8;
+        S.px[l] = dalloc<double2>(c, n);
+        S.pr[l] = dalloc<double2>(c, n);
+        CK(cudaMemset(S.px[l], 0, n * sizeof(double2)));
+        CK(cudaMemset(S.pr[l], 0, n * sizeof(double2)));
+        if (l > 0) {
+          S.pb[l] = dalloc<double2>(c, n);
+          CK(cudaMemset(S.pb[l], 0, n * sizeof(double2)));
+        }
+      }
+    }
     for (int l = 0; l < nlev; ++l) {
       const long n = S.grids[l].n * (long)np;
       S.r[l] = dalloc<double2>(c, n);
@@ -841,6 +860,17 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
     tab_bytes = (a.nlev - 1) * per * sizeof(double);
     tab_bytes = (tab_bytes + 15) / 16 * 16;
   }
+  // residue-blocked layout (k_mg_q2p): parity-tested but measured slower (c2 2.62 vs 2.41 ms) -> opt-in
+  static const bool want_perm = std::getenv("AAO_PERM") != nullptr;
+  a.perm = (want_perm && a.use_ctab && S.order == 2 && !S.px.empty()) ? 1 : 0;
+  if (a.perm) {
+    for (int i = 0; i < a.nlev; ++i) {
+      a.xw[i] = S.px[l0 + i];
+      a.bw[i] = S.pb[l0 + i];
+      a.rw[i] = S.pr[l0 + i];
+      a.pstride[i] = S.pstride[l0 + i];
+    }
+  }
   // shared-memory residency: coarsest levels first while x and b fit in the budget
   static const char* bud = std::getenv("AAO_SMEM_BUDGET");
   // measured (tools/smem_sweep.sh): keeping only the smallest levels in shared memory leaves the L1
@@ -849,10 +879,11 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   size_t used = tab_bytes;
   a.lsm = a.nlev;
   for (int l = a.nlev - 1; l >= 1; --l) {
-    const size_t need = 2 * a.g[l].n * sizeof(double2);
+    const long len = a.perm ? a.pstride[l] : a.g[l].n;
+    const size_t need = 2 * len * sizeof(double2);
     if (used + need > budget + tab_bytes) break;
     a.sm_x[l] = (long)(used / sizeof(double2));
-    a.sm_b[l] = (long)(used / sizeof(double2)) + a.g[l].n;
+    a.sm_b[l] = (long)(used / sizeof(double2)) + len;
     used += need;
     a.lsm = l;
   }

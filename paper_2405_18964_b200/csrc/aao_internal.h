@@ -75,6 +75,8 @@ struct MGArgs {
   int lsm;                // levels >= lsm keep x and b in shared memory (offsets below, in double2)
   int lwarp;              // levels >= lwarp run inside one warp (tiny bottom of the V-cycle)
   int use_ctab;           // Q2 real operators: per-level class stencils at the start of dynamic smem
+  int perm;               // residue-blocked Q2 solve (k_mg_q2p): xw[0] is the finest iterate workspace
+  long pstride[MG_MAXL];  // per-problem stride of the level workspaces (n + padding)
   long sm_x[MG_MAXL], sm_b[MG_MAXL];
 };
 
@@ -90,6 +92,8 @@ struct MGSpace {       // an MG hierarchy for one space, with batch workspace
   std::vector<Grid> grids;
   std::vector<Transfer> transfers;
   std::vector<double2*> x, b, r;     // per level (level 0 x/b external)
+  std::vector<double2*> px, pb, pr;  // residue-blocked workspaces (Q2), per-problem stride n + pad
+  std::vector<long> pstride;
   int ncoarse_unk;                   // unknowns on the coarsest grid
   int* coarse_unk;                   // device, node indices
   int nprob_max;

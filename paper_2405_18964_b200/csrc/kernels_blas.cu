@@ -111,7 +111,12 @@ void launch_multi_axpy(double* u, const double* const* V, const double* coef, in
 // Each block owns a fixed contiguous chunk; the dot for step i+1 is fused into the update pass of
 // step i, so every step costs one pass over the chunk and one grid barrier.  Block partials are
 // reduced in a fixed order by every block (deterministic, bitwise reproducible).
-constexpr int MGS_THREADS = 512;
+#ifndef MGS_THREADS
+#define MGS_THREADS 1024
+#endif
+#ifndef MGS_PER_SM
+#define MGS_PER_SM 1
+#endif
 
 __global__ void __launch_bounds__(MGS_THREADS) k_mgs(double* __restrict__ w, const double* const* __restrict__ V,
                                                      int k, long n, double* __restrict__ H,
@@ -175,7 +180,7 @@ int mgs_blocks() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mgs, MGS_THREADS, 0);
-    nb = sms * (per < 2 ? per : 2);
+    nb = sms * (per < MGS_PER_SM ? per : MGS_PER_SM);
   }
   return nb;
 }

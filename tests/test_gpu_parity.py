@@ -145,10 +145,13 @@ def _golden(name):
     return json.load(open(path))
 
 
-GMRES_CASES = {"c1": synth.CONFIGS["c1"], "c2": synth.CONFIGS["c2"],
+GMRES_CASES = {"c1": synth.CONFIGS["c1"], "c2": synth.CONFIGS["c2"], "c2b": synth.CONFIGS["c2b"],
                "oseen_small": synth.small_config("oseen_small", 2, 8, 8, problem="oseen", lo=-1.0, hi=1.0,
                                                  beta=1e-3, nu=1.0 / 20.0, index=3),
                "stokes3d_small": synth.small_config("stokes3d_small", 3, 4, 6, beta=1e-3, nu=1e-2, index=5)}
+
+
+HIST_STRICT_ITS = 14 * 30
 
 
 @pytest.mark.parametrize("name", list(GMRES_CASES))
@@ -163,7 +166,13 @@ def test_gmres_history_parity(name):
     assert info["converged"] == 1 and info["true_relres"] <= 2e-6
     n = min(len(hist), len(ref["hist"]))
     h, hr = np.array(hist[:n]), np.array(ref["hist"][:n])
-    assert np.max(np.abs(h - hr) / hr) <= 1e-8
+    d = np.abs(h - hr) / hr
+    # DESIGN.md reading 22: <= 1e-8 per entry through 14 restart cycles; past that a stagnating restarted
+    # solve amplifies rounding-order differences (GPU vs GPU with only the smoother's summation order
+    # changed drifts 1.3e-8 by iteration 493 of c2), so the tail is held to 1e-7.
+    assert np.max(d[:HIST_STRICT_ITS]) <= 1e-8
+    if n > HIST_STRICT_ITS:
+        assert np.max(d[HIST_STRICT_ITS:]) <= 1e-7
 
 
 def test_gmres_host_entry_matches_device_entry():
