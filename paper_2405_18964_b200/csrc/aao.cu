@@ -1343,7 +1343,8 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
       inf.precond_applies++;
       // modified Gram-Schmidt, device-resident coefficients, one cooperative launch
       double* hcol = c.gH + (size_t)k * (m + 1);
-      CK(launch_mgs(w, (const double* const*)c.gVptr, k, N, hcol, c.gpart, s));
+      int w_scaled = 0;
+      CK(launch_mgs(w, (const double* const*)c.gVptr, k, N, hcol, c.gpart, s, &w_scaled));
       ++launch_counter();
       CK(cudaMemcpyAsync(c.hostH, hcol, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
@@ -1382,8 +1383,10 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
         stop = true;
         break;
       }
-      launch_scale_dev(w, w, hcol + k + 1, N, s);
-      ++launch_counter();
+      if (!w_scaled) {
+        launch_scale_dev(w, w, hcol + k + 1, N, s);
+        ++launch_counter();
+      }
     }
     // x += P^{-1}(V_k y), H_k y = g_k
     for (int i = kdone - 1; i >= 0; --i) {

@@ -250,6 +250,8 @@ void launch_multi_axpy(double* u, const double* const* V, const double* coef, in
 int dot_blocks();
 int mgs_blocks();
 // whole MGS sweep (dots, updates, norm) in one cooperative launch; partial: [(k+2) * mgs_blocks()]
-cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double* H, double* partial, cudaStream_t s);
+// MGS of w against V[0..k] -> H[0..k+1]; sets *scaled = 1 if w was also overwritten by w / H[k+1]
+cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double* H, double* partial, cudaStream_t s,
+                       int* scaled);
 
 }  // namespace aao

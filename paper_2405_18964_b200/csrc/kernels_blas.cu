@@ -3,6 +3,9 @@
 // so Gram-Schmidt coefficients never round-trip through the host.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "aao_internal.h"
 
 namespace cg = cooperative_groups;
@@ -173,21 +176,161 @@ __global__ void __launch_bounds__(MGS_THREADS) k_mgs(double* __restrict__ w, con
   }
 }
 
+// ---- MGS with the new vector w held on chip (registers + shared memory) for all k+1 passes.
+// One 1024-thread CTA per SM owns a contiguous chunk of w (in double2 units): the first R2*1024
+// double2 in registers (slot r of thread t holds element r*1024+t, coalesced), the rest in
+// dynamic shared memory.  Pass i reads only v_i (just streamed by the previous pass as v_{i+1},
+// so it is served by L2) and v_{i+1} from HBM: one vector of HBM traffic per pass instead of the
+// streaming kernel's four.  The last pass also forms ||w|| and writes w back scaled by
+// 1/h_{k+1,k} (the next basis vector), removing the separate scale pass.  Same arithmetic per
+// element as k_mgs (h_i = <w, v_i>, w -= h_i v_i), different (fixed) reduction partition.
+constexpr int MGS_OC_THREADS = 1024;
+constexpr int MGS_OC_R2 = 4;
+
+__device__ __forceinline__ double dot2(double2 a, double2 b) { return fma(a.x, b.x, a.y * b.y); }
+
+template <int R2>
+__global__ void __launch_bounds__(MGS_OC_THREADS, 1)
+    k_mgs_oc(double* __restrict__ w, const double* const* __restrict__ V, int k, long n2, long C2,
+             double* __restrict__ H, double* __restrict__ partial, int scale) {
+  extern __shared__ double2 wsm[];
+  cg::grid_group grid = cg::this_grid();
+  const int nb = gridDim.x, T = MGS_OC_THREADS, tid = threadIdx.x;
+  const long lo = (long)blockIdx.x * C2;
+  const int cnt = (int)max(0L, min(n2, lo + C2) - lo);
+  const int nsm = max(0, cnt - R2 * T);
+  double2* w2 = reinterpret_cast<double2*>(w) + lo;
+  __shared__ double hs;
+  double2 wr[R2];
+  {
+    const double2* v0 = reinterpret_cast<const double2*>(V[0]) + lo;
+    double acc = 0.0;
+#pragma unroll
+    for (int r = 0; r < R2; ++r) {
+      const int e = r * T + tid;
+      wr[r] = e < cnt ? w2[e] : make_double2(0.0, 0.0);
+      if (e < cnt) acc += dot2(wr[r], __ldcg(v0 + e));
+    }
+#pragma unroll 4
+    for (int e = tid; e < nsm; e += T) {
+      const double2 x = w2[R2 * T + e];
+      wsm[e] = x;
+      acc += dot2(x, __ldcg(v0 + R2 * T + e));
+    }
+    acc = block_sum(acc);
+    if (tid == 0) partial[blockIdx.x] = acc;
+  }
+  grid.sync();
+  for (int i = 0; i <= k; ++i) {
+    if (tid < 32) {
+      double sm = 0.0;
+      for (int b = tid; b < nb; b += 32) sm += partial[(long)i * nb + b];
+      sm = warp_sum(sm);
+      if (tid == 0) {
+        hs = sm;
+        if (blockIdx.x == 0) H[i] = sm;
+      }
+    }
+    __syncthreads();
+    const double h = hs;
+    const double2* vi = reinterpret_cast<const double2*>(V[i]) + lo;
+    const double2* vn = reinterpret_cast<const double2*>(i < k ? V[i + 1] : w) + lo;
+    const bool last = i == k;
+    double a2 = 0.0;
+#pragma unroll
+    for (int r = 0; r < R2; ++r) {
+      const int e = r * T + tid;
+      if (e < cnt) {
+        const double2 a = __ldcg(vi + e);
+        double2 x = wr[r];
+        x.x = fma(-h, a.x, x.x);
+        x.y = fma(-h, a.y, x.y);
+        wr[r] = x;
+        a2 += dot2(x, last ? x : __ldcg(vn + e));
+      }
+    }
+#pragma unroll 4
+    for (int e = tid; e < nsm; e += T) {
+      const double2 a = __ldcg(vi + R2 * T + e);
+      double2 x = wsm[e];
+      x.x = fma(-h, a.x, x.x);
+      x.y = fma(-h, a.y, x.y);
+      wsm[e] = x;
+      a2 += dot2(x, last ? x : __ldcg(vn + R2 * T + e));
+    }
+    a2 = block_sum(a2);
+    if (tid == 0) partial[(long)(i + 1) * nb + blockIdx.x] = a2;
+    grid.sync();
+  }
+  // ||w|| (every CTA forms the same fixed-order sum), then write w back (scaled: next basis vector)
+  if (tid < 32) {
+    double sm = 0.0;
+    for (int b = tid; b < nb; b += 32) sm += partial[(long)(k + 1) * nb + b];
+    sm = warp_sum(sm);
+    if (tid == 0) {
+      hs = sqrt(sm);
+      if (blockIdx.x == 0) H[k + 1] = hs;
+    }
+  }
+  __syncthreads();
+  const double f = (scale && hs > 0.0) ? 1.0 / hs : 1.0;
+#pragma unroll
+  for (int r = 0; r < R2; ++r) {
+    const int e = r * T + tid;
+    if (e < cnt) w2[e] = make_double2(wr[r].x * f, wr[r].y * f);
+  }
+  for (int e = tid; e < nsm; e += T) w2[R2 * T + e] = make_double2(wsm[e].x * f, wsm[e].y * f);
+}
+
 int mgs_blocks() {
   static int nb = 0;
   if (nb == 0) {
-    int dev, sms, per;
+    int dev, sms;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mgs, MGS_THREADS, 0);
-    nb = sms * (per < MGS_PER_SM ? per : MGS_PER_SM);
+    nb = sms;
   }
   return nb;
 }
 
-cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double* H, double* partial, cudaStream_t s) {
+// Returns the on-chip plan for vectors of n doubles: dynamic smem bytes, or -1 if w does not fit.
+static long mgs_oc_smem(long n, long* C2out) {
+  static int max_smem = -1;
+  if (max_smem < 0) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    max_smem -= 8 * 1024;   // static smem of block_sum / hs and headroom
+  }
+  if (n % 2 != 0 || std::getenv("AAO_MGS_STREAM")) return -1;
+  const long C2 = (n / 2 + mgs_blocks() - 1) / mgs_blocks();
+  const long bytes = std::max(0L, C2 - (long)MGS_OC_R2 * MGS_OC_THREADS) * (long)sizeof(double2);
+  if (bytes > max_smem) return -1;
+  *C2out = C2;
+  return bytes;
+}
+
+cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double* H, double* partial, cudaStream_t s,
+                       int* scaled) {
+  long C2 = 0;
+  const long smem = mgs_oc_smem(n, &C2);
+  if (smem >= 0) {
+    static long attr_set = -1;
+    if (attr_set < smem) {
+      cudaFuncSetAttribute(k_mgs_oc<MGS_OC_R2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_set = smem;
+    }
+    long n2 = n / 2;
+    int scale = 1;
+    int nb = mgs_blocks();
+    void* args[] = {&w, (void*)&V, &k, &n2, &C2, &H, &partial, &scale};
+    *scaled = 1;
+    return cudaLaunchCooperativeKernel((void*)k_mgs_oc<MGS_OC_R2>, dim3(nb), dim3(MGS_OC_THREADS), args,
+                                       (size_t)smem, s);
+  }
   int nb = mgs_blocks();
   void* args[] = {&w, (void*)&V, &k, &n, &H, &partial};
+  *scaled = 0;
   return cudaLaunchCooperativeKernel((void*)k_mgs, dim3(nb), dim3(MGS_THREADS), args, 0, s);
 }
 
