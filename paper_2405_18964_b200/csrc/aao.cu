@@ -538,6 +538,12 @@ void setup(Ctx& c, const aao_config& cfg) {
   c.tPmT = upload(c, L[0].t.PmT);
   c.tGmT = upload(c, L[0].t.GmT);
   c.tMfull = upload(c, L[0].t.M2full);
+  c.h_M2 = L[0].t.M2;
+  c.h_K2 = L[0].t.K2;
+  c.h_Pm = L[0].t.Pm;
+  c.h_Gm = L[0].t.Gm;
+  c.h_PmT = L[0].t.PmT;
+  c.h_GmT = L[0].t.GmT;
 
   // frequency constants: d_k = 1 - exp(-2 pi i k / n_b) (reading C.2 #2)
   const int n_f = c.n_f, n_b = c.n_b;
@@ -896,8 +902,26 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
       a.lwarp = l;
       break;
     }
+  static const char* q2c_env = std::getenv("AAO_Q2C");
+  a.q2c = q2c_env ? std::atoi(q2c_env) : 0;
+  // profiling only: per-level SM-cycle accounting of CTA 0, printed per launch (AAO_MG_CLOCK=1)
+  static const bool mg_clock = std::getenv("AAO_MG_CLOCK") != nullptr;
+  static unsigned long long* clk_dev = nullptr;
+  if (mg_clock) {
+    if (!clk_dev) cudaMalloc(&clk_dev, 2 * MG_MAXL * sizeof(unsigned long long));
+    cudaMemsetAsync(clk_dev, 0, 2 * MG_MAXL * sizeof(unsigned long long), s);
+    a.clk = clk_dev;
+  }
   launch_mg_cta(a, nprob, used, s);
   ++launch_counter();
+  if (mg_clock) {
+    unsigned long long h[2 * MG_MAXL];
+    cudaMemcpyAsync(h, clk_dev, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "mg_clock order %d nprob %d lwarp %d:", S.order, nprob, a.lwarp);
+    for (int l = 0; l < a.nlev - 1; ++l) std::fprintf(stderr, " L%d(n1=%d) %llu/%llu", l, a.g[l].n1, h[2 * l], h[2 * l + 1]);
+    std::fprintf(stderr, " bottom %llu\n", h[2 * MG_MAXL - 1]);
+  }
 }
 
 // schedule: 0 = whole solve CTA-resident, 1 = one launch per level / colour, 2 = hybrid (launches on the

@@ -78,6 +78,8 @@ struct MGArgs {
   int perm;               // residue-blocked Q2 solve (k_mg_q2p): xw[0] is the finest iterate workspace
   long pstride[MG_MAXL];  // per-problem stride of the level workspaces (n + padding)
   long sm_x[MG_MAXL], sm_b[MG_MAXL];
+  int q2c;                  // 2-D Q2 real class stencils: parity sub-lattice sweeps (AAO_Q2C)
+  unsigned long long* clk;  // profiling (AAO_MG_CLOCK): CTA 0 accumulates SM cycles per [level][down, up]
 };
 
 // a frequency vector: velocity part [k][half][comp][node] and pressure part [k][half][node] (complex)
@@ -111,6 +113,7 @@ struct Ctx {
   double *tPm = nullptr, *tGm = nullptr;    // [n1q1][5] B rows: int psi_I phi_j, int psi_I phi_j'
   double *tPmT = nullptr, *tGmT = nullptr;  // [n1q2][3] B^T rows, Q1 cols floor((i-1)/2)+o
   double* tMfull = nullptr;                 // [n1q2][5] un-eliminated Q2 mass rows (RHS)
+  std::vector<double> h_M2, h_K2, h_Pm, h_Gm, h_PmT, h_GmT;  // host copies of the fine 1-D rows
   FreqConst* fc = nullptr;                  // device [n_f]
   std::vector<FreqConst> fch;
   double2* tw = nullptr;                    // [n_b] (cos, sin)(2 pi m / n_b)
@@ -222,6 +225,7 @@ void launch_Bv(const Grid& g2, const Grid& g1, const double* tPm, const double* 
 void launch_fft_fwd(const Ctx& c, const double* r, cudaStream_t s);
 void launch_fft_inv(const Ctx& c, double* z, cudaStream_t s);
 void launch_kkt(const Ctx& c, const double* x, double* y, cudaStream_t s);
+bool launch_kkt_march(const Ctx& c, const double* x, double* y, cudaStream_t s);
 void launch_mask_copy(const Ctx& c, const double* in, double* out, cudaStream_t s);
 void launch_rhs(const Ctx& c, const double* vd, double* b, cudaStream_t s);
 void launch_debug_block(const Ctx& c, int k, double2* out, cudaStream_t s);

@@ -664,6 +664,7 @@ void launch_fft_inv_from(const Ctx& c, FVec x, double* z, cudaStream_t s) {
 }
 
 void launch_kkt(const Ctx& c, const double* x, double* y, cudaStream_t s) {
+  if (launch_kkt_march(c, x, y, s)) return;   // 2-D: time-marching kernel (kernels_kkt.cu)
   KKTTab T;
   T.tM = c.vel.grids[0].tM;
   T.tK = c.vel.grids[0].tK;

@@ -1,0 +1,9 @@
+#!/bin/bash
+# GPU round check: parity tests, bench line, ncu full capture of the dominant MG launch.
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q --timeout 600 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_mg_cta --launch-skip 6 -c 1 \
+  -o gpurun_out/mg_cta_c2 -f python tools/run_precond.py --config c2 --reps 3 > gpurun_out/ncu_full.log 2>&1
+echo "ncu rc=$?" >> gpurun_out/ncu_full.log

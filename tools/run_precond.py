@@ -14,8 +14,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--kkt", action="store_true")
+ap.add_argument("--nt", type=int, default=0, help="override n_t (fewer frequencies, same mesh)")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
+if a.nt:
+    import dataclasses
+    cfg = dataclasses.replace(cfg, n_t=a.nt)
 ctx = Context.from_config(cfg, synth.wind(cfg))
 r = torch.from_numpy(synth.probe_vector(cfg)).cuda()
 z = torch.empty_like(r)
