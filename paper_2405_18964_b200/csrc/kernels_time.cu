@@ -156,6 +156,170 @@ __global__ void k_fft_fwd(Geo G, const double* __restrict__ r, double2* __restri
   }
 }
 
+// Forward transform with the real-input symmetry (the time series are real):
+//   r_hat_k = r_0 + sum_{t=1}^{(n-1)/2} [(r_t + r_{n-t}) cos(2 pi k t / n) - i (r_t - r_{n-t}) sin(2 pi k t / n)]
+//             (+ r_{n/2} (-1)^k for even n)
+// -- half the multiply-adds of the plain sum.  The pair sums/differences are formed in place in shared
+// memory; every thread keeps KB frequencies of one column in registers, so each staged value is read
+// once per KB outputs and each twiddle load is a warp broadcast.
+__device__ __forceinline__ void fwd_store(const Geo& G, double2* __restrict__ Fv, double2* __restrict__ Fp,
+                                          const FreqConst& f, int k, long col, double2 s0, double2 s1, int stokes) {
+  const double st = sqrt(G.tau);
+  if (col < G.n_v) {
+    if (stokes) {
+      const double2 q1 = make_double2(s0.x / st, s0.y / st);
+      const double a = f.dc / st, g = f.c2 / st;
+      s1 = make_double2((s1.x + a * q1.y) * g, (s1.y - a * q1.x) * g);
+      s0 = q1;
+    }
+    const long comp = col / G.n_s, node = col % G.n_s;
+    Fv[(((long)k * 2 + 0) * G.dim + comp) * G.n_s + node] = s0;
+    Fv[(((long)k * 2 + 1) * G.dim + comp) * G.n_s + node] = s1;
+  } else {
+    if (stokes) {
+      const double den = st * f.c2;
+      const double2 q3 = make_double2(s0.x / den, s0.y / den);
+      const double a = f.dc * f.c2 / st;
+      s1 = make_double2((s1.x + a * q3.y) / st, (s1.y - a * q3.x) / st);
+      s0 = q3;
+    }
+    const long node = col - G.n_v;
+    Fp[((long)k * 2 + 0) * G.n_p + node] = s0;
+    Fp[((long)k * 2 + 1) * G.n_p + node] = s1;
+  }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(256) k_fft_fwd_sym(Geo G, const double* __restrict__ r, double2* __restrict__ Fv,
+                                                     double2* __restrict__ Fp, const FreqConst* __restrict__ fc,
+                                                     const double2* __restrict__ tw, int TD, int stokes) {
+  extern __shared__ double sm[];
+  const int n = G.n_b;
+  double2* stw = reinterpret_cast<double2*>(sm);
+  double* xs = sm + 2 * n;  // [2 n][TD]
+  const int tx = threadIdx.x, ty = threadIdx.y, KY = blockDim.y;
+  const int tid = ty * blockDim.x + tx;
+  for (int m = tid; m < n; m += blockDim.x * KY) stw[m] = tw[m];
+  const long col = (long)blockIdx.x * TD + tx;
+  const bool valid = col < G.nblk;
+  const bool msk = !valid || col_masked(G, col);
+  for (int row = ty; row < 2 * n; row += KY)
+    xs[row * TD + tx] = msk ? 0.0 : __ldg(r + (long)row * G.nblk + col);
+  __syncthreads();
+  const int hh = (n - 1) / 2;   // pairs t, n - t (t = 1..hh); even n: t = n/2 unpaired
+  for (int t = 1 + ty; t <= hh; t += KY)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double a = xs[(h * n + t) * TD + tx], b = xs[(h * n + n - t) * TD + tx];
+      xs[(h * n + t) * TD + tx] = a + b;
+      xs[(h * n + n - t) * TD + tx] = a - b;
+    }
+  __syncthreads();
+  if (!valid) return;
+  const bool even = (n & 1) == 0;
+  int kk[KB], m[KB];
+  double re[KB][2], im[KB][2];
+  const double x00 = xs[tx], x10 = xs[n * TD + tx];
+  const double xn0 = even ? xs[(n / 2) * TD + tx] : 0.0, xn1 = even ? xs[(n + n / 2) * TD + tx] : 0.0;
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+    kk[j] = ty + KY * j;
+    m[j] = 0;
+    const double sg = (kk[j] & 1) ? -1.0 : 1.0;
+    re[j][0] = x00 + sg * xn0;
+    re[j][1] = x10 + sg * xn1;
+    im[j][0] = im[j][1] = 0.0;
+  }
+  for (int t = 1; t <= hh; ++t) {
+    const double p0 = xs[t * TD + tx], q0 = xs[(n - t) * TD + tx];
+    const double p1 = xs[(n + t) * TD + tx], q1 = xs[(2 * n - t) * TD + tx];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      m[j] += kk[j];
+      if (m[j] >= n) m[j] -= n;
+      const double2 w = stw[m[j]];
+      re[j][0] = fma(p0, w.x, re[j][0]);
+      im[j][0] = fma(-q0, w.y, im[j][0]);
+      re[j][1] = fma(p1, w.x, re[j][1]);
+      im[j][1] = fma(-q1, w.y, im[j][1]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+    const int k = kk[j];
+    if (k >= G.n_f) continue;
+    fwd_store(G, Fv, Fp, fc[k], k, col, make_double2(re[j][0], im[j][0]), make_double2(re[j][1], im[j][1]), stokes);
+  }
+}
+
+// Inverse transform with the same symmetry: for t and n - t
+//   y_t, y_{n-t} = (1/n) [y_hat_0 + 2 (C_t -+ S_t) (+ Nyquist)],  C_t = sum_k Re y_hat_k cos(2 pi k t / n),
+//   S_t = sum_k Im y_hat_k sin(2 pi k t / n),  k = 1..n_f-1 (even n: y_hat_{n/2} (-1)^t once).
+template <int TB>
+__global__ void __launch_bounds__(256) k_fft_inv_sym(Geo G, InvSrc S, double* __restrict__ z,
+                                                     const FreqConst* __restrict__ fc, const double2* __restrict__ tw,
+                                                     int TD) {
+  extern __shared__ double sm[];
+  const int n = G.n_b, n_f = G.n_f;
+  double2* stw = reinterpret_cast<double2*>(sm);
+  double2* ys = stw + n;  // [2][n_f][TD]
+  const int tx = threadIdx.x, ty = threadIdx.y, KY = blockDim.y;
+  const int tid = ty * blockDim.x + tx;
+  for (int m = tid; m < n; m += blockDim.x * KY) stw[m] = tw[m];
+  const long col = (long)blockIdx.x * TD + tx;
+  const bool valid = col < G.nblk;
+  const bool msk = !valid || col_masked(G, col);
+  for (int k = ty; k < n_f; k += KY) {
+    double2 y0 = make_double2(0, 0), y1 = y0;
+    if (!msk) slot_values(G, S, fc[k], k, col, y0, y1);
+    ys[(0 * n_f + k) * TD + tx] = y0;
+    ys[(1 * n_f + k) * TD + tx] = y1;
+  }
+  __syncthreads();
+  if (!valid) return;
+  const bool even = (n & 1) == 0;
+  const int kend = even ? n_f - 1 : n_f;   // k = 1..kend-1 with weight 2; even n: Nyquist k = n/2 once
+  const int thalf = n / 2;                 // t = 0..thalf (mirror n - t)
+  int tt[TB], m[TB];
+  double C[TB][2], Sn[TB][2];
+#pragma unroll
+  for (int j = 0; j < TB; ++j) {
+    tt[j] = ty + KY * j;
+    m[j] = 0;
+    C[j][0] = C[j][1] = Sn[j][0] = Sn[j][1] = 0.0;
+  }
+  for (int k = 1; k < kend; ++k) {
+    const double2 a = ys[(0 * n_f + k) * TD + tx], b = ys[(1 * n_f + k) * TD + tx];
+#pragma unroll
+    for (int j = 0; j < TB; ++j) {
+      m[j] += tt[j];
+      while (m[j] >= n) m[j] -= n;
+      const double2 w = stw[m[j]];
+      C[j][0] = fma(a.x, w.x, C[j][0]);
+      Sn[j][0] = fma(a.y, w.y, Sn[j][0]);
+      C[j][1] = fma(b.x, w.x, C[j][1]);
+      Sn[j][1] = fma(b.y, w.y, Sn[j][1]);
+    }
+  }
+  const double inv_n = 1.0 / n;
+  const double2 a0 = ys[tx], b0 = ys[n_f * TD + tx];
+  const double2 an = even ? ys[(n_f - 1) * TD + tx] : make_double2(0, 0);
+  const double2 bn = even ? ys[(2 * n_f - 1) * TD + tx] : make_double2(0, 0);
+#pragma unroll
+  for (int j = 0; j < TB; ++j) {
+    const int t = tt[j];
+    if (t > thalf) continue;
+    const double sg = (t & 1) ? -1.0 : 1.0;
+    const double base0 = a0.x + sg * an.x, base1 = b0.x + sg * bn.x;
+    z[(long)t * G.nblk + col] = msk ? 0.0 : (base0 + 2.0 * (C[j][0] - Sn[j][0])) * inv_n;
+    z[(long)(n + t) * G.nblk + col] = msk ? 0.0 : (base1 + 2.0 * (C[j][1] - Sn[j][1])) * inv_n;
+    if (t > 0 && 2 * t != n) {
+      z[(long)(n - t) * G.nblk + col] = msk ? 0.0 : (base0 + 2.0 * (C[j][0] + Sn[j][0])) * inv_n;
+      z[(long)(2 * n - t) * G.nblk + col] = msk ? 0.0 : (base1 + 2.0 * (C[j][1] + Sn[j][1])) * inv_n;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ inverse transform
 __global__ void k_fft_inv(Geo G, InvSrc S, double* __restrict__ z, const FreqConst* __restrict__ fc,
                           const double2* __restrict__ tw, int TD) {
@@ -617,16 +781,59 @@ int tile_width(int n_b, int n_f, size_t* smem_fwd, size_t* smem_inv) {
 
 }  // namespace
 
+namespace {
+bool dense_fft() {
+  static const bool d = std::getenv("AAO_FFT_DENSE") != nullptr;
+  return d;
+}
+// frequencies (forward) / time pairs (inverse) per thread: 1, 2, 4 or 8
+int per_thread(int count, int ky) {
+  const int need = (count + ky - 1) / ky;
+  return need <= 1 ? 1 : (need <= 2 ? 2 : (need <= 4 ? 4 : 8));
+}
+void launch_inv_sym(const Ctx& c, const InvSrc& S, double* z, cudaStream_t s) {
+  size_t sf, si;
+  const int TD = tile_width(c.n_b, c.n_f, &sf, &si);
+  const int KY = 256 / TD;
+  const int TB = per_thread(c.n_b / 2 + 1, KY);
+  dim3 blk(TD, KY), grd((unsigned)((c.nblk + TD - 1) / TD));
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)si);
+    kern<<<grd, blk, si, s>>>(geo_of(c), S, z, c.fc, c.tw, TD);
+  };
+  if (TB == 1) go(k_fft_inv_sym<1>);
+  else if (TB == 2) go(k_fft_inv_sym<2>);
+  else if (TB == 4) go(k_fft_inv_sym<4>);
+  else go(k_fft_inv_sym<8>);
+}
+}  // namespace
+
 void launch_fft_fwd(const Ctx& c, const double* r, cudaStream_t s) {
   size_t sf, si;
   const int TD = tile_width(c.n_b, c.n_f, &sf, &si);
-  cudaFuncSetAttribute(k_fft_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
   dim3 blk(TD, 256 / TD);
   dim3 grd((unsigned)((c.nblk + TD - 1) / TD));
-  k_fft_fwd<<<grd, blk, sf, s>>>(geo_of(c), r, c.Fv, c.Fp, c.fc, c.tw, TD, c.oseen ? 0 : 1);
+  if (dense_fft()) {
+    cudaFuncSetAttribute(k_fft_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
+    k_fft_fwd<<<grd, blk, sf, s>>>(geo_of(c), r, c.Fv, c.Fp, c.fc, c.tw, TD, c.oseen ? 0 : 1);
+    return;
+  }
+  const int KB = per_thread(c.n_f, 256 / TD);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
+    kern<<<grd, blk, sf, s>>>(geo_of(c), r, c.Fv, c.Fp, c.fc, c.tw, TD, c.oseen ? 0 : 1);
+  };
+  if (KB == 1) go(k_fft_fwd_sym<1>);
+  else if (KB == 2) go(k_fft_fwd_sym<2>);
+  else if (KB == 4) go(k_fft_fwd_sym<4>);
+  else go(k_fft_fwd_sym<8>);
 }
 
 void launch_fft_inv(const Ctx& c, double* z, cudaStream_t s) {
+  if (!dense_fft()) {
+    launch_inv_sym(c, src_of(c), z, s);
+    return;
+  }
   size_t sf, si;
   const int TD = tile_width(c.n_b, c.n_f, &sf, &si);
   cudaFuncSetAttribute(k_fft_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)si);
@@ -655,6 +862,10 @@ void launch_debug_block(const Ctx& c, int k, double2* out, cudaStream_t s) {
 }
 
 void launch_fft_inv_from(const Ctx& c, FVec x, double* z, cudaStream_t s) {
+  if (!dense_fft()) {
+    launch_inv_sym(c, src_of_fvec(c, x), z, s);
+    return;
+  }
   size_t sf, si;
   const int TD = tile_width(c.n_b, c.n_f, &sf, &si);
   cudaFuncSetAttribute(k_fft_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)si);

@@ -59,6 +59,10 @@ SMALL = [
     synth.small_config("o2d_even", 2, 16, 7, problem="oseen", lo=-1.0, hi=1.0, beta=1e-2, nu=1 / 20, index=3),
     synth.small_config("s3d", 3, 4, 6, beta=1e-3, nu=1e-2, index=5),
     synth.small_config("s3d_even", 3, 8, 5, beta=1e-2, nu=1e-2, index=5),
+    # long time axes on a tiny mesh: the transform kernels' widest register blocking (n_b = 255, 511)
+    synth.small_config("s2d_nt256", 2, 4, 256, beta=1e-2, nu=1e-2),
+    synth.small_config("s2d_nt512", 2, 4, 512, beta=1e-3, nu=1e-2),
+    synth.small_config("o2d_nt256", 2, 4, 256, problem="oseen", lo=-1.0, hi=1.0, beta=1e-3, nu=1 / 20, index=3),
 ]
 
 
