@@ -994,11 +994,11 @@ __device__ void q2c_residual(const double* tabl, const double2* x, const double2
 template <int DIM, int ORD, bool CONV, bool W, bool TAB>
 __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
                                           const double2* b, int sweeps, bool reverse, double omega, int tid, int nth,
-                                          const double* tabl, bool fast = false) {
+                                          const double* tabl, int fast = 0) {
   constexpr int C1 = ORD == 2 ? 3 : 2;
   constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
   if constexpr (TAB && !CONV && ORD == 2 && DIM == 2) {
-    if (fast) {
+    if (fast == 1 || (fast == 2 && !W)) {
       q2c_sweep<W>(tabl, x, b, g.n1, sweeps, reverse, omega, tid, nth);
       return;
     }
@@ -1098,10 +1098,10 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
   }
   const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
                                                        : ClassTab<DIM>::PER_LEVEL) : nullptr;
-  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl, a.q2c != 0);
+  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl, a.q2c);
   double2* rl = S.R(l);
   const double* cvl = S.CV(l);
-  if (TAB && !CONV && ORD == 2 && DIM == 2 && a.q2c) {
+  if (TAB && !CONV && ORD == 2 && DIM == 2 && (a.q2c == 1 || (a.q2c == 2 && !W))) {
     q2c_residual<W>(tabl, xl, bl, rl, g.n1, tid, nth);
   } else
   cta_all_unknowns<DIM, ORD>(g.n1, tid, nth, [&](const int* c, int i) {
@@ -1226,7 +1226,7 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
   gsync<W>();
   const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
                                                    : ClassTab<DIM>::PER_LEVEL) : nullptr;
-  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl, a.q2c != 0);
+  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl, a.q2c);
 }
 
 template <int DIM, int ORD, bool CONV, bool TAB>

@@ -782,7 +782,7 @@ int tile_width(int n_b, int n_f, size_t* smem_fwd, size_t* smem_inv) {
 }  // namespace
 
 namespace {
-bool dense_fft() {
+bool dense_fft_env() {
   static const bool d = std::getenv("AAO_FFT_DENSE") != nullptr;
   return d;
 }
@@ -791,9 +791,21 @@ int per_thread(int count, int ky) {
   const int need = (count + ky - 1) / ky;
   return need <= 1 ? 1 : (need <= 2 ? 2 : (need <= 4 ? 4 : 8));
 }
+// tile width for the symmetric kernels: fits shared memory and needs at most 8 outputs per thread
+int sym_tile(const Ctx& c, int count, size_t* sf, size_t* si) {
+  int TD = tile_width(c.n_b, c.n_f, sf, si);
+  while (TD > 8 && (count + 256 / TD - 1) / (256 / TD) > 8) TD /= 2;
+  *sf = (size_t)c.n_b * 16 + 2ull * c.n_b * TD * 8;
+  *si = (size_t)c.n_b * 16 + 2ull * c.n_f * TD * 16;
+  return TD;
+}
+// dense (plain-sum) kernels: on request, or when a 256-thread tile cannot cover the outputs in 8 per thread
+bool dense_fft(const Ctx& c) {
+  return dense_fft_env() || (c.n_b / 2 + 1 > 8 * 32) || (c.n_f > 8 * 32);
+}
 void launch_inv_sym(const Ctx& c, const InvSrc& S, double* z, cudaStream_t s) {
   size_t sf, si;
-  const int TD = tile_width(c.n_b, c.n_f, &sf, &si);
+  const int TD = sym_tile(c, c.n_b / 2 + 1, &sf, &si);
   const int KY = 256 / TD;
   const int TB = per_thread(c.n_b / 2 + 1, KY);
   dim3 blk(TD, KY), grd((unsigned)((c.nblk + TD - 1) / TD));
@@ -813,15 +825,18 @@ void launch_fft_fwd(const Ctx& c, const double* r, cudaStream_t s) {
   const int TD = tile_width(c.n_b, c.n_f, &sf, &si);
   dim3 blk(TD, 256 / TD);
   dim3 grd((unsigned)((c.nblk + TD - 1) / TD));
-  if (dense_fft()) {
+  if (dense_fft(c)) {
     cudaFuncSetAttribute(k_fft_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
     k_fft_fwd<<<grd, blk, sf, s>>>(geo_of(c), r, c.Fv, c.Fp, c.fc, c.tw, TD, c.oseen ? 0 : 1);
     return;
   }
-  const int KB = per_thread(c.n_f, 256 / TD);
+  const int TDs = sym_tile(c, c.n_f, &sf, &si);
+  const int KB = per_thread(c.n_f, 256 / TDs);
+  blk = dim3(TDs, 256 / TDs);
+  grd = dim3((unsigned)((c.nblk + TDs - 1) / TDs));
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
-    kern<<<grd, blk, sf, s>>>(geo_of(c), r, c.Fv, c.Fp, c.fc, c.tw, TD, c.oseen ? 0 : 1);
+    kern<<<grd, blk, sf, s>>>(geo_of(c), r, c.Fv, c.Fp, c.fc, c.tw, TDs, c.oseen ? 0 : 1);
   };
   if (KB == 1) go(k_fft_fwd_sym<1>);
   else if (KB == 2) go(k_fft_fwd_sym<2>);
@@ -830,7 +845,7 @@ void launch_fft_fwd(const Ctx& c, const double* r, cudaStream_t s) {
 }
 
 void launch_fft_inv(const Ctx& c, double* z, cudaStream_t s) {
-  if (!dense_fft()) {
+  if (!dense_fft(c)) {
     launch_inv_sym(c, src_of(c), z, s);
     return;
   }
@@ -862,7 +877,7 @@ void launch_debug_block(const Ctx& c, int k, double2* out, cudaStream_t s) {
 }
 
 void launch_fft_inv_from(const Ctx& c, FVec x, double* z, cudaStream_t s) {
-  if (!dense_fft()) {
+  if (!dense_fft(c)) {
     launch_inv_sym(c, src_of_fvec(c, x), z, s);
     return;
   }
