@@ -49,7 +49,7 @@ struct KMArgs {
   double* y;
   const double* conv;    // Oseen: N  [n_s][25] (node-major, taps (ob, oa)); nullptr for Stokes
   const double* convT;   // Oseen: N^T
-  int n1, m1, n_b, ntx, chunk;
+  int n1, m1, n_b, ntx, tiles;
   long nblk, n_s, n_v;
   double tau, tnu, tob;  // tau, tau nu, tau / beta
 };
@@ -98,15 +98,12 @@ __device__ __forceinline__ constexpr bool ytap(int q, int jj) {
   return (jj & 1) ? (q - jj >= 1 && q - jj <= 3) : (q - jj >= 0 && q - jj <= 4);
 }
 
+// one segment: tile `tile`, output time blocks [t0, t1)
 template <bool CONV>
-__global__ void __launch_bounds__(KM_THREADS, 1) k_kkt_march(KMArgs a, KMRows R) {
-  extern __shared__ double kms[];
-  const int tile = blockIdx.x, chunk = blockIdx.y;
+__device__ __forceinline__ void km_segment(const KMArgs& a, const KMRows& R, double* kms, int tile, int t0, int t1) {
   const int tx = tile % a.ntx, ty = tile / a.ntx;
   const int x0 = tx * KM_TX, y0 = ty * KM_TY;
   const int n1 = a.n1, m1 = a.m1, n_b = a.n_b;
-  const int t0 = chunk * a.chunk;
-  const int t1 = min(n_b, t0 + a.chunk);
   const int tid = threadIdx.x, lane = tid & 31, g = tid >> 5;
   const int i0 = x0 + 2 * lane, j0 = y0 + 4 * g;      // velocity: cols i0, i0+1, rows j0..j0+3
   const int Ip = x0 / 2 + lane, Jp = y0 / 2 + 2 * g;  // pressure: col Ip, rows Jp, Jp+1
@@ -417,6 +414,24 @@ __global__ void __launch_bounds__(KM_THREADS, 1) k_kkt_march(KMArgs a, KMRows R)
   }
 }
 
+// Work is the linearised (tile, time block) space, split evenly over the grid (one CTA per SM slot):
+// a CTA marches through at most a few contiguous segments, so there is no partial last wave.
+template <bool CONV>
+__global__ void __launch_bounds__(KM_THREADS, 1) k_kkt_march(KMArgs a, KMRows R) {
+  extern __shared__ double kms[];
+  const long total = (long)a.tiles * a.n_b;
+  const long per = (total + gridDim.x - 1) / gridDim.x;
+  long gbeg = (long)blockIdx.x * per;
+  const long gend = min(total, gbeg + per);
+  while (gbeg < gend) {
+    const int tile = (int)(gbeg / a.n_b), t0 = (int)(gbeg % a.n_b);
+    const int t1 = (int)min((long)a.n_b, t0 + (gend - gbeg));
+    km_segment<CONV>(a, R, kms, tile, t0, t1);
+    gbeg += t1 - t0;
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 // true if the time-marching kernel handles this context (2-D); launched on stream s
@@ -466,11 +481,16 @@ bool launch_kkt_march(const Ctx& c, const double* x, double* y, cudaStream_t s) 
   a.ntx = (c.n1q2 - 1 + KM_TX - 1) / KM_TX;
   const int nty = (c.n1q2 - 1 + KM_TY - 1) / KM_TY;
   const int tiles = a.ntx * nty;
-  // time chunks: enough CTAs for two per SM-slot, chunks of at least 4 blocks
-  int nch = (2 * 148 + tiles - 1) / tiles;
-  nch = std::max(1, std::min(nch, (c.n_b + 3) / 4));
-  a.chunk = (c.n_b + nch - 1) / nch;
-  nch = (c.n_b + a.chunk - 1) / a.chunk;
+  a.tiles = tiles;
+  // one CTA per SM (shared memory bound); at least 4 time blocks per CTA
+  const long total = (long)tiles * c.n_b;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = (int)std::max(1L, std::min((long)sms, (total + 3) / 4));
   const size_t smem = 2 * KM_STAGE * sizeof(double);
   static bool attr = false;
   if (!attr) {
@@ -478,7 +498,6 @@ bool launch_kkt_march(const Ctx& c, const double* x, double* y, cudaStream_t s) 
     cudaFuncSetAttribute(k_kkt_march<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  dim3 grid((unsigned)tiles, (unsigned)nch);
   if (c.oseen)
     k_kkt_march<true><<<grid, KM_THREADS, smem, s>>>(a, R);
   else
