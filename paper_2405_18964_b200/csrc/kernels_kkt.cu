@@ -432,14 +432,350 @@ __global__ void __launch_bounds__(KM_THREADS, 1) k_kkt_march(KMArgs a, KMRows R)
   }
 }
 
+
+// ------------------------------------------------------------------------------------------ 3-D
+// Same time march in 3-D (Stokes).  A CTA owns a 16 x 8 x 8 box of Q2 nodes (+ the boundary layer past
+// the last box in each direction, whose velocity outputs are zeros and whose Q1 nodes are unknowns).
+// The pipeline unit is one (time block, component) sub-step: the component's v and lam boxes (+2 halo)
+// are staged with cp.async while the previous sub-step is computed.  A thread owns one (x, y) column
+// and 4 consecutive z outputs: per staged z-plane it forms the x-direction products on the 3 or 5 rows
+// of its y (y parity is warp-uniform), the y-direction combinations, and scatters them into its 4 z
+// outputs (sum factorisation of M = Mz (x) My (x) Mx, K = Kz My Mx + Mz Ky Mx + Mz My Kx).
+// B^T p, B^T mu (all components) are formed at the component-0 sub-step from the staged Q1 boxes;
+// B v, B lam accumulate over the three component sub-steps (one (Q1 node, field) item per thread).
+constexpr int K3_TX = 16, K3_TY = 8, K3_TZ = 8;
+constexpr int K3_SX = 22, K3_SY = 13, K3_SZ = 13;   // staged: x0-2..x0+19, y0-2..y0+10, z0-2..z0+10
+constexpr int K3_PX = 12, K3_PY = 8, K3_PZ = 8;     // staged Q1: from (x0/2-1, y0/2-1, z0/2-1)
+constexpr int K3_Q2 = K3_SX * K3_SY * K3_SZ, K3_Q1 = K3_PX * K3_PY * K3_PZ;
+constexpr int K3_STAGE = 2 * K3_Q2 + 2 * K3_Q1;     // v_c, lam_c, p, mu
+
+struct K3Args {
+  const double* x;
+  double* y;
+  int n1, m1, n_b, ntx, nty, tiles;
+  long nblk, n_s, n_v;
+  double tau, tnu, tob;
+};
+
+__device__ __forceinline__ void k3_stage(const K3Args& a, double* st, int s, int c, bool wv, bool wl, bool wp,
+                                         int x0, int y0, int z0, int tid) {
+  const int n1 = a.n1, m1 = a.m1;
+  for (int f = 0; f < 2; ++f) {
+    if (!(f == 0 ? wv : wl)) continue;
+    const double* src = a.x + ((long)f * a.n_b + s) * a.nblk + c * a.n_s;
+    double* dst = st + f * K3_Q2;
+    for (int e = tid; e < K3_Q2; e += 256) {
+      const int li = e % K3_SX, r = e / K3_SX, lj = r % K3_SY, lk = r / K3_SY;
+      const int gi = x0 - 2 + li, gj = y0 - 2 + lj, gk = z0 - 2 + lk;
+      const bool ok = gi >= 1 && gi <= n1 - 2 && gj >= 1 && gj <= n1 - 2 && gk >= 1 && gk <= n1 - 2;
+      cp_async8(dst + e, ok ? src + ((long)gk * n1 + gj) * n1 + gi : a.x, ok);
+    }
+  }
+  if (!wp) return;
+  for (int f = 0; f < 2; ++f) {
+    const double* q = a.x + ((long)f * a.n_b + s) * a.nblk + a.n_v;
+    double* dq = st + 2 * K3_Q2 + f * K3_Q1;
+    for (int e = tid; e < K3_Q1; e += 256) {
+      const int li = e % K3_PX, r = e / K3_PX, lj = r % K3_PY, lk = r / K3_PY;
+      const int I = x0 / 2 - 1 + li, J = y0 / 2 - 1 + lj, K = z0 / 2 - 1 + lk;
+      const bool ok = I >= 0 && I < m1 && J >= 0 && J < m1 && K >= 0 && K < m1 && (I | J | K) != 0;
+      cp_async8(dq + e, ok ? q + ((long)K * m1 + J) * m1 + I : a.x, ok);
+    }
+  }
+}
+
+// M and K products of one staged field at the thread's 4 z outputs (PY: y parity of the thread's row)
+template <int PY>
+__device__ __forceinline__ void k3_mk(const KMRows& R, const double* U, int xl, int yl, int zq0, bool xodd,
+                                      double* Mo, double* Ko) {
+  constexpr int B0 = PY ? 1 : 0, B1 = PY ? 4 : 5;
+  double mx[5], kx[5];
+#pragma unroll
+  for (int o = 0; o < 5; ++o) {
+    mx[o] = xodd ? R.mm[o] : R.mv[o];
+    kx[o] = xodd ? R.km[o] : R.kv[o];
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) Mo[r] = Ko[r] = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {   // planes z_out0 - 2 + q
+    const double* P = U + (zq0 + q) * (K3_SX * K3_SY) + yl * K3_SX + xl;
+    double pmm = 0.0, pkm = 0.0, pmk = 0.0;
+#pragma unroll
+    for (int ob = B0; ob < B1; ++ob) {
+      const double* row = P + ob * K3_SX;
+      double rm = 0.0, rk = 0.0;
+#pragma unroll
+      for (int oa = 0; oa < 5; ++oa) {
+        const double u = row[oa];
+        rm = fma(mx[oa], u, rm);
+        rk = fma(kx[oa], u, rk);
+      }
+      const double my = PY ? R.mm[ob] : R.mv[ob], ky = PY ? R.km[ob] : R.kv[ob];
+      pmm = fma(my, rm, pmm);
+      pkm = fma(ky, rm, pkm);
+      pmk = fma(my, rk, pmk);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {   // output z parity = parity of r (z0 and 4 zh even)
+      const int o = q - r;
+      const bool ok = (r & 1) ? (o >= 1 && o <= 3) : (o >= 0 && o <= 4);
+      if (!ok) continue;
+      const double mz = (r & 1) ? R.mm[o] : R.mv[o], kz = (r & 1) ? R.km[o] : R.kv[o];
+      Mo[r] = fma(mz, pmm, Mo[r]);
+      Ko[r] = fma(kz, pmm, fma(mz, pkm + pmk, Ko[r]));
+    }
+  }
+}
+
+// B^T q (all 3 components) at the thread's 4 z outputs from the staged Q1 box
+template <int PY>
+__device__ __forceinline__ void k3_bt(const KMRows& R, const double* Q, int x, int yq0, int zq0, bool xodd,
+                                      double T[3][4]) {
+  // Q1 cols for the thread's x: vertex x = 2e -> e-1..e+1, midpoint 2e+1 -> e..e+2; local = e - 1 - (x0/2 - 1)
+  const int xq0 = (x >> 1) + (xodd ? 1 : 0);   // local Q1 col of tap 0 (x local, x0 even)
+  double fpx[3], fgx[3];
+#pragma unroll
+  for (int o = 0; o < 3; ++o) {
+    fpx[o] = xodd ? R.tpm[o] : R.tpv[o];
+    fgx[o] = xodd ? R.tgm[o] : R.tgv[o];
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) T[c][r] = 0.0;
+#pragma unroll
+  for (int kq = 0; kq < 5; ++kq) {   // Q1 planes zq0 + kq
+    double xy[3] = {0.0, 0.0, 0.0};  // comp 0: Gx Py, comp 1: Px Gy, comp 2: Px Py
+#pragma unroll
+    for (int jq = 0; jq < 3; ++jq) {
+      const double* row = Q + (zq0 + kq) * (K3_PX * K3_PY) + (yq0 + jq) * K3_PX + xq0;
+      double sp = 0.0, sg = 0.0;
+#pragma unroll
+      for (int o = 0; o < 3; ++o) {
+        const double v = row[o];
+        sp = fma(fpx[o], v, sp);
+        sg = fma(fgx[o], v, sg);
+      }
+      const double py = PY ? R.tpm[jq] : R.tpv[jq], gy = PY ? R.tgm[jq] : R.tgv[jq];
+      xy[0] = fma(py, sg, xy[0]);
+      xy[1] = fma(gy, sp, xy[1]);
+      xy[2] = fma(py, sp, xy[2]);
+    }
+    // z: output r uses Q1 planes base(r) + o, base = {0, 1, 1, 2}[r] relative to zq0 (as in 2-D)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int base = r == 0 ? 0 : (r == 3 ? 2 : 1);
+      const int o = kq - base;
+      if (o < 0 || o > 2) continue;
+      const double pz = (r & 1) ? R.tpm[o] : R.tpv[o], gz = (r & 1) ? R.tgm[o] : R.tgv[o];
+      T[0][r] = fma(pz, xy[0], T[0][r]);
+      T[1][r] = fma(pz, xy[1], T[1][r]);
+      T[2][r] = fma(gz, xy[2], T[2][r]);
+    }
+  }
+}
+
+__device__ __forceinline__ void k3_segment(const K3Args& a, const KMRows& R, double* sm, int tile, int t0, int t1) {
+  const int tx = tile % a.ntx, ty = (tile / a.ntx) % a.nty, tz = tile / (a.ntx * a.nty);
+  const int x0 = tx * K3_TX, y0 = ty * K3_TY, z0 = tz * K3_TZ;
+  const int n1 = a.n1, m1 = a.m1, n_b = a.n_b;
+  const bool xlast = x0 + K3_TX == n1 - 1, ylast = y0 + K3_TY == n1 - 1, zlast = z0 + K3_TZ == n1 - 1;
+  const int tid = threadIdx.x, xl = tid & 15, zh = (tid >> 4) & 1, yl = tid >> 5;
+  const int xg = x0 + xl, yg = y0 + yl, zg0 = z0 + 4 * zh;
+  const bool xodd = xg & 1, yodd = yg & 1;
+  const double tau = a.tau, tnu = a.tnu, tob = a.tob;
+  const long nblk = a.nblk, ns = a.n_s;
+  // owned Q1 box (+1 layer past the last tile) and this thread's (node, field) items
+  const int nIx = K3_TX / 2 + (xlast ? 1 : 0), nIy = K3_TY / 2 + (ylast ? 1 : 0), nIz = K3_TZ / 2 + (zlast ? 1 : 0);
+  const int nitems = 2 * nIx * nIy * nIz;
+  double cMv[3][4], cA[3][4], Tp[3][4], Tm[3][4], Bacc[2];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) cMv[c][r] = cA[c][r] = Tp[c][r] = Tm[c][r] = 0.0;
+  const int s_begin = t0 > 0 ? t0 - 1 : 0;
+  const int s_end = t1 < n_b ? t1 : n_b - 1;
+  const int nsub = 3 * (s_end - s_begin + 1);
+  auto stage = [&](int k, double* buf) {
+    const int s = s_begin + k / 3, c = k % 3;
+    const bool pro = s < t0, epi = s >= t1;
+    k3_stage(a, buf, s, c, !epi, !pro, !pro && !epi && c == 0, x0, y0, z0, tid);
+  };
+  stage(0, sm);
+  cp_commit();
+  for (int k = 0; k < nsub; ++k) {
+    if (k + 1 < nsub) {
+      stage(k + 1, sm + ((k + 1) & 1) * K3_STAGE);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const double* st = sm + (k & 1) * K3_STAGE;
+    const int s = s_begin + k / 3, c = k % 3;
+    const bool pro = s < t0, epi = s >= t1, main = !pro && !epi;
+    double Mv[4], Kv[4], Ml[4], Kl[4];
+    if (!epi) {
+      if (yodd) k3_mk<1>(R, st, xl, yl, 4 * zh, xodd, Mv, Kv);
+      else k3_mk<0>(R, st, xl, yl, 4 * zh, xodd, Mv, Kv);
+    }
+    if (!pro) {
+      if (yodd) k3_mk<1>(R, st + K3_Q2, xl, yl, 4 * zh, xodd, Ml, Kl);
+      else k3_mk<0>(R, st + K3_Q2, xl, yl, 4 * zh, xodd, Ml, Kl);
+    }
+    if (main && c == 0) {
+      // Q1 rows/planes of the thread's y and z outputs: local base (y0 even) = yl/2 (+ parity shift)
+      const double* sp = st + 2 * K3_Q2;
+      const int yq0 = (yl >> 1) + (yodd ? 1 : 0), zq0 = 2 * zh;
+      if (yodd) {
+        k3_bt<1>(R, sp, xl, yq0, zq0, xodd, Tp);
+        k3_bt<1>(R, sp + K3_Q1, xl, yq0, zq0, xodd, Tm);
+      } else {
+        k3_bt<0>(R, sp, xl, yq0, zq0, xodd, Tp);
+        k3_bt<0>(R, sp + K3_Q1, xl, yq0, zq0, xodd, Tm);
+      }
+      Bacc[0] = Bacc[1] = 0.0;
+    }
+    const bool rin = xg >= 1 && xg <= n1 - 2 && yg >= 1 && yg <= n1 - 2;
+    if (pro) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) cMv[0][r] = Mv[r];
+    } else {
+      // deferred y1v_{s-1} = A_{s-1} - M lam_s
+      if (s > t0) {
+        double* yo = a.y + (long)(s - 1) * nblk + c * ns;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int zg = zg0 + r;
+          if (xg < n1 && yg < n1 && zg < n1) {
+            const bool in = rin && zg >= 1 && zg <= n1 - 2;
+            yo[((long)zg * n1 + yg) * n1 + xg] = in ? cA[0][r] - Ml[r] : 0.0;
+          }
+        }
+      }
+      if (main) {
+        double* y2 = a.y + ((long)n_b + s) * nblk + c * ns;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int zg = zg0 + r;
+          const double val = Mv[r] - cMv[0][r] - tob * Ml[r] + tnu * Kv[r] - tau * Tp[0][r];
+          if (xg < n1 && yg < n1 && zg < n1) {
+            const bool in = rin && zg >= 1 && zg <= n1 - 2;
+            y2[((long)zg * n1 + yg) * n1 + xg] = in ? val : 0.0;
+          }
+          cMv[0][r] = Mv[r];
+          cA[0][r] = tau * Mv[r] + Ml[r] + tnu * Kl[r] - tau * Tm[0][r];
+        }
+        // pressure rows: B_c v_c and B_c lam_c of the owned Q1 nodes (item = (node, field))
+        const double* bx = c == 0 ? R.bg : R.bp;
+        const double* by = c == 1 ? R.bg : R.bp;
+        const double* bz = c == 2 ? R.bg : R.bp;
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+          const int item = tid + 256 * it;
+          if (item >= nitems) continue;
+          const int f = item & 1, nd = item >> 1;
+          const int Il = nd % nIx, Jl = (nd / nIx) % nIy, Kl2 = nd / (nIx * nIy);
+          const double* U = st + f * K3_Q2;
+          // Q2 cols 2I-2..2I+2 -> local 2 Il (x0 even): box origin x0 - 2
+          double acc = 0.0;
+          for (int oc = 0; oc < 5; ++oc) {
+            double pl = 0.0;
+#pragma unroll
+            for (int ob = 0; ob < 5; ++ob) {
+              const double* row = U + (2 * Kl2 + oc) * (K3_SX * K3_SY) + (2 * Jl + ob) * K3_SX + 2 * Il;
+              double rs = 0.0;
+#pragma unroll
+              for (int oa = 0; oa < 5; ++oa) rs = fma(bx[oa], row[oa], rs);
+              pl = fma(by[ob], rs, pl);
+            }
+            acc = fma(bz[oc], pl, acc);
+          }
+          Bacc[it] += acc;
+        }
+        if (c == 2) {
+#pragma unroll
+          for (int it = 0; it < 2; ++it) {
+            const int item = tid + 256 * it;
+            if (item >= nitems) continue;
+            const int f = item & 1, nd = item >> 1;
+            const int I = x0 / 2 + nd % nIx, J = y0 / 2 + (nd / nIx) % nIy, K = z0 / 2 + nd / (nIx * nIy);
+            if (I >= m1 || J >= m1 || K >= m1) continue;
+            const long pn = ((long)K * m1 + J) * m1 + I;
+            // field 1 (lam) -> y1p (half 0), field 0 (v) -> y2p (half 1)
+            a.y[((long)(f == 1 ? 0 : n_b) + s) * nblk + a.n_v + pn] = pn == 0 ? 0.0 : -tau * Bacc[it];
+          }
+        }
+        // zero velocity outputs on the boundary layer past the last box (all comps at c == 0)
+        if (c == 0 && (xlast || ylast || zlast)) {
+          const int ex = K3_TX + (xlast ? 1 : 0), ey = K3_TY + (ylast ? 1 : 0), ez = K3_TZ + (zlast ? 1 : 0);
+          const int tot = ex * ey * ez;
+          for (int e = tid; e < tot; e += 256) {
+            const int li = e % ex, lj = (e / ex) % ey, lk = e / (ex * ey);
+            if (li < K3_TX && lj < K3_TY && lk < K3_TZ) continue;
+            const int gi = x0 + li, gj = y0 + lj, gk = z0 + lk;
+            if (gi >= n1 || gj >= n1 || gk >= n1) continue;
+            const long nd = ((long)gk * n1 + gj) * n1 + gi;
+            for (int cc = 0; cc < 3; ++cc) {
+              a.y[(long)s * nblk + cc * ns + nd] = 0.0;
+              a.y[((long)n_b + s) * nblk + cc * ns + nd] = 0.0;
+            }
+          }
+        }
+      }
+    }
+    // the current component's carries live in slot 0: rotate so the next component's move there
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      double t;
+      t = cMv[0][r]; cMv[0][r] = cMv[1][r]; cMv[1][r] = cMv[2][r]; cMv[2][r] = t;
+      t = cA[0][r]; cA[0][r] = cA[1][r]; cA[1][r] = cA[2][r]; cA[2][r] = t;
+      t = Tp[0][r]; Tp[0][r] = Tp[1][r]; Tp[1][r] = Tp[2][r]; Tp[2][r] = t;
+      t = Tm[0][r]; Tm[0][r] = Tm[1][r]; Tm[1][r] = Tm[2][r]; Tm[2][r] = t;
+    }
+    __syncthreads();
+  }
+  if (t1 == n_b) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double* yo = a.y + (long)(n_b - 1) * nblk + c * ns;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int zg = zg0 + r;
+        if (xg < n1 && yg < n1 && zg < n1) {
+          const bool in = xg >= 1 && xg <= n1 - 2 && yg >= 1 && yg <= n1 - 2 && zg >= 1 && zg <= n1 - 2;
+          yo[((long)zg * n1 + yg) * n1 + xg] = in ? cA[c][r] : 0.0;
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) k_kkt_march3(K3Args a, KMRows R) {
+  extern __shared__ double k3s[];
+  const long total = (long)a.tiles * a.n_b;
+  const long per = (total + gridDim.x - 1) / gridDim.x;
+  long gbeg = (long)blockIdx.x * per;
+  const long gend = min(total, gbeg + per);
+  while (gbeg < gend) {
+    const int tile = (int)(gbeg / a.n_b), t0 = (int)(gbeg % a.n_b);
+    const int t1 = (int)min((long)a.n_b, t0 + (gend - gbeg));
+    k3_segment(a, R, k3s, tile, t0, t1);
+    gbeg += t1 - t0;
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 // true if the time-marching kernel handles this context (2-D); launched on stream s
 bool launch_kkt_march(const Ctx& c, const double* x, double* y, cudaStream_t s) {
-  if (c.dim != 2) return false;
   static const bool off = std::getenv("AAO_KKT_TILED") != nullptr;
   if (off) return false;
   if (c.n1q2 < 9) return false;   // generic rows need an interior vertex and midpoint (N_c >= 4)
+  if (c.dim == 3 && c.oseen) return false;
   // Oseen: the per-node convection stencils (25 coefficients per node and time block, read through L2)
   // make the marching kernel slower than the tiled one (c3: 2.92 vs 2.07 ms) -- opt-in until restructured
   static const bool march_oseen = std::getenv("AAO_KKT_MARCH_OSEEN") != nullptr;
@@ -464,6 +800,40 @@ bool launch_kkt_march(const Ctx& c, const double* x, double* y, cudaStream_t s) 
     R.bp[o] = c.h_Pm[I * 5 + o];
     R.bg[o] = c.h_Gm[I * 5 + o];
   }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (c.dim == 3) {
+    K3Args a;
+    a.x = x;
+    a.y = y;
+    a.n1 = c.n1q2;
+    a.m1 = c.n1q1;
+    a.n_b = c.n_b;
+    a.nblk = c.nblk;
+    a.n_s = c.n_s;
+    a.n_v = c.n_v;
+    a.tau = c.tau;
+    a.tnu = c.tau * c.nu;
+    a.tob = c.tau / c.beta;
+    a.ntx = (c.n1q2 - 1 + K3_TX - 1) / K3_TX;
+    a.nty = (c.n1q2 - 1 + K3_TY - 1) / K3_TY;
+    const int ntz = (c.n1q2 - 1 + K3_TZ - 1) / K3_TZ;
+    a.tiles = a.ntx * a.nty * ntz;
+    const long total = (long)a.tiles * c.n_b;
+    const int grid = (int)std::max(1L, std::min((long)sms, (total + 3) / 4));
+    const size_t smem = 2 * K3_STAGE * sizeof(double);
+    static bool attr3 = false;
+    if (!attr3) {
+      cudaFuncSetAttribute(k_kkt_march3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr3 = true;
+    }
+    k_kkt_march3<<<grid, 256, smem, s>>>(a, R);
+    return true;
+  }
   KMArgs a;
   a.x = x;
   a.y = y;
@@ -484,12 +854,6 @@ bool launch_kkt_march(const Ctx& c, const double* x, double* y, cudaStream_t s) 
   a.tiles = tiles;
   // one CTA per SM (shared memory bound); at least 4 time blocks per CTA
   const long total = (long)tiles * c.n_b;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
   const int grid = (int)std::max(1L, std::min((long)sms, (total + 3) / 4));
   const size_t smem = 2 * KM_STAGE * sizeof(double);
   static bool attr = false;
