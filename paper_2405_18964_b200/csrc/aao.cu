@@ -1312,6 +1312,7 @@ void gmres_alloc(Ctx& c, int m) {
     c.gZptr = upload(c, zp);
   }
   CK(cudaMallocHost(&c.hostH, sizeof(double) * (m + 2) * 2));
+  for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c.gm_ev[i], cudaEventDisableTiming));
   c.gm_m = m;
 }
 
@@ -1358,21 +1359,36 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
     std::fill(g.begin(), g.end(), 0.0);
     g[0] = beta0;
     int kdone = 0;
-    for (int k = 0; k < m; ++k) {
+    // Iteration k on the device: z_k = P^{-1} v_k, w = A z_k, MGS against v_0..v_k with w normalised on
+    // the device (v_{k+1}), and the Hessenberg column copied to host buffer k & 1.  The linear path
+    // enqueues iteration k+1 before the host has read column k (the host's Givens update and
+    // convergence test overlap the next iteration); a solve that stops at k leaves one speculative
+    // iteration in the stream whose results are never used.  Same arithmetic, same history.
+    auto enqueue = [&](int k) {
       double* Vk = c.gV + (size_t)k * N;
       double* w = c.gV + (size_t)(k + 1) * N;
       double* zk = c.nonlinear ? c.gZ + (size_t)k * N : c.gz;
       precond_apply(c, Vk, zk, s);
       kkt_apply(c, zk, w, s);
-      inf.precond_applies++;
-      // modified Gram-Schmidt, device-resident coefficients, one cooperative launch
       double* hcol = c.gH + (size_t)k * (m + 1);
       int w_scaled = 0;
       CK(launch_mgs(w, (const double* const*)c.gVptr, k, N, hcol, c.gpart, s, &w_scaled));
       ++launch_counter();
-      CK(cudaMemcpyAsync(c.hostH, hcol, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      for (int i = 0; i <= k + 1; ++i) H[(size_t)i * m + k] = c.hostH[i];
+      if (!w_scaled) {
+        launch_scale_dev(w, w, hcol + k + 1, N, s);
+        ++launch_counter();
+      }
+      CK(cudaMemcpyAsync(c.hostH + (k & 1) * (m + 2), hcol, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, s));
+      CK(cudaEventRecord(c.gm_ev[k & 1], s));
+    };
+    const bool speculate = !c.nonlinear;   // Algorithm 2 synchronises inside precond_apply
+    enqueue(0);
+    for (int k = 0; k < m; ++k) {
+      if (speculate && k + 1 < m && it + 1 < kry.max_iters) enqueue(k + 1);
+      CK(cudaEventSynchronize(c.gm_ev[k & 1]));
+      inf.precond_applies++;
+      const double* hh = c.hostH + (k & 1) * (m + 2);
+      for (int i = 0; i <= k + 1; ++i) H[(size_t)i * m + k] = hh[i];
       // Givens rotations (same arithmetic as oracle/gmres.py)
       for (int i = 0; i < k; ++i) {
         const double t = cs[i] * H[(size_t)i * m + k] + sn[i] * H[(size_t)(i + 1) * m + k];
@@ -1407,10 +1423,7 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
         stop = true;
         break;
       }
-      if (!w_scaled) {
-        launch_scale_dev(w, w, hcol + k + 1, N, s);
-        ++launch_counter();
-      }
+      if (!speculate && k + 1 < m) enqueue(k + 1);
     }
     // x += P^{-1}(V_k y), H_k y = g_k
     for (int i = kdone - 1; i >= 0; --i) {
@@ -1537,6 +1550,8 @@ void aao_destroy(aao_ctx* ctx) {
   if (!ctx) return;
   for (void* p : ctx->c.allocs) cudaFree(p);
   if (ctx->c.hostH) cudaFreeHost(ctx->c.hostH);
+  for (auto e : ctx->c.gm_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& e : ctx->c.ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->c.prof_ev) cudaEventDestroy(e);

@@ -152,7 +152,8 @@ struct Ctx {
   double *gV = nullptr, *gz = nullptr, *gw = nullptr, *gu = nullptr, *gr = nullptr;
   double *gH = nullptr, *gpart = nullptr, *gscal = nullptr;
   double **gVptr = nullptr;
-  double* hostH = nullptr;   // pinned
+  double* hostH = nullptr;   // pinned, 2 x (m + 2): Hessenberg columns of iterations k, k+1
+  cudaEvent_t gm_ev[2] = {nullptr, nullptr};
   // bookkeeping
   std::vector<void*> allocs;
   size_t bytes = 0;

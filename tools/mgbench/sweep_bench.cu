@@ -213,6 +213,42 @@ __global__ void __launch_bounds__(MAXT, 1) k_v3(double2* X, const double2* B, in
   if (threadIdx.x == 0) cyc[blockIdx.x] = clock64() - t0;
 }
 
+// V5: V0 with the iterate resident in shared memory (copied in once; n1^2 * 16 B must fit)
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_v5(double2* X, const double2* B, int n1, int sweeps, long long* cyc) {
+  extern __shared__ double2 xs[];
+  double2* xg = X + (long)blockIdx.x * n1 * n1;
+  const double2* b = B + (long)blockIdx.x * n1 * n1;
+  for (int i = threadIdx.x; i < n1 * n1; i += blockDim.x) xs[i] = xg[i];
+  __syncthreads();
+  double2* x = xs;
+  const long long t0 = clock64();
+  for (int sw = 0; sw < sweeps; ++sw)
+    for (int colour = 0; colour < 9; ++colour) {
+      const int rx = colour % 3, ry = colour / 3;
+      for (int py = 0; py < 2; ++py) {
+        int sy = ry + 3 * py; if (sy < 1) sy += 6;
+        const int sx = rx < 1 ? rx + 3 : rx;
+        const int cx = (n1 - 2 - sx) / 3 + 1, cy = sy > n1 - 2 ? 0 : (n1 - 2 - sy) / 6 + 1;
+        const int total = cx * cy;
+        for (int t = threadIdx.x; t < total; t += blockDim.x) {
+          const int q = t / cx;
+          const int i = sx + 3 * (t - q * cx), j = sy + 6 * q;
+          const int idx = j * n1 + i;
+          const int cls = (i & 1) | ((j & 1) << 1);
+          const double2 bb = b[idx];
+          const double2 ax = (sy & 1) ? eval_nat<1>(x, i, j, n1, cls) : eval_nat<0>(x, i, j, n1, cls);
+          const double2 xc = x[idx];
+          const double oi = ctab[cls * 26 + 25];
+          x[idx] = make_double2(xc.x + oi * (bb.x - ax.x), xc.y + oi * (bb.y - ax.y));
+        }
+      }
+      __syncthreads();
+    }
+  if (threadIdx.x == 0) cyc[blockIdx.x] = clock64() - t0;
+  for (int i = threadIdx.x; i < n1 * n1; i += blockDim.x) xg[i] = xs[i];
+}
+
 int main(int argc, char** argv) {
   const int n1 = argc > 1 ? atoi(argv[1]) : 129;
   const int P = argc > 2 ? atoi(argv[2]) : 128;
@@ -267,6 +303,12 @@ int main(int argc, char** argv) {
   run("V1 residue t512", [&] { k_v1<512><<<P, 512>>>(X, B, n1, sweeps, cyc); });
   run("V1 residue t1024", [&] { k_v1<1024><<<P, 1024>>>(X, B, n1, sweeps, cyc); });
   run("V3 residue6 t512", [&] { k_v3<512><<<P, 512>>>(X, B, n1, sweeps, cyc); });
+  if (n * 16 <= 220 * 1024) {
+    cudaFuncSetAttribute(k_v5<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_v5<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    run("V5 smem-resident t512", [&] { k_v5<512><<<P, 512, n * 16>>>(X, B, n1, sweeps, cyc); });
+    run("V5 smem-resident t1024", [&] { k_v5<1024><<<P, 1024, n * 16>>>(X, B, n1, sweeps, cyc); });
+  }
   run("V3 residue6 t1024", [&] { k_v3<1024><<<P, 1024>>>(X, B, n1, sweeps, cyc); });
   return 0;
 }
