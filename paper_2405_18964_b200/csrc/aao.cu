@@ -902,6 +902,25 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
       a.lwarp = l;
       break;
     }
+  // band-wavefront sweeps (opt-in AAO_WAVE=1, parity-green, measured slower on c2: 2.73 vs 2.37 ms;
+  // AAO_WAVE_MIN: smallest n1, AAO_WAVE_H: band height): 2-D Q2 real operators
+  static const char* wave_env = std::getenv("AAO_WAVE");
+  static const char* wmin_env = std::getenv("AAO_WAVE_MIN");
+  a.wave_h = 0;
+  if ((wave_env ? std::atoi(wave_env) : 0) && c.dim == 2 && S.order == 2 && a.use_ctab && op.conv_sel == 0 &&
+      !a.perm && c.mg_mode != 1) {
+    const int n1 = a.g[0].n1;
+    static const char* wh_env = std::getenv("AAO_WAVE_H");
+    const int h = wh_env ? std::atoi(wh_env) : (n1 <= 129 ? 6 : 3);
+    const size_t ring = (size_t)8 * h * n1 * sizeof(double2);
+    if (used + ring <= 220 * 1024) {
+      a.wave_h = h;
+      a.wave_min = wmin_env ? std::atoi(wmin_env) : 65;
+      used = (used + 15) / 16 * 16;
+      a.ring_off = (long)(used / sizeof(double2));
+      used += ring;
+    }
+  }
   static const char* q2c_env = std::getenv("AAO_Q2C");
   a.q2c = q2c_env ? std::atoi(q2c_env) : 0;
   // profiling only: per-level SM-cycle accounting of CTA 0, printed per launch (AAO_MG_CLOCK=1)

@@ -991,12 +991,140 @@ __device__ void q2c_residual(const double* tabl, const double2* x, const double2
       q2c_dispatch<true>(tabl, const_cast<double2*>(x), b, r, n1, 1 + qx, 1 + qy, 2, 0.0, tid, nth);
 }
 
+// ---- band-wavefront multicolour SOR (2-D Q2, real class stencils) --------------------------------
+// The 9 colour steps of one sweep are fused into ONE pass over the grid.  Rows are grouped in bands of
+// H rows; a row j of class c = (j mod 3) (c' = 2 - c for the reversed colour order) is updated at step
+// tau(j) = floor(j / H) + 2 c'.  For rows at distance <= 2 (the stencil reach) this orders every
+// earlier colour before and every later colour after, exactly as the 9 separate colour steps do
+// (|floor(j/H) - floor(j'/H)| <= 1 < 2 |c - c'|), and rows active in one step are >= H + 1 apart.
+// Each step runs the three x-colours (i mod 3) of its three active bands in order.  The rows the
+// active bands can touch (bands T-5 .. T+1) live in a shared-memory ring of 8 bands: a band is
+// streamed in (cp.async) two steps ahead and written back when no later step can read it, so every
+// value of the iterate crosses L2/HBM once per sweep instead of once per colour, and every stencil tap
+// is a shared-memory load.  Same updates, same values as cta_sweep (only the summation schedule of
+// independent nodes differs: none, each node's stencil sum is evaluated in the same order).
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_commit_all() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+template <int RR, int PY>
+__device__ __forceinline__ double2 ring_eval(const double* T, const double2* ring, int r0, int i, int n1) {
+  constexpr int AY0 = PY ? 1 : 0, AY1 = PY ? 4 : 5;
+  const int xl = i >= 2 ? i - 2 : i, xr = i + 2 <= n1 - 1 ? i + 2 : i;
+  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int ob = AY0; ob < AY1; ++ob) {
+    int r = r0 + ob - 2;
+    r += r < 0 ? RR : 0;
+    r -= r >= RR ? RR : 0;
+    const double2* row = ring + r * n1;
+    const double* t = T + ob * 5;
+    acc = cfma(t[0], row[xl], acc);
+    acc = cfma(t[1], row[i - 1], acc);
+    acc = cfma(t[2], row[i], acc);
+    acc = cfma(t[3], row[i + 1], acc);
+    acc = cfma(t[4], row[xr], acc);
+  }
+  return acc;
+}
+
+template <int H>
+__device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __restrict__ b, double2* ring, int n1,
+                             bool reverse, double omega, int tid, int nth) {
+  constexpr int RR = 8 * H;   // ring rows: 8 bands
+  const int nb = (n1 + H - 1) / H;
+  auto band_rows = [&](int band, int& j0, int& cnt) {
+    j0 = band * H;
+    cnt = (min(n1, j0 + H) - j0) * n1;
+  };
+  auto load_async = [&](int band) {
+    int j0, cnt;
+    band_rows(band, j0, cnt);
+    double2* dst = ring + (j0 % RR) * n1;
+    const double2* src = x + (long)j0 * n1;
+    for (int e = tid; e < cnt; e += nth) cp_async16(dst + e, src + e);
+    cp_commit_all();
+  };
+  auto writeback = [&](int band) {
+    int j0, cnt;
+    band_rows(band, j0, cnt);
+    const double2* src = ring + (j0 % RR) * n1;
+    double2* dst = x + (long)j0 * n1;
+    for (int e = tid; e < cnt; e += nth) dst[e] = src[e];
+  };
+  load_async(0);
+  if (nb > 1) load_async(1);
+  const int i0s[3] = {3, 1, 2};
+  for (int T = 0; T <= nb + 3; ++T) {
+    cp_wait_all();
+    __syncthreads();
+    if (T >= 6) {
+      writeback(T - 6);
+      __syncthreads();
+    }
+    if (T + 2 < nb) load_async(T + 2);
+    for (int q = 0; q < 3; ++q) {
+      const int rx = reverse ? 2 - q : q;
+      const int i0 = i0s[rx];
+      const int cx = i0 > n1 - 2 ? 0 : (n1 - 2 - i0) / 3 + 1;
+      const int per = (H / 3) * cx;
+      const int total = 3 * per;
+      const float rper = 1.0f / (float)max(per, 1), rcx = 1.0f / (float)max(cx, 1);
+      for (int t = tid; t < total; t += nth) {
+        int p = __float2int_rz(((float)t + 0.5f) * rper);
+        int rem = t - p * per;
+        if (rem >= per) { rem -= per; ++p; } else if (rem < 0) { rem += per; --p; }
+        const int band = T - 2 * p;
+        if (band < 0 || band >= nb) continue;
+        const int cls = reverse ? 2 - p : p;   // row class j mod 3 of pair p
+        int kk = __float2int_rz(((float)rem + 0.5f) * rcx);
+        int m = rem - kk * cx;
+        if (m >= cx) { m -= cx; ++kk; } else if (m < 0) { m += cx; --kk; }
+        const int k0 = ((cls - band * H) % 3 + 3) % 3;
+        const int j = band * H + k0 + 3 * kk;
+        if (j < 1 || j > n1 - 2) continue;
+        const int i = i0 + 3 * m;
+        const double2 bb = b[(long)j * n1 + i];
+        const int r0 = j % RR;
+        const int ccls = (i & 1) | ((j & 1) << 1);
+        const double* Tc = tabl + ccls * (ClassTab<2>::NT + 1);
+        const double invD = Tc[ClassTab<2>::NT];
+        const double2 Ax = (j & 1) ? ring_eval<RR, 1>(Tc, ring, r0, i, n1) : ring_eval<RR, 0>(Tc, ring, r0, i, n1);
+        double2* xp = ring + r0 * n1 + i;
+        const double2 xo = *xp;
+        *xp = make_double2(xo.x + omega * invD * (bb.x - Ax.x), xo.y + omega * invD * (bb.y - Ax.y));
+      }
+      __syncthreads();
+    }
+  }
+  for (int band = max(0, nb - 2); band < nb; ++band)
+    if (band + 6 > nb + 3) writeback(band);
+  __syncthreads();
+}
+
 template <int DIM, int ORD, bool CONV, bool W, bool TAB>
 __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
                                           const double2* b, int sweeps, bool reverse, double omega, int tid, int nth,
-                                          const double* tabl, int fast = 0) {
+                                          const double* tabl, int fast = 0, double2* ring = nullptr,
+                                          int waveH = 0) {
   constexpr int C1 = ORD == 2 ? 3 : 2;
   constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
+  if constexpr (TAB && !CONV && ORD == 2 && DIM == 2 && !W) {
+    if (ring && waveH) {
+      for (int sw = 0; sw < sweeps; ++sw) {
+        switch (waveH) {
+          case 3: q2_wave_pass<3>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth); break;
+          case 6: q2_wave_pass<6>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth); break;
+          case 9: q2_wave_pass<9>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth); break;
+          default: q2_wave_pass<12>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth); break;
+        }
+      }
+      return;
+    }
+  }
   if constexpr (TAB && !CONV && ORD == 2 && DIM == 2) {
     if (fast == 1 || (fast == 2 && !W)) {
       q2c_sweep<W>(tabl, x, b, g.n1, sweeps, reverse, omega, tid, nth);
@@ -1098,7 +1226,9 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
   }
   const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
                                                        : ClassTab<DIM>::PER_LEVEL) : nullptr;
-  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl, a.q2c);
+  const bool wv = a.wave_h && l < a.lsm && g.n1 >= a.wave_min;
+  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl, a.q2c,
+                                    wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0);
   double2* rl = S.R(l);
   const double* cvl = S.CV(l);
   if (TAB && !CONV && ORD == 2 && DIM == 2 && (a.q2c == 1 || (a.q2c == 2 && !W))) {
@@ -1226,7 +1356,9 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
   gsync<W>();
   const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
                                                    : ClassTab<DIM>::PER_LEVEL) : nullptr;
-  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl, a.q2c);
+  const bool wv = a.wave_h && l < a.lsm && g.n1 >= a.wave_min;
+  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl, a.q2c,
+                                    wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0);
 }
 
 template <int DIM, int ORD, bool CONV, bool TAB>
