@@ -22,28 +22,9 @@ from .problem import Problem
 from .timeops import backward_euler_E
 
 
-def exact_v(x, y, t, T):
-    e = np.exp(T - t)
-    return np.stack([e * 20 * x * y**3, e * (5 * x**4 - 5 * y**4)])
-
-
-def forcing(x, y, t, T):
-    """f of P:818-820."""
-    e = np.exp(T - t)
-    a = (x**2 - 1) ** 2 * (y**2 - 1)
-    b = (x**2 - 1) * (y**2 - 1) ** 2
-    return np.stack([e * (-20 * x * y**3 - 2 * y * a) + 2 * y * a,
-                     e * (5 * (y**4 - x**4) + 2 * x * b) - 2 * x * b])
-
-
-def desired(x, y, t, T, beta):
-    """v_d of P:815-817."""
-    e = np.exp(T - t)
-    c1 = 4 * beta * (y * (2 * (3 * x**2 - 1) * (y**2 - 1) + 3 * (x**2 - 1) ** 2))
-    c2 = 4 * beta * (-x * (3 * (y**2 - 1) ** 2 + 2 * (x**2 - 1) * (3 * y**2 - 1)))
-    d1 = e * (20 * x * y**3 + 2 * beta * y * ((x**2 - 1) ** 2 * (y**2 - 7) - 4 * (3 * x**2 - 1) * (y**2 - 1) + 2))
-    d2 = e * (5 * (x**4 - y**4) - 2 * beta * x * ((y**2 - 1) ** 2 * (x**2 - 7) - 4 * (x**2 - 1) * (3 * y**2 - 1) - 2))
-    return np.stack([c1 + d1, c2 + d2])
+exact_v = synth.mms_velocity        # the paper's data live in synth/ (inputs of both sides)
+forcing = synth.mms_forcing
+desired = synth.mms_desired
 
 
 def exact_lambda(x, y, t, T, beta):
@@ -53,9 +34,51 @@ def exact_lambda(x, y, t, T, beta):
     return np.stack([g * 2 * y * (x**2 - 1) ** 2 * (y**2 - 1), -g * 2 * x * (x**2 - 1) * (y**2 - 1) ** 2])
 
 
-def solve_manufactured(n_cells, n_t, T=1.0, beta=1e-2):
-    """Solve the discrete optimality system; return the max-over-t_j relative nodal errors of v and lambda."""
-    cfg = synth.small_config("mms", 2, n_cells, n_t, lo=-1.0, hi=1.0, beta=beta, nu=1.0)
+def rhs_with_data(prob, vd, f, g, v0):
+    """Right-hand side of the optimality system with time-dependent data, paper order.
+
+    vd, f: (n_b, d, n_s) nodal v_d and f at t_m, m = 1..n_b; g: (n_b + 1, d, n_s) Dirichlet data at
+    t_0..t_{n_b} (boundary entries used); v0: (d, n_s) initial state on every node (or None: g[0]).
+    Boundary columns of the state are moved to the right-hand side (lifting):
+      adjoint rows (half 0):  tau M (v_d^m - G^m) |_I
+      state rows   (half 1):  [M (tau f^m - G^m + H^{m-1}) - tau L G^m] |_I,  H^0 = v0, H^{m-1} = G^{m-1}
+      divergence rows (half 1): -tau B G^m |_Ip
+    with G^m = g^m on boundary nodes and 0 inside, L = nu K (Stokes).  Every matrix is the full
+    (un-eliminated) assembled operator restricted to the unknown rows."""
+    cfg = prob.cfg
+    f_lv = fem.Level(cfg.dim, cfg.n_cells, cfg.x_lo, cfg.x_hi)
+    fine = prob.fine
+    Iv, Ip = fine.Iv, fine.Ip
+    n_s, d, n_b, tau = prob.n_s, cfg.dim, prob.n_b, prob.tau
+    bmask = np.ones(n_s, dtype=bool)
+    bmask[Iv] = False
+    Mfull, Kfull, Bfull = f_lv.mass_q2(), f_lv.stiff_q2(), f_lv.div()
+    Lfull = cfg.nu * Kfull
+    V = np.zeros((2, n_b, d, len(Iv)))
+    P = np.zeros((2, n_b, fine.npu))
+    G = lambda m, c: np.where(bmask, g[m][c], 0.0) if g is not None else np.zeros(n_s)
+    for j in range(n_b):
+        m = j + 1
+        Gfull = np.zeros(d * n_s)
+        for c in range(d):
+            Gm = G(m, c)
+            Gfull[c * n_s:(c + 1) * n_s] = Gm
+            vdm = vd[j][c] if vd is not None else np.zeros(n_s)
+            V[0, j, c] = tau * (Mfull @ (vdm - Gm))[Iv]
+            fm = f[j][c] if f is not None else np.zeros(n_s)
+            if m == 1:
+                H = v0[c] if v0 is not None else G(0, c)
+            else:
+                H = G(m - 1, c)
+            V[1, j, c] = (Mfull @ (tau * fm - Gm + H) - tau * (Lfull @ Gm))[Iv]
+        P[1, j] = -tau * (Bfull @ Gfull)[Ip]
+    return prob.from_reduced(V, P)
+
+
+def solve_manufactured(n_cells, n_t, T=1.0, beta=1e-2, full=False):
+    """Solve the discrete optimality system; return the max-over-t_j relative nodal errors of v and lambda
+    (and, with full=True, the solution in paper order)."""
+    cfg = synth.mms_config(n_cells, n_t, beta)
     prob = Problem(cfg)
     f = prob.fine
     Lv = fem.Level(2, n_cells, -1.0, 1.0)
@@ -85,33 +108,11 @@ def solve_manufactured(n_cells, n_t, T=1.0, beta=1e-2):
     T1 = sp.bmat([[tau * I, E.T], [E, -(tau / beta) * I]])
     A = (sp.kron(T1, MM) + tau * sp.kron(sp.bmat([[O, O], [I, O]]), S1)
          + tau * sp.kron(sp.bmat([[O, I], [O, O]]), S2)).tocsc()
-    # right-hand side with lifting, block m = 1..n_b at t_m = m tau
+    # right-hand side with lifting (rhs_with_data), in the ordering of A: blocks (half, t), [v comps, p]
     nb = nv + npu
-    b = np.zeros(2 * n_b * nb)
-    vB = lambda m: exact_v(x[Bd], y[Bd], m * tau, T)           # boundary values (d, |Bd|)
-    for m in range(1, n_b + 1):
-        j = m - 1
-        # adjoint rows (half 0): tau M (v_d - v); the boundary part of v^(m) stays on the RHS
-        vd = desired(x, y, m * tau, T, beta)
-        r0 = np.concatenate([tau * ((Mfull @ vd[c])[Iv] - M_IB @ vB(m)[c]) for c in range(2)])
-        b[(0 * n_b + j) * nb:(0 * n_b + j) * nb + nv] = r0
-        # state rows (half 1): M(v^m - v^{m-1}) + tau L v^m + tau B^T p^m - tau/beta M lam^m = tau M f^m
-        fm = forcing(x, y, m * tau, T)
-        r1 = []
-        for c in range(2):
-            rc = tau * (Mfull @ fm[c])[Iv] - M_IB @ vB(m)[c] - tau * (L_IB @ vB(m)[c])
-            if m == 1:
-                v0 = exact_v(x, y, 0.0, T)[c]                   # v^(0) = v_0, all nodes
-                rc = rc + (Mfull @ v0)[Iv]
-            else:
-                rc = rc + M_IB @ vB(m - 1)[c]
-            r1.append(rc)
-        b[(1 * n_b + j) * nb:(1 * n_b + j) * nb + nv] = np.concatenate(r1)
-        # divergence rows (half 1 pressure): tau B v^m = 0 -> tau B_I v_I = -tau B_B v_B
-        vfull = np.zeros(2 * Lv.n_s)
-        for c in range(2):
-            vfull[c * Lv.n_s + Bd] = vB(m)[c]
-        b[(1 * n_b + j) * nb + nv:(1 * n_b + j + 1) * nb] = -tau * (Bfull @ vfull)[Ip]
+    vd, fd, gd, v0 = synth.mms_inputs(cfg)
+    Vr, Pr = prob.to_reduced(rhs_with_data(prob, vd, fd, gd, v0))
+    b = np.concatenate([np.concatenate([Vr[h, j].reshape(-1), Pr[h, j]]) for h in range(2) for j in range(n_b)])
     sol = spla.spsolve(A, b)
     err, ref, lerr, lref = 0.0, 0.0, 0.0, 0.0
     for m in range(1, n_b + 1):
@@ -124,4 +125,13 @@ def solve_manufactured(n_cells, n_t, T=1.0, beta=1e-2):
         le = exact_lambda(x[Iv], y[Iv], m * tau, T, beta)
         lerr = max(lerr, np.sqrt(np.mean((lh - le) ** 2)))
         lref = max(lref, np.sqrt(np.mean(le**2)))
+    if full:
+        V = np.zeros((2, n_b, 2, len(Iv)))
+        P = np.zeros((2, n_b, npu))
+        for h in range(2):
+            for j in range(n_b):
+                blk = sol[(h * n_b + j) * nb:(h * n_b + j + 1) * nb]
+                V[h, j] = blk[:nv].reshape(2, -1)
+                P[h, j] = blk[nv:]
+        return err / ref, lerr / lref, prob.from_reduced(V, P)
     return err / ref, lerr / lref

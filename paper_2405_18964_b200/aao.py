@@ -45,7 +45,8 @@ class Info(ctypes.Structure):
 
 
 EXPORTS = ["aao_config_defaults", "aao_create", "aao_destroy", "aao_last_error", "aao_vector_len",
-           "aao_device_bytes", "aao_pack", "aao_build_rhs", "aao_kkt_apply", "aao_precond_apply",
+           "aao_device_bytes", "aao_pack", "aao_build_rhs", "aao_build_rhs_general", "aao_kkt_apply",
+           "aao_precond_apply",
            "aao_gmres_solve", "aao_gmres_solve_host", "aao_debug_freq_block", "aao_set_timing",
            "aao_last_phase_ms", "aao_last_launch_count", "aao_profile_smoother", "aao_profile_read",
            "aao_last_inner_iterations"]
@@ -75,6 +76,8 @@ def load(path: str = LIB_PATH):
     for name in ("aao_pack", "aao_build_rhs", "aao_kkt_apply", "aao_precond_apply"):
         getattr(L, name).argtypes = [vp, vp, vp, vp]
         getattr(L, name).restype = st
+    L.aao_build_rhs_general.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+    L.aao_build_rhs_general.restype = st
     L.aao_gmres_solve.argtypes = [vp, vp, vp, ctypes.POINTER(Krylov), ctypes.POINTER(Info), dp, i, vp]
     L.aao_gmres_solve.restype = st
     L.aao_gmres_solve_host.argtypes = [vp, dp, dp, ctypes.POINTER(Krylov), ctypes.POINTER(Info), dp, i, vp]
@@ -189,6 +192,21 @@ class Context:
         vd = vd.to(device="cuda", dtype=self.torch.float64).contiguous()
         out = self.empty() if out is None else out
         self._check(self.L.aao_build_rhs(self.h, _ptr(vd), _ptr(self._vec(out)), self._stream(stream)), "build_rhs")
+        return out
+
+    def build_rhs_general(self, vd=None, f=None, g=None, v0=None, out=None, stream=None):
+        """aao_build_rhs_general: time-dependent v_d, f, Dirichlet data g (lifting) and v0 (numpy or torch;
+        vd, f: (n_b, d, n_s); g: (n_b + 1, d, n_s); v0: (d, n_s))."""
+        def dev(a):
+            if a is None:
+                return None
+            t = a if isinstance(a, self.torch.Tensor) else self.torch.as_tensor(np.ascontiguousarray(a))
+            return t.to(device="cuda", dtype=self.torch.float64).contiguous()
+        arrs = [dev(a) for a in (vd, f, g, v0)]
+        out = self.empty() if out is None else out
+        ptrs = [_ptr(a) if a is not None else None for a in arrs]
+        self._check(self.L.aao_build_rhs_general(self.h, *ptrs, _ptr(self._vec(out)), self._stream(stream)),
+                    "build_rhs_general")
         return out
 
     def kkt_apply(self, x, out=None, stream=None):

@@ -107,7 +107,7 @@ struct Ref1D {
 
 // assembled 1-D rows on N cells of width h
 struct Tables1D {
-  std::vector<double> M2, K2, M2full, M1, K1, Pm, Gm, PmT, GmT;
+  std::vector<double> M2, K2, M2full, K2full, M1, K1, Pm, Gm, Pmfull, Gmfull, PmT, GmT;
 };
 
 Tables1D tables_1d(const Ref1D& R, int N, double h) {
@@ -123,6 +123,7 @@ Tables1D tables_1d(const Ref1D& R, int N, double h) {
         T.K2[i * 5 + (j - i + 2)] += R.k2[li][lj] / h;
       }
   T.M2full = T.M2;
+  T.K2full = T.K2;
   for (int i = 0; i < n1; ++i)
     for (int o = 0; o < 5; ++o) {
       const int j = i + o - 2;
@@ -130,7 +131,7 @@ Tables1D tables_1d(const Ref1D& R, int N, double h) {
         T.M2[i * 5 + o] = 0.0;
         T.K2[i * 5 + o] = 0.0;
       }
-      if (j < 0 || j > n1 - 1) T.M2full[i * 5 + o] = 0.0;
+      if (j < 0 || j > n1 - 1) T.M2full[i * 5 + o] = T.K2full[i * 5 + o] = 0.0;
     }
   T.M1.assign(m1 * 3, 0.0);
   T.K1.assign(m1 * 3, 0.0);
@@ -151,10 +152,13 @@ Tables1D tables_1d(const Ref1D& R, int N, double h) {
         T.Pm[I * 5 + (j - 2 * I + 2)] += h * R.pm[li][lj];
         T.Gm[I * 5 + (j - 2 * I + 2)] += R.gm[li][lj];
       }
+  T.Pmfull = T.Pm;   // boundary (Dirichlet) Q2 columns kept: lifting of boundary data (aao_build_rhs_general)
+  T.Gmfull = T.Gm;
   for (int I = 0; I < m1; ++I)
     for (int o = 0; o < 5; ++o) {
       const int j = 2 * I + o - 2;
       if (j <= 0 || j >= n1 - 1) T.Pm[I * 5 + o] = T.Gm[I * 5 + o] = 0.0;
+      if (j < 0 || j > n1 - 1) T.Pmfull[I * 5 + o] = T.Gmfull[I * 5 + o] = 0.0;
     }
   T.PmT.assign(n1 * 3, 0.0);
   T.GmT.assign(n1 * 3, 0.0);
@@ -538,6 +542,9 @@ void setup(Ctx& c, const aao_config& cfg) {
   c.tPmT = upload(c, L[0].t.PmT);
   c.tGmT = upload(c, L[0].t.GmT);
   c.tMfull = upload(c, L[0].t.M2full);
+  c.tKfull = upload(c, L[0].t.K2full);
+  c.tPmfull = upload(c, L[0].t.Pmfull);
+  c.tGmfull = upload(c, L[0].t.Gmfull);
   c.h_M2 = L[0].t.M2;
   c.h_K2 = L[0].t.K2;
   c.h_Pm = L[0].t.Pm;
@@ -1594,6 +1601,16 @@ aao_status aao_pack(aao_ctx* ctx, const double* in, double* out, void* stream) {
 aao_status aao_build_rhs(aao_ctx* ctx, const double* vd, double* b, void* stream) {
   if (!ctx || !vd || !b) return AAO_ERR_SHAPE;
   ABI_GUARD(ctx, { aao::launch_rhs(ctx->c, vd, b, (cudaStream_t)stream); ++aao::launch_counter(); });
+  return AAO_OK;
+}
+
+aao_status aao_build_rhs_general(aao_ctx* ctx, const double* vd, const double* f, const double* g, const double* v0,
+                                 double* b, void* stream) {
+  if (!ctx || !b) return AAO_ERR_SHAPE;
+  if (g && ctx->c.oseen)
+    return fail(ctx, AAO_ERR_CONFIG, "aao_build_rhs_general: inhomogeneous Dirichlet data with convection "
+                                     "(Oseen lifting) is not implemented");
+  ABI_GUARD(ctx, { aao::launch_rhs_general(ctx->c, vd, f, g, v0, b, (cudaStream_t)stream); ++aao::launch_counter(); });
   return AAO_OK;
 }
 

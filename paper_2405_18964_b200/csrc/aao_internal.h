@@ -115,6 +115,7 @@ struct Ctx {
   double *tPm = nullptr, *tGm = nullptr;    // [n1q1][5] B rows: int psi_I phi_j, int psi_I phi_j'
   double *tPmT = nullptr, *tGmT = nullptr;  // [n1q2][3] B^T rows, Q1 cols floor((i-1)/2)+o
   double* tMfull = nullptr;                 // [n1q2][5] un-eliminated Q2 mass rows (RHS)
+  double *tKfull = nullptr, *tPmfull = nullptr, *tGmfull = nullptr;  // un-eliminated K rows, B rows (lifting)
   std::vector<double> h_M2, h_K2, h_Pm, h_Gm, h_PmT, h_GmT;  // host copies of the fine 1-D rows
   FreqConst* fc = nullptr;                  // device [n_f]
   std::vector<FreqConst> fch;
@@ -231,6 +232,8 @@ void launch_kkt(const Ctx& c, const double* x, double* y, cudaStream_t s);
 bool launch_kkt_march(const Ctx& c, const double* x, double* y, cudaStream_t s);
 void launch_mask_copy(const Ctx& c, const double* in, double* out, cudaStream_t s);
 void launch_rhs(const Ctx& c, const double* vd, double* b, cudaStream_t s);
+void launch_rhs_general(const Ctx& c, const double* vd, const double* f, const double* g, const double* v0, double* b,
+                        cudaStream_t s);
 void launch_debug_block(const Ctx& c, int k, double2* out, cudaStream_t s);
 
 // frequency-vector kernels (kernels_freq.cu)

@@ -724,6 +724,113 @@ __global__ void k_rhs(Geo G, const double* __restrict__ tMf, const double* __res
   *bo = G.tau * acc;
 }
 
+// Right-hand side with time-dependent data and lifting of inhomogeneous Dirichlet data (
+// NEXT-2: the paper's manufactured problem).  Row block m = j + 1 (t_m = m tau), component c:
+//   adjoint rows (half 0):   tau [M (v_d^m - G^m)]_i
+//   state rows   (half 1):   [M (tau f^m - G^m + H^{m-1}) - tau nu K G^m]_i,  H^0 = v0, H^{m-1} = G^{m-1}
+//   divergence rows (half 1): -tau [B G^m]_I  (B = -(int psi d_c phi))
+// with G^m = g^m on boundary nodes and 0 inside, all operators un-eliminated (boundary columns kept).
+// vd, f: [n_b][d][n_s]; g: [n_b + 1][d][n_s]; v0: [d][n_s]; any may be null (= 0; v0 null -> g^0).
+struct RhsData {
+  const double *vd, *f, *g, *v0;
+  const double *tM, *tK, *tPm, *tGm;   // full 1-D rows
+};
+
+__device__ __forceinline__ bool q2_boundary(int i, int j, int k, int n1, int dim) {
+  bool b = i == 0 || i == n1 - 1 || j == 0 || j == n1 - 1;
+  if (dim == 3) b = b || k == 0 || k == n1 - 1;
+  return b;
+}
+
+template <int DIM>
+__global__ void k_rhs_gen(Geo G, RhsData D, double* __restrict__ b) {
+  const long col = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= G.nblk) return;
+  const int row = blockIdx.y, h = row / G.n_b, j = row % G.n_b, m = j + 1;
+  double* bo = b + (long)row * G.nblk + col;
+  const int n1 = G.n1q2;
+  const long ns = G.n_s;
+  auto gb = [&](int mm, int comp, long nd, int ii, int jj, int kk) -> double {   // G^mm (boundary data only)
+    return (D.g && q2_boundary(ii, jj, kk, n1, DIM)) ? D.g[((long)mm * G.dim + comp) * ns + nd] : 0.0;
+  };
+  if (col < G.n_v) {
+    const int comp = (int)(col / ns);
+    const long node = col % ns;
+    int c[3];
+    c[0] = (int)(node % n1);
+    c[1] = (int)((node / n1) % n1);
+    c[2] = DIM == 3 ? (int)(node / ((long)n1 * n1)) : 0;
+    if (q2_boundary(c[0], c[1], c[2], n1, DIM)) {
+      *bo = 0.0;
+      return;
+    }
+    double accM = 0.0, accK = 0.0;
+    for (int oc = 0; oc < (DIM == 3 ? 5 : 1); ++oc) {
+      const int kk = DIM == 3 ? c[2] + oc - 2 : 0;
+      if (DIM == 3 && (kk < 0 || kk >= n1)) continue;
+      const double mz = DIM == 3 ? D.tM[c[2] * 5 + oc] : 1.0, kz = DIM == 3 ? D.tK[c[2] * 5 + oc] : 0.0;
+      for (int ob = 0; ob < 5; ++ob) {
+        const int jj = c[1] + ob - 2;
+        if (jj < 0 || jj >= n1) continue;
+        const double my = D.tM[c[1] * 5 + ob], ky = D.tK[c[1] * 5 + ob];
+        for (int oa = 0; oa < 5; ++oa) {
+          const int ii = c[0] + oa - 2;
+          if (ii < 0 || ii >= n1) continue;
+          const double mx = D.tM[c[0] * 5 + oa], kx = D.tK[c[0] * 5 + oa];
+          const double wm = mz * my * mx;
+          const double wk = kz * my * mx + mz * ky * mx + mz * my * kx;
+          const long nd = ((long)kk * n1 + jj) * n1 + ii;
+          const double Gm = gb(m, comp, nd, ii, jj, kk);
+          double w;
+          if (h == 0) {
+            w = (D.vd ? D.vd[((long)j * G.dim + comp) * ns + nd] : 0.0) - Gm;
+          } else {
+            const double fm = D.f ? D.f[((long)j * G.dim + comp) * ns + nd] : 0.0;
+            const double H = m == 1 ? (D.v0 ? D.v0[(long)comp * ns + nd] : gb(0, comp, nd, ii, jj, kk))
+                                    : gb(m - 1, comp, nd, ii, jj, kk);
+            w = G.tau * fm - Gm + H;
+            accK = fma(wk, Gm, accK);
+          }
+          accM = fma(wm, w, accM);
+        }
+      }
+    }
+    *bo = h == 0 ? G.tau * accM : accM - G.tau * G.nu * accK;
+    return;
+  }
+  // pressure rows
+  const long pn = col - G.n_v;
+  if (h == 0 || pn == 0 || !D.g) {
+    *bo = 0.0;
+    return;
+  }
+  const int m1 = G.n1q1;
+  int c[3];
+  c[0] = (int)(pn % m1);
+  c[1] = (int)((pn / m1) % m1);
+  c[2] = DIM == 3 ? (int)(pn / ((long)m1 * m1)) : 0;
+  double acc = 0.0;   // (B G^m)_I = -sum_c sum (G_c on axis c)(P elsewhere) G^m_c
+  for (int comp = 0; comp < DIM; ++comp)
+    for (int oc = 0; oc < (DIM == 3 ? 5 : 1); ++oc) {
+      const int kk = DIM == 3 ? 2 * c[2] + oc - 2 : 0;
+      if (DIM == 3 && (kk < 0 || kk >= n1)) continue;
+      const double fz = DIM == 3 ? (comp == 2 ? D.tGm : D.tPm)[c[2] * 5 + oc] : 1.0;
+      for (int ob = 0; ob < 5; ++ob) {
+        const int jj = 2 * c[1] + ob - 2;
+        if (jj < 0 || jj >= n1) continue;
+        const double fy = (comp == 1 ? D.tGm : D.tPm)[c[1] * 5 + ob];
+        for (int oa = 0; oa < 5; ++oa) {
+          const int ii = 2 * c[0] + oa - 2;
+          if (ii < 0 || ii >= n1) continue;
+          const double fx = (comp == 0 ? D.tGm : D.tPm)[c[0] * 5 + oa];
+          const long nd = ((long)kk * n1 + jj) * n1 + ii;
+          acc = fma(-fz * fy * fx, gb(m, comp, nd, ii, jj, kk), acc);
+        }
+      }
+    }
+  *bo = -G.tau * acc;
+}
+
 Geo geo_of(const Ctx& c) {
   Geo g;
   g.dim = c.dim;
@@ -926,6 +1033,16 @@ void launch_kkt(const Ctx& c, const double* x, double* y, cudaStream_t s) {
 
 void launch_mask_copy(const Ctx& c, const double* in, double* out, cudaStream_t s) {
   k_mask_copy<<<(unsigned)((c.N + 255) / 256), 256, 0, s>>>(geo_of(c), in, out, c.N);
+}
+
+void launch_rhs_general(const Ctx& c, const double* vd, const double* f, const double* g, const double* v0, double* b,
+                        cudaStream_t s) {
+  RhsData D{vd, f, g, v0, c.tMfull, c.tKfull, c.tPmfull, c.tGmfull};
+  dim3 grd((unsigned)((c.nblk + 127) / 128), 2 * c.n_b);
+  if (c.dim == 2)
+    k_rhs_gen<2><<<grd, 128, 0, s>>>(geo_of(c), D, b);
+  else
+    k_rhs_gen<3><<<grd, 128, 0, s>>>(geo_of(c), D, b);
 }
 
 void launch_rhs(const Ctx& c, const double* vd, double* b, cudaStream_t s) {

@@ -198,3 +198,51 @@ def probe_vector(cfg: Config, seed_offset: int = 0) -> np.ndarray:
     r = rng.standard_normal(cfg.n_dofs)
     r[~full_mask(cfg)] = 0.0
     return r
+
+
+# ----------------------------------------------------------------------------
+# the paper's manufactured Stokes problem: data only (exact state, forcing, desired state);
+# both the oracle (direct solve) and the GPU path (aao_build_rhs_general) consume these arrays
+# ----------------------------------------------------------------------------
+def mms_config(n_cells: int, n_t: int, beta: float = 1e-2) -> Config:
+    """Omega = [-1,1]^2, nu = 1, T = 1 (P:812-814)."""
+    return small_config(f"mms{n_cells}x{n_t}", 2, n_cells, n_t, lo=-1.0, hi=1.0, beta=beta, nu=1.0)
+
+
+def mms_velocity(x, y, t, T=1.0):
+    """v = e^{T-t} [20 x y^3, 5 x^4 - 5 y^4]."""
+    e = np.exp(T - t)
+    return np.stack([e * 20 * x * y**3, e * (5 * x**4 - 5 * y**4)])
+
+
+def mms_forcing(x, y, t, T=1.0):
+    """f of P:818-820."""
+    e = np.exp(T - t)
+    a = (x**2 - 1) ** 2 * (y**2 - 1)
+    b = (x**2 - 1) * (y**2 - 1) ** 2
+    return np.stack([e * (-20 * x * y**3 - 2 * y * a) + 2 * y * a,
+                     e * (5 * (y**4 - x**4) + 2 * x * b) - 2 * x * b])
+
+
+def mms_desired(x, y, t, T, beta):
+    """v_d of P:815-817."""
+    e = np.exp(T - t)
+    c1 = 4 * beta * (y * (2 * (3 * x**2 - 1) * (y**2 - 1) + 3 * (x**2 - 1) ** 2))
+    c2 = 4 * beta * (-x * (3 * (y**2 - 1) ** 2 + 2 * (x**2 - 1) * (3 * y**2 - 1)))
+    d1 = e * (20 * x * y**3 + 2 * beta * y * ((x**2 - 1) ** 2 * (y**2 - 7) - 4 * (3 * x**2 - 1) * (y**2 - 1) + 2))
+    d2 = e * (5 * (x**4 - y**4) - 2 * beta * x * ((y**2 - 1) ** 2 * (x**2 - 7) - 4 * (x**2 - 1) * (3 * y**2 - 1) - 2))
+    return np.stack([c1 + d1, c2 + d2])
+
+
+def mms_inputs(cfg: Config):
+    """Nodal data on the full Q2 grid at t_m = m tau: v_d (n_b, d, n_s) and f (n_b, d, n_s) for m = 1..n_b,
+    Dirichlet data g (n_b + 1, d, n_s) for m = 0..n_b (exact v; only boundary entries are data), and
+    v0 (d, n_s) = v(t = 0) on every node (initial and boundary data given by v)."""
+    X = q2_coords(cfg)
+    x, y = X[0], X[1]
+    tau = cfg.T / cfg.n_t
+    n_b = cfg.n_b
+    vd = np.stack([mms_desired(x, y, m * tau, cfg.T, cfg.beta) for m in range(1, n_b + 1)])
+    f = np.stack([mms_forcing(x, y, m * tau, cfg.T) for m in range(1, n_b + 1)])
+    g = np.stack([mms_velocity(x, y, m * tau, cfg.T) for m in range(0, n_b + 1)])
+    return vd, f, g, g[0].copy()
