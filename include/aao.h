@@ -140,6 +140,16 @@ aao_status aao_build_rhs(aao_ctx* ctx, const double* vd_q2, double* b, void* str
 aao_status aao_build_rhs_general(aao_ctx* ctx, const double* vd, const double* f, const double* g, const double* v0,
                                  double* b, void* stream);
 
+/* Arnoldi process on A P^{-1} (right preconditioning, the GMRES iteration of aao_gmres_solve without the
+   Givens update, the spectra of P:359-367 and P:607-632): v_0 = v0 / ||v0||, then for
+   k = 0..m-1  w = A P^{-1} v_k, modified Gram-Schmidt against v_0..v_k, h_{k+1,k} = ||w||.
+   v0: DEVICE, length aao_vector_len (masked entries ignored).  H: HOST, row-major (m + 1) x m, receives
+   the unrotated Hessenberg matrix (zeros beyond the steps done); *m_done (may be NULL) = steps done
+   (< m at breakdown, h_{k+1,k} < 1e-14 ||v0||).  Eigenvalues of H[:k, :k] (Ritz values) estimate those
+   of P^{-1} A.  Uses the GMRES workspace: m must not exceed the restart of the first solve on ctx.
+   Synchronises the stream once per step.  Errors: AAO_ERR_SHAPE, AAO_ERR_CONFIG, AAO_ERR_NUMERIC. */
+aao_status aao_arnoldi(aao_ctx* ctx, const double* v0, int m, double* H, int* m_done, void* stream);
+
 /* y = A x, eq. (FinalA) (step A2).  Device pointers, x != y. */
 aao_status aao_kkt_apply(aao_ctx* ctx, const double* x, double* y, void* stream);
 

@@ -79,3 +79,23 @@ def gmres(apply_A, apply_Pinv, b, tol=1e-6, restart=30, max_iters=2000):
         info["restarts"] += 1
     info["iterations"] = it
     return x, hist, info
+
+
+def arnoldi(apply_A, apply_Pinv, v0, m):
+    """m steps of the Arnoldi process on A P^{-1} (right preconditioning, as in gmres above) with modified
+    Gram-Schmidt, from v0 / ||v0||.  Returns H ((k+1) x k, unrotated) for the k <= m steps done (stops at
+    h_{k+1,k} < 1e-14 ||v0||).  The eigenvalues of H[:k, :k] (Ritz values) estimate those of A P^{-1},
+    i.e. of P^{-1} A (similar matrices) -- the spectra of P:607-632."""
+    nrm = np.linalg.norm(v0)
+    V = [v0 / nrm]
+    H = np.zeros((m + 1, m))
+    for k in range(m):
+        w = apply_A(apply_Pinv(V[k]))
+        for i in range(k + 1):
+            H[i, k] = np.dot(w, V[i])
+            w = w - H[i, k] * V[i]
+        H[k + 1, k] = np.linalg.norm(w)
+        if H[k + 1, k] < 1e-14 * nrm:
+            return H[:k + 2, :k + 1]
+        V.append(w / H[k + 1, k])
+    return H

@@ -45,7 +45,7 @@ class Info(ctypes.Structure):
 
 
 EXPORTS = ["aao_config_defaults", "aao_create", "aao_destroy", "aao_last_error", "aao_vector_len",
-           "aao_device_bytes", "aao_pack", "aao_build_rhs", "aao_build_rhs_general", "aao_kkt_apply",
+           "aao_device_bytes", "aao_pack", "aao_build_rhs", "aao_build_rhs_general", "aao_arnoldi", "aao_kkt_apply",
            "aao_precond_apply",
            "aao_gmres_solve", "aao_gmres_solve_host", "aao_debug_freq_block", "aao_set_timing",
            "aao_last_phase_ms", "aao_last_launch_count", "aao_profile_smoother", "aao_profile_read",
@@ -76,6 +76,8 @@ def load(path: str = LIB_PATH):
     for name in ("aao_pack", "aao_build_rhs", "aao_kkt_apply", "aao_precond_apply"):
         getattr(L, name).argtypes = [vp, vp, vp, vp]
         getattr(L, name).restype = st
+    L.aao_arnoldi.argtypes = [vp, vp, i, dp, ctypes.POINTER(ctypes.c_int), vp]
+    L.aao_arnoldi.restype = st
     L.aao_build_rhs_general.argtypes = [vp, vp, vp, vp, vp, vp, vp]
     L.aao_build_rhs_general.restype = st
     L.aao_gmres_solve.argtypes = [vp, vp, vp, ctypes.POINTER(Krylov), ctypes.POINTER(Info), dp, i, vp]
@@ -208,6 +210,16 @@ class Context:
         self._check(self.L.aao_build_rhs_general(self.h, *ptrs, _ptr(self._vec(out)), self._stream(stream)),
                     "build_rhs_general")
         return out
+
+    def arnoldi(self, v0, m, stream=None):
+        """aao_arnoldi: m Arnoldi steps on A P^{-1} from v0; returns the unrotated Hessenberg (k+1, k), k = steps
+        done (numpy).  Ritz values: np.linalg.eigvals(H[:k, :k])."""
+        H = np.zeros((m + 1) * m)
+        k = ctypes.c_int(0)
+        self._check(self.L.aao_arnoldi(self.h, _ptr(self._vec(v0)), int(m), H.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                       ctypes.byref(k), self._stream(stream)), "arnoldi")
+        H = H.reshape(m + 1, m)
+        return H[:k.value + 1, :k.value]
 
     def kkt_apply(self, x, out=None, stream=None):
         out = self.empty() if out is None else out

@@ -1483,6 +1483,39 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
   return inf.converged ? AAO_OK : AAO_NOT_CONVERGED;
 }
 
+// m steps of Arnoldi on A P^{-1}, the GMRES iteration without the Givens update:
+// v_0 = v0 / ||v0||, w = A P^{-1} v_k, MGS against v_0..v_k, h_{k+1,k} = ||w||.  H (host, row-major
+// (m+1) x m, unrotated) receives the columns done; returns the number of steps (stops at breakdown).
+int arnoldi(Ctx& c, const double* v0, int m, double* H, cudaStream_t s) {
+  gmres_alloc(c, m);
+  const long N = c.N;
+  const double nrm = dot_host(c, v0, v0, 1, s);
+  std::memset(H, 0, sizeof(double) * (size_t)(m + 1) * m);
+  if (nrm == 0.0) return 0;
+  launch_scale_dev(c.gV, v0, c.gscal, N, s);
+  ++launch_counter();
+  for (int k = 0; k < m; ++k) {
+    double* Vk = c.gV + (size_t)k * N;
+    double* w = c.gV + (size_t)(k + 1) * N;
+    precond_apply(c, Vk, c.gz, s);
+    kkt_apply(c, c.gz, w, s);
+    double* hcol = c.gH + (size_t)k * (m + 1);
+    int w_scaled = 0;
+    CK(launch_mgs(w, (const double* const*)c.gVptr, k, N, hcol, c.gpart, s, &w_scaled));
+    ++launch_counter();
+    if (!w_scaled) {
+      launch_scale_dev(w, w, hcol + k + 1, N, s);
+      ++launch_counter();
+    }
+    CK(cudaMemcpyAsync(c.hostH, hcol, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int i = 0; i <= k + 1; ++i) H[(size_t)i * m + k] = c.hostH[i];
+    if (!std::isfinite(c.hostH[k + 1])) throw CudaError(AAO_ERR_NUMERIC, "NaN/Inf in Arnoldi");
+    if (c.hostH[k + 1] < 1e-14 * nrm) return k + 1;
+  }
+  return m;
+}
+
 }  // namespace
 }  // namespace aao
 
@@ -1611,6 +1644,14 @@ aao_status aao_build_rhs_general(aao_ctx* ctx, const double* vd, const double* f
     return fail(ctx, AAO_ERR_CONFIG, "aao_build_rhs_general: inhomogeneous Dirichlet data with convection "
                                      "(Oseen lifting) is not implemented");
   ABI_GUARD(ctx, { aao::launch_rhs_general(ctx->c, vd, f, g, v0, b, (cudaStream_t)stream); ++aao::launch_counter(); });
+  return AAO_OK;
+}
+
+aao_status aao_arnoldi(aao_ctx* ctx, const double* v0, int m, double* H, int* m_done, void* stream) {
+  if (!ctx || !v0 || !H || m < 1) return AAO_ERR_SHAPE;
+  int k = 0;
+  ABI_GUARD(ctx, { k = aao::arnoldi(ctx->c, v0, m, H, (cudaStream_t)stream); });
+  if (m_done) *m_done = k;
   return AAO_OK;
 }
 

@@ -276,3 +276,22 @@ def test_fgmres_nonlinear_history_parity(name):
     assert abs(info["iterations"] - ref["iterations"]) <= 1 and info["converged"] == 1
     n = min(len(hist), len(ref["hist"]))
     assert np.max(np.abs(np.array(hist[:n]) - np.array(ref["hist"][:n])) / np.array(ref["hist"][:n])) <= 1e-8
+
+
+@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[3], SMALL[5]], ids=lambda c: c.name)
+def test_arnoldi_hessenberg_parity(cfg):
+    """NEXT-3: aao_arnoldi (A P^{-1}, MGS) against the oracle's Arnoldi on the same v0: the Hessenberg
+    entries agree (rounding grows slowly through the steps, as in the GMRES histories)."""
+    torch = _torch()
+    from oracle import gmres, kkt
+    prob, pc = oracle_for(cfg)
+    ctx = gpu_ctx(cfg)
+    m = 20
+    v0 = synth.probe_vector(cfg, seed_offset=3)
+    Hg = ctx.arnoldi(torch.from_numpy(v0).cuda(), m)
+    Ho = gmres.arnoldi(lambda v: kkt.kkt_apply(prob, v), pc.apply, v0, m)
+    assert Hg.shape == Ho.shape
+    assert np.linalg.norm(Hg - Ho) <= 1e-9 * np.linalg.norm(Ho)
+    ritz_g = np.sort_complex(np.linalg.eigvals(Hg[:m, :m]))
+    ritz_o = np.sort_complex(np.linalg.eigvals(Ho[:m, :m]))
+    assert np.max(np.abs(ritz_g - ritz_o)) <= 1e-7 * np.max(np.abs(ritz_o))

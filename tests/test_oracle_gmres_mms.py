@@ -84,3 +84,26 @@ def test_manufactured_solution_converges():
     assert el[0] > 4 * el[1] > 16 * el[2] and el[2] < 2e-2
     lt = [solve_manufactured(8, nt)[1] for nt in (8, 16, 32)]
     assert lt[0] > lt[1] > lt[2]
+
+
+def test_arnoldi_relation_and_full_spectrum():
+    """Textbook Arnoldi pins: A P^{-1} V_m = V_{m+1} H_m (MGS), and at m = n the Ritz values are the
+    eigenvalues of A P^{-1} (= those of P^{-1} A)."""
+    rng = np.random.default_rng(5)
+    n = 12
+    A = rng.standard_normal((n, n)) + n * np.eye(n)
+    P = np.eye(n) + 0.1 * rng.standard_normal((n, n))
+    Pinv = np.linalg.inv(P)
+    v0 = rng.standard_normal(n)
+    H = gmres.arnoldi(lambda v: A @ v, lambda v: Pinv @ v, v0, 6)
+    # rebuild V by the same recurrence and check the relation
+    V = np.zeros((n, 7))
+    V[:, 0] = v0 / np.linalg.norm(v0)
+    for k in range(6):
+        w = A @ Pinv @ V[:, k] - V[:, :k + 1] @ H[:k + 1, k]
+        V[:, k + 1] = w / H[k + 1, k]
+    np.testing.assert_allclose(A @ Pinv @ V[:, :6], V @ H, atol=1e-10)
+    Hf = gmres.arnoldi(lambda v: A @ v, lambda v: Pinv @ v, v0, n)
+    ritz = np.sort_complex(np.linalg.eigvals(Hf[:n, :n]))
+    ev = np.sort_complex(np.linalg.eigvals(Pinv @ A))
+    np.testing.assert_allclose(ritz, ev, rtol=1e-9, atol=1e-9)
