@@ -130,13 +130,13 @@ aao_status aao_build_rhs(aao_ctx* ctx, const double* vd_q2, double* b, void* str
    side by lifting (the paper's manufactured problem P:812-824).
    For time block m = 1..n_b (t_m = m tau), component c, with G^m = g^m on boundary nodes and 0 inside:
      adjoint rows (half 0):    tau [M (v_d^m - G^m)] on interior velocity nodes
-     state rows (half 1):      [M (tau f^m - G^m + H^{m-1}) - tau nu K G^m],  H^0 = v0, H^{m-1} = G^{m-1}
+     state rows (half 1):      [M (tau f^m - G^m + H^{m-1}) - tau L G^m],  H^0 = v0, H^{m-1} = G^{m-1},
+                               L = nu K (Stokes) or nu K + N (Oseen, the context's wind)
      divergence rows (half 1): -tau [B G^m] on unknown pressure nodes;  all other rows 0,
    M, K, B un-eliminated (boundary columns kept).  All pointers DEVICE, full Q2 grids, x fastest:
      vd, f: [n_b][d][n_s] at t_1..t_{n_b};  g: [n_b + 1][d][n_s] at t_0..t_{n_b} (only boundary entries
      are read);  v0: [d][n_s] on every node.  Any of vd, f, g, v0 may be NULL (= 0; v0 NULL -> g^0).
-   b: DEVICE, length aao_vector_len (paper order).  Errors: AAO_ERR_SHAPE (null ctx/b),
-   AAO_ERR_CONFIG (g given for an Oseen context: the convective lifting is not implemented). */
+   b: DEVICE, length aao_vector_len (paper order).  Errors: AAO_ERR_SHAPE (null ctx/b). */
 aao_status aao_build_rhs_general(aao_ctx* ctx, const double* vd, const double* f, const double* g, const double* v0,
                                  double* b, void* stream);
 

@@ -34,7 +34,7 @@ def exact_lambda(x, y, t, T, beta):
     return np.stack([g * 2 * y * (x**2 - 1) ** 2 * (y**2 - 1), -g * 2 * x * (x**2 - 1) * (y**2 - 1) ** 2])
 
 
-def rhs_with_data(prob, vd, f, g, v0):
+def rhs_with_data(prob, vd, f, g, v0, wind=None):
     """Right-hand side of the optimality system with time-dependent data, paper order.
 
     vd, f: (n_b, d, n_s) nodal v_d and f at t_m, m = 1..n_b; g: (n_b + 1, d, n_s) Dirichlet data at
@@ -43,8 +43,9 @@ def rhs_with_data(prob, vd, f, g, v0):
       adjoint rows (half 0):  tau M (v_d^m - G^m) |_I
       state rows   (half 1):  [M (tau f^m - G^m + H^{m-1}) - tau L G^m] |_I,  H^0 = v0, H^{m-1} = G^{m-1}
       divergence rows (half 1): -tau B G^m |_Ip
-    with G^m = g^m on boundary nodes and 0 inside, L = nu K (Stokes).  Every matrix is the full
-    (un-eliminated) assembled operator restricted to the unknown rows."""
+    with G^m = g^m on boundary nodes and 0 inside, L = nu K (Stokes) or nu K + N (Oseen, `wind` the Q2 nodal
+    wind of the problem).  Every matrix is the full (un-eliminated) assembled operator restricted to the
+    unknown rows."""
     cfg = prob.cfg
     f_lv = fem.Level(cfg.dim, cfg.n_cells, cfg.x_lo, cfg.x_hi)
     fine = prob.fine
@@ -54,6 +55,8 @@ def rhs_with_data(prob, vd, f, g, v0):
     bmask[Iv] = False
     Mfull, Kfull, Bfull = f_lv.mass_q2(), f_lv.stiff_q2(), f_lv.div()
     Lfull = cfg.nu * Kfull
+    if prob.oseen:
+        Lfull = Lfull + f_lv.conv_q2(wind)
     V = np.zeros((2, n_b, d, len(Iv)))
     P = np.zeros((2, n_b, fine.npu))
     G = lambda m, c: np.where(bmask, g[m][c], 0.0) if g is not None else np.zeros(n_s)

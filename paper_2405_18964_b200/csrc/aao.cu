@@ -216,7 +216,7 @@ void transfer_1d(const Ref1D&, int Nc, int order, std::vector<double>& tP, std::
 // convection stencils N_ij = int phi_i (w_h . grad phi_j) by an element loop (3^d Gauss points)
 // on the Q2 space (order 2) or Q1 space (order 1) with the Q2 nodal wind of the level.
 void convection(const Ref1D& R, int dim, int N, double h, int order, const std::vector<double>& wind,
-                std::vector<double>& conv, std::vector<double>& convT) {
+                std::vector<double>& conv, std::vector<double>& convT, std::vector<double>* conv_full = nullptr) {
   const int n1q2 = 2 * N + 1;
   const long ns = (long)std::pow(n1q2, dim);
   const int n1 = order * N + 1, W = 2 * order + 1, nl1 = order + 1;
@@ -295,6 +295,7 @@ void convection(const Ref1D& R, int dim, int N, double h, int order, const std::
       }
     }
   }
+  if (conv_full) *conv_full = conv;   // un-eliminated (boundary columns kept): lifting of Dirichlet data
   // eliminate: rows/columns of masked nodes (Dirichlet boundary for Q2, pinned node 0 for Q1)
   auto is_masked = [&](long node) {
     if (order == 1) return node == 0;
@@ -478,7 +479,10 @@ void setup(Ctx& c, const aao_config& cfg) {
         for (int comp = 0; comp < dim; ++comp) L[l].wind[(size_t)comp * ncn + I] = L[l - 1].wind[(size_t)comp * nfn + f];
       }
     }
-    for (int l = 0; l < nlev; ++l) convection(R, dim, L[l].N, L[l].h, 2, L[l].wind, L[l].conv, L[l].convT);
+    std::vector<double> conv_full;
+    for (int l = 0; l < nlev; ++l)
+      convection(R, dim, L[l].N, L[l].h, 2, L[l].wind, L[l].conv, L[l].convT, l == 0 ? &conv_full : nullptr);
+    c.convFull = upload(c, conv_full);
   }
 
   // MG spaces
@@ -1640,9 +1644,6 @@ aao_status aao_build_rhs(aao_ctx* ctx, const double* vd, double* b, void* stream
 aao_status aao_build_rhs_general(aao_ctx* ctx, const double* vd, const double* f, const double* g, const double* v0,
                                  double* b, void* stream) {
   if (!ctx || !b) return AAO_ERR_SHAPE;
-  if (g && ctx->c.oseen)
-    return fail(ctx, AAO_ERR_CONFIG, "aao_build_rhs_general: inhomogeneous Dirichlet data with convection "
-                                     "(Oseen lifting) is not implemented");
   ABI_GUARD(ctx, { aao::launch_rhs_general(ctx->c, vd, f, g, v0, b, (cudaStream_t)stream); ++aao::launch_counter(); });
   return AAO_OK;
 }

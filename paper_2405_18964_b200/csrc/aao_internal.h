@@ -116,6 +116,7 @@ struct Ctx {
   double *tPmT = nullptr, *tGmT = nullptr;  // [n1q2][3] B^T rows, Q1 cols floor((i-1)/2)+o
   double* tMfull = nullptr;                 // [n1q2][5] un-eliminated Q2 mass rows (RHS)
   double *tKfull = nullptr, *tPmfull = nullptr, *tGmfull = nullptr;  // un-eliminated K rows, B rows (lifting)
+  double* convFull = nullptr;   // Oseen: un-eliminated fine convection stencil [n_s][5^d] (lifting)
   std::vector<double> h_M2, h_K2, h_Pm, h_Gm, h_PmT, h_GmT;  // host copies of the fine 1-D rows
   FreqConst* fc = nullptr;                  // device [n_f]
   std::vector<FreqConst> fch;

@@ -727,13 +727,14 @@ __global__ void k_rhs(Geo G, const double* __restrict__ tMf, const double* __res
 // Right-hand side with time-dependent data and lifting of inhomogeneous Dirichlet data (
 // NEXT-2: the paper's manufactured problem).  Row block m = j + 1 (t_m = m tau), component c:
 //   adjoint rows (half 0):   tau [M (v_d^m - G^m)]_i
-//   state rows   (half 1):   [M (tau f^m - G^m + H^{m-1}) - tau nu K G^m]_i,  H^0 = v0, H^{m-1} = G^{m-1}
+//   state rows   (half 1):   [M (tau f^m - G^m + H^{m-1}) - tau (nu K + N) G^m]_i,  H^0 = v0, H^{m-1} = G^{m-1}
 //   divergence rows (half 1): -tau [B G^m]_I  (B = -(int psi d_c phi))
 // with G^m = g^m on boundary nodes and 0 inside, all operators un-eliminated (boundary columns kept).
 // vd, f: [n_b][d][n_s]; g: [n_b + 1][d][n_s]; v0: [d][n_s]; any may be null (= 0; v0 null -> g^0).
 struct RhsData {
   const double *vd, *f, *g, *v0;
   const double *tM, *tK, *tPm, *tGm;   // full 1-D rows
+  const double* conv;                  // Oseen: un-eliminated convection stencil per node, or null
 };
 
 __device__ __forceinline__ bool q2_boundary(int i, int j, int k, int n1, int dim) {
@@ -795,7 +796,18 @@ __global__ void k_rhs_gen(Geo G, RhsData D, double* __restrict__ b) {
         }
       }
     }
-    *bo = h == 0 ? G.tau * accM : accM - G.tau * G.nu * accK;
+    double accN = 0.0;   // Oseen: (N G^m)_i with the un-eliminated stencil (taps (oc, ob, oa), x fastest)
+    if (h == 1 && D.conv && D.g) {
+      constexpr int NT = DIM == 2 ? 25 : 125;
+      const double* cv = D.conv + node * NT;
+      for (int t = 0; t < NT; ++t) {
+        const int oa = t % 5, ob = (t / 5) % 5, oc = t / 25;
+        const int ii = c[0] + oa - 2, jj = c[1] + ob - 2, kk = DIM == 3 ? c[2] + oc - 2 : 0;
+        if (ii < 0 || ii >= n1 || jj < 0 || jj >= n1 || kk < 0 || kk >= n1) continue;
+        accN = fma(cv[t], gb(m, comp, ((long)kk * n1 + jj) * n1 + ii, ii, jj, kk), accN);
+      }
+    }
+    *bo = h == 0 ? G.tau * accM : accM - G.tau * (G.nu * accK + accN);
     return;
   }
   // pressure rows
@@ -1037,7 +1049,7 @@ void launch_mask_copy(const Ctx& c, const double* in, double* out, cudaStream_t 
 
 void launch_rhs_general(const Ctx& c, const double* vd, const double* f, const double* g, const double* v0, double* b,
                         cudaStream_t s) {
-  RhsData D{vd, f, g, v0, c.tMfull, c.tKfull, c.tPmfull, c.tGmfull};
+  RhsData D{vd, f, g, v0, c.tMfull, c.tKfull, c.tPmfull, c.tGmfull, c.oseen ? c.convFull : nullptr};
   dim3 grd((unsigned)((c.nblk + 127) / 128), 2 * c.n_b);
   if (c.dim == 2)
     k_rhs_gen<2><<<grd, 128, 0, s>>>(geo_of(c), D, b);

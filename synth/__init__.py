@@ -246,3 +246,46 @@ def mms_inputs(cfg: Config):
     f = np.stack([mms_forcing(x, y, m * tau, cfg.T) for m in range(1, n_b + 1)])
     g = np.stack([mms_velocity(x, y, m * tau, cfg.T) for m in range(0, n_b + 1)])
     return vd, f, g, g[0].copy()
+
+
+# ----------------------------------------------------------------------------
+# the paper's Oseen lid-driven cavity: data only
+# ----------------------------------------------------------------------------
+def cavity_config(n_cells: int, n_t: int, beta: float = 1e-3, nu: float = 1 / 20) -> Config:
+    """Omega = [-1,1]^2, Oseen; beta, nu as BASELINE c3."""
+    return small_config(f"cavity{n_cells}x{n_t}", 2, n_cells, n_t, problem="oseen", lo=-1.0, hi=1.0,
+                        beta=beta, nu=nu, index=3)
+
+
+def cavity_wind(cfg: Config) -> np.ndarray:
+    """Two-vortex wind of P:908-913 (DESIGN.md reading: the second vortex uses (x1 + 1/2), the printed
+    (x1 - 1/2) does not vanish at its own centre c_2 = 1)."""
+    X = q2_coords(cfg)
+    x1, x2 = X[0], X[1]
+    a, b = (100 / 99) ** 2, (100 / 49) ** 2
+    c1 = 1 - np.sqrt((100 / 49 * (x1 - 0.5)) ** 2 + (100 / 99 * x2) ** 2)
+    c2 = 1 - np.sqrt((100 / 49 * (x1 + 0.5)) ** 2 + (100 / 99 * x2) ** 2)
+    w = np.zeros((2, cfg.n_s))
+    m1, m2 = c1 >= 0, (c2 >= 0) & ~(c1 >= 0)
+    w[0, m1] = c1[m1] * a * x2[m1]
+    w[1, m1] = -c1[m1] * b * (x1[m1] - 0.5)
+    w[0, m2] = c2[m2] * a * x2[m2]
+    w[1, m2] = c2[m2] * b * (x1[m2] + 0.5)
+    return w
+
+
+def cavity_inputs(cfg: Config):
+    """v_d, f (time-independent) on t_1..t_{n_b}, lid data h = [1, 0] on x2 = 1 at
+    t_0..t_{n_b}, v0 = [1, 0] where |x1| < x2; same shapes as mms_inputs."""
+    X = q2_coords(cfg)
+    x1, x2 = X[0], X[1]
+    q = (1 - x1**4) * (1 - x2**4)
+    vd = np.stack([2 * x2 * q + np.where(x2 >= 0.8, 5 * x2 - 4, 0.0), -2 * x1 * q])
+    f = np.stack([-20 * x1 * x2**3 - 2 * x2 * (x1**2 - 1) ** 2 * (x2**2 - 1),
+                  5 * (x2**4 - x1**4) + 2 * x1 * (x1**2 - 1) * (x2**2 - 1) ** 2])
+    lid = np.isclose(x2, 1.0)
+    h = np.stack([np.where(lid, 1.0, 0.0), np.zeros(cfg.n_s)])
+    v0 = np.stack([np.where((x1 > -x2) & (x1 < x2), 1.0, 0.0), np.zeros(cfg.n_s)])
+    n_b = cfg.n_b
+    return (np.repeat(vd[None], n_b, axis=0), np.repeat(f[None], n_b, axis=0),
+            np.repeat(h[None], n_b + 1, axis=0), v0)

@@ -91,3 +91,38 @@ def test_manufactured_gpu_convergence_rate():
         pytest.skip("needs the three manufactured solves above")
     e = [_ERRS[k] for k in ((4, 8), (8, 16), (16, 32))]
     assert e[0] > 4 * e[1] > 16 * e[2] and e[2] < 2e-3
+
+
+# ---------------------------------------------------------------- the Oseen lid-driven cavity
+@pytest.mark.parametrize("nc,nt", [(8, 8), (16, 9)])
+def test_cavity_rhs_matches_oracle(nc, nt):
+    """Lifting with convection: the lid data enter the state rows through nu K + N (un-eliminated)."""
+    _torch()
+    from oracle import manufactured
+    from oracle.problem import Problem
+    from paper_2405_18964_b200 import Context
+    cfg = synth.cavity_config(nc, nt)
+    w = synth.cavity_wind(cfg)
+    ctx = Context.from_config(cfg, w)
+    vd, f, g, v0 = synth.cavity_inputs(cfg)
+    b = ctx.build_rhs_general(vd, f, g, v0).cpu().numpy()
+    bo = manufactured.rhs_with_data(Problem(cfg, w), vd, f, g, v0, wind=w)
+    assert rel(b, bo) <= 1e-13
+
+
+def test_cavity_solve_gpu():
+    """Algorithm 2 + FGMRES(10) solves the cavity optimality system; the converged x
+    satisfies the oracle's A x = b (true residual through oracle/kkt.py)."""
+    torch = _torch()
+    from oracle import kkt
+    from oracle.problem import Problem
+    from paper_2405_18964_b200 import Context
+    cfg = synth.cavity_config(16, 9)
+    w = synth.cavity_wind(cfg)
+    ctx = Context.from_config(cfg, w, nonlinear=True, inner_eps=1e-2, inner_maxit=60)
+    b = ctx.build_rhs_general(*synth.cavity_inputs(cfg))
+    x, info, hist, rc = ctx.gmres_solve(b, tol=1e-8, restart=10, max_iters=200)
+    assert info["converged"], info
+    bn = b.cpu().numpy()
+    r = bn - kkt.kkt_apply(Problem(cfg, w), x.cpu().numpy())
+    assert np.linalg.norm(r) <= 1e-7 * np.linalg.norm(bn)
