@@ -745,6 +745,32 @@ __device__ __forceinline__ double2 class_eval(const double* tabl, const double2*
   }
 }
 
+// Branch-free 2-D class-stencil evaluation (all 25 taps; rows and columns clamped into the grid where the
+// class coefficient is zero) with one accumulator per stencil row: for the small, latency-bound levels,
+// where one node per thread and one colour per barrier phase leave nothing to overlap, a single
+// warp-convergent pass with short dependency chains beats the parity-split visits.
+__device__ __forceinline__ double2 class_eval_flat2(const double* tabl, const double2* x, int i, int j, int n1,
+                                                    double& invD) {
+  const int cls = (i & 1) | ((j & 1) << 1);
+  const double* T = tabl + cls * (ClassTab<2>::NT + 1);
+  invD = T[ClassTab<2>::NT];
+  const int xl = i >= 2 ? i - 2 : i, xr = i + 2 <= n1 - 1 ? i + 2 : i;
+  double2 acc[5];
+#pragma unroll
+  for (int ob = 0; ob < 5; ++ob) {
+    int r = j + ob - 2;
+    r = r < 0 ? 0 : (r > n1 - 1 ? n1 - 1 : r);
+    const double2* row = x + r * n1;
+    const double* t = T + ob * 5;
+    double2 a = make_double2(t[0] * row[xl].x, t[0] * row[xl].y);
+    a = cfma(t[1], row[i - 1], a);
+    a = cfma(t[2], row[i], a);
+    a = cfma(t[3], row[i + 1], a);
+    acc[ob] = cfma(t[4], row[xr], a);
+  }
+  return cadd(cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])), acc[4]);
+}
+
 // ---------------------------------------------------------------- CTA-resident solvers
 // One CTA owns one problem (one frequency / slot / component) and runs the WHOLE fixed-count
 // solve -- every level, colour, transfer and V-cycle -- with block barriers only.  The problems
@@ -1109,7 +1135,7 @@ template <int DIM, int ORD, bool CONV, bool W, bool TAB>
 __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
                                           const double2* b, int sweeps, bool reverse, double omega, int tid, int nth,
                                           const double* tabl, int fast = 0, double2* ring = nullptr,
-                                          int waveH = 0) {
+                                          int waveH = 0, int flat_max = 0) {
   constexpr int C1 = ORD == 2 ? 3 : 2;
   constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
   if constexpr (TAB && !CONV && ORD == 2 && DIM == 2 && !W) {
@@ -1154,7 +1180,18 @@ __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const d
           sor_node<DIM, ORD, CONV>(g, cf, cv, x, b, c, idx, omega);
         }
       };
-      if (ORD == 2) {
+      if (ORD == 2 && TAB && !CONV && DIM == 2 && g.n1 <= flat_max) {
+        // small level: one visit of the whole colour (stride 3 in x and y), branch-free evaluation
+        int st[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) st[a] = 3;
+        cta_visit<DIM>(g.n1, res, st, 1, g.n1 - 2, tid, nth, [&](const int* c, int idx) {
+          double invD;
+          const double2 Ax = class_eval_flat2(tabl, x, c[0], c[1], g.n1, invD);
+          const double2 xo = x[idx], bb = b[idx];
+          x[idx] = cadd(xo, cscale(omega * invD, csub(bb, Ax)));
+        });
+      } else if (ORD == 2) {
         // colour residue r: x nodes r + 3m (coalesced); y/z in parity classes r + 3p + 6m so that
         // the row taps are warp-uniform
         for (int cls = 0; cls < (1 << (DIM - 1)); ++cls) {
@@ -1228,11 +1265,23 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
                                                        : ClassTab<DIM>::PER_LEVEL) : nullptr;
   const bool wv = a.wave_h && l < a.lsm && g.n1 >= a.wave_min;
   cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl, a.q2c,
-                                    wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0);
+                                    wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0, a.flat_max);
   double2* rl = S.R(l);
   const double* cvl = S.CV(l);
   if (TAB && !CONV && ORD == 2 && DIM == 2 && (a.q2c == 1 || (a.q2c == 2 && !W))) {
     q2c_residual<W>(tabl, xl, bl, rl, g.n1, tid, nth);
+  } else if (TAB && !CONV && ORD == 2 && DIM == 2 && g.n1 <= a.flat_max) {
+    int s1[DIM], st1[DIM];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      s1[d] = 1;
+      st1[d] = 1;
+    }
+    cta_visit<DIM>(g.n1, s1, st1, 1, g.n1 - 2, tid, nth, [&](const int* c, int i) {
+      double invD;
+      const double2 Ax = class_eval_flat2(tabl, xl, c[0], c[1], g.n1, invD);
+      rl[i] = csub(bl[i], Ax);
+    });
   } else
   cta_all_unknowns<DIM, ORD>(g.n1, tid, nth, [&](const int* c, int i) {
     double2 Ax;
@@ -1358,7 +1407,7 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
                                                    : ClassTab<DIM>::PER_LEVEL) : nullptr;
   const bool wv = a.wave_h && l < a.lsm && g.n1 >= a.wave_min;
   cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl, a.q2c,
-                                    wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0);
+                                    wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0, a.flat_max);
 }
 
 template <int DIM, int ORD, bool CONV, bool TAB>
