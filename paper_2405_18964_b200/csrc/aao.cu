@@ -892,7 +892,10 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   static const char* bud = std::getenv("AAO_SMEM_BUDGET");
   // measured (tools/smem_sweep.sh): keeping only the smallest levels in shared memory leaves the L1
   // to the finest level, which matters more (c2 3.02 vs 3.17 ms, c3 277 vs 437 ms)
-  const size_t budget = bud ? (size_t)std::atol(bud) : 20 * 1024;
+  // 2-D Q2 real operators with the merged small-level visits: no level in shared memory (c2 2.216 -> 2.175 ms:
+  // the L1 cache serves every level better than a split); elsewhere the smallest levels within 20 KB
+  const bool flat2d_sm = c.dim == 2 && S.order == 2 && a.use_ctab && op.conv_sel == 0;
+  const size_t budget = bud ? (size_t)std::atol(bud) : (flat2d_sm ? 0 : 20 * 1024);
   size_t used = tab_bytes;
   a.lsm = a.nlev;
   for (int l = a.nlev - 1; l >= 1; --l) {
@@ -906,7 +909,10 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   }
   // the bottom levels (few unknowns) run warp-synchronously: their phases are pure latency
   static const char* wl = std::getenv("AAO_WARP_UNKNOWNS");
-  const long wmax = wl ? std::atol(wl) : 256;
+  // 2-D Q2 real operators use the merged branch-free colour visits on the small levels (flat_max), which
+  // run faster block-wide than in one warp (c2 precond 2.25 -> 2.22 ms); elsewhere levels <= 256 unknowns
+  const bool flat2d = c.dim == 2 && S.order == 2 && a.use_ctab && op.conv_sel == 0;
+  const long wmax = wl ? std::atol(wl) : (flat2d ? 0 : 256);
   a.lwarp = a.nlev;
   for (int l = 1; l < a.nlev; ++l)
     if (unknowns(a.g[l]) <= wmax) {
