@@ -958,7 +958,8 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
     cudaStreamSynchronize(s);
     std::fprintf(stderr, "mg_clock order %d nprob %d lwarp %d:", S.order, nprob, a.lwarp);
     for (int l = 0; l < a.nlev - 1; ++l) std::fprintf(stderr, " L%d(n1=%d) %llu/%llu", l, a.g[l].n1, h[2 * l], h[2 * l + 1]);
-    std::fprintf(stderr, " bottom %llu\n", h[2 * MG_MAXL - 1]);
+    std::fprintf(stderr, " bottom %llu | L0 down: sweeps %llu residual %llu restrict %llu\n", h[2 * MG_MAXL - 1],
+                 h[2 * MG_MAXL - 2], h[2 * MG_MAXL - 3], h[2 * MG_MAXL - 4]);
   }
 }
 

@@ -1263,9 +1263,20 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
   }
   const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
                                                        : ClassTab<DIM>::PER_LEVEL) : nullptr;
+  // profiling (AAO_MG_CLOCK): split of the level-0 down-leg into sweeps / residual / restriction
+  const bool pclk = a.clk != nullptr && blockIdx.x == 0 && tid == 0 && l == 0;
+  unsigned long long pt = pclk ? clock64() : 0ull;
+  auto pmark = [&](int slot) {
+    if (pclk) {
+      const unsigned long long t1 = clock64();
+      a.clk[slot] += t1 - pt;
+      pt = t1;
+    }
+  };
   const bool wv = a.wave_h && l < a.lsm && g.n1 >= a.wave_min;
   cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl, a.q2c,
                                     wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0, a.flat_max);
+  pmark(2 * MG_MAXL - 2);
   double2* rl = S.R(l);
   const double* cvl = S.CV(l);
   if (TAB && !CONV && ORD == 2 && DIM == 2 && (a.q2c == 1 || (a.q2c == 2 && !W))) {
@@ -1301,6 +1312,7 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
     rl[i] = csub(bl[i], Ax);
   });
   gsync<W>();
+  pmark(2 * MG_MAXL - 3);
   const Grid gc = a.g[l + 1];
   const Transfer t = a.t[l];
   const int o7 = ORD == 2 ? 0 : 2;
@@ -1340,6 +1352,7 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
     bn[I] = acc;
   }
   gsync<W>();
+  pmark(2 * MG_MAXL - 4);
 }
 
 // coarsest level: dense inverse (masked entries of the coarsest iterate read as 0 in the prolongation)
