@@ -1264,7 +1264,7 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
   const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
                                                        : ClassTab<DIM>::PER_LEVEL) : nullptr;
   // profiling (AAO_MG_CLOCK): split of the level-0 down-leg into sweeps / residual / restriction
-  const bool pclk = a.clk != nullptr && blockIdx.x == 0 && tid == 0 && l == 0;
+  const bool pclk = DIM == 2 && a.clk != nullptr && blockIdx.x == 0 && tid == 0 && l == 0;
   unsigned long long pt = pclk ? clock64() : 0ull;
   auto pmark = [&](int slot) {
     if (pclk) {
