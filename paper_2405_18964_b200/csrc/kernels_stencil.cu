@@ -1423,8 +1423,18 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
                                     wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0, a.flat_max);
 }
 
+// threads per CTA of the CTA-resident MG; 3-D measured: 512 (spills at 128 registers) 205 ms vs 256 (no
+// spills, half the warps) 224 ms on c5
+#ifndef MG_THREADS_3D
+#define MG_THREADS_3D 512
+#endif
+template <int DIM, bool TAB>
+constexpr int mg_threads() {
+  return DIM == 3 ? MG_THREADS_3D : (TAB ? MG_THREADS_TAB : MG_THREADS);
+}
+
 template <int DIM, int ORD, bool CONV, bool TAB>
-__global__ void __launch_bounds__(TAB ? MG_THREADS_TAB : MG_THREADS, 1) k_mg_cta(MGArgs a) {
+__global__ void __launch_bounds__(mg_threads<DIM, TAB>(), 1) k_mg_cta(MGArgs a) {
   extern __shared__ double2 smem[];
   const int p = blockIdx.x;
   const int L = a.nlev;
@@ -2359,13 +2369,13 @@ static void mgcta_t(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
     else
       k_mg_q2p<DIM, false><<<nprob, MG_THREADS_TAB, smem, s>>>(a);
   } else if (a.op.conv_sel != 0 && ORD == 2 && a.use_ctab)
-    k_mg_cta<DIM, ORD, true, (ORD == 2)><<<nprob, MG_THREADS_TAB, smem, s>>>(a);
+    k_mg_cta<DIM, ORD, true, (ORD == 2)><<<nprob, mg_threads<DIM, true>(), smem, s>>>(a);
   else if (a.op.conv_sel != 0)
-    k_mg_cta<DIM, ORD, true, false><<<nprob, MG_THREADS, smem, s>>>(a);
+    k_mg_cta<DIM, ORD, true, false><<<nprob, mg_threads<DIM, false>(), smem, s>>>(a);
   else if (ORD == 2 && a.use_ctab)
-    k_mg_cta<DIM, ORD, false, (ORD == 2)><<<nprob, MG_THREADS_TAB, smem, s>>>(a);
+    k_mg_cta<DIM, ORD, false, (ORD == 2)><<<nprob, mg_threads<DIM, true>(), smem, s>>>(a);
   else
-    k_mg_cta<DIM, ORD, false, false><<<nprob, MG_THREADS, smem, s>>>(a);
+    k_mg_cta<DIM, ORD, false, false><<<nprob, mg_threads<DIM, false>(), smem, s>>>(a);
 }
 void launch_mg_cta(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
   SWITCH_DO(a.g[0], mgcta_t, a, nprob, smem, s);
