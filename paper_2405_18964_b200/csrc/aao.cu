@@ -1691,24 +1691,23 @@ aao_status aao_gmres_solve_host(aao_ctx* ctx, const double* b_host, double* x_ho
   if (!ctx || !b_host || !x_host || !kry) return AAO_ERR_SHAPE;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t bytes = ctx->c.N * sizeof(double);
-  double *db = nullptr, *dx = nullptr;
   aao_status st = AAO_OK;
   try {
     if (!ctx->c.gr) aao::gmres_alloc(ctx->c, kry->restart);
+    // device staging for b and x, allocated once per context (owned, freed by aao_destroy)
+    if (!ctx->c.stage_b) {
+      ctx->c.stage_b = aao::dalloc<double>(ctx->c, ctx->c.N);
+      ctx->c.stage_x = aao::dalloc<double>(ctx->c, ctx->c.N);
+    }
   } catch (const CudaError& e) {
     return fail(ctx, e.st, e.what());
   }
-  if (cudaMalloc(&db, bytes) != cudaSuccess || cudaMalloc(&dx, bytes) != cudaSuccess) {
-    if (db) cudaFree(db);
-    return fail(ctx, AAO_ERR_OOM, "aao_gmres_solve_host: cudaMalloc");
-  }
+  double *db = ctx->c.stage_b, *dx = ctx->c.stage_x;
   cudaMemcpyAsync(db, b_host, bytes, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(dx, x_host, bytes, cudaMemcpyHostToDevice, s);
   st = aao_gmres_solve(ctx, db, dx, kry, info, hist, hist_cap, stream);
   cudaMemcpyAsync(x_host, dx, bytes, cudaMemcpyDeviceToHost, s);
   cudaStreamSynchronize(s);
-  cudaFree(db);
-  cudaFree(dx);
   return st;
 }
 

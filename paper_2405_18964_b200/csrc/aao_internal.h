@@ -157,6 +157,7 @@ struct Ctx {
   double *gV = nullptr, *gz = nullptr, *gw = nullptr, *gu = nullptr, *gr = nullptr;
   double *gH = nullptr, *gpart = nullptr, *gscal = nullptr;
   double **gVptr = nullptr;
+  double *stage_b = nullptr, *stage_x = nullptr;   // device staging of aao_gmres_solve_host
   double* hostH = nullptr;   // pinned, 2 x (m + 2): Hessenberg columns of iterations k, k+1
   cudaEvent_t gm_ev[2] = {nullptr, nullptr};
   // bookkeeping
