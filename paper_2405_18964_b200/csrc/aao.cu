@@ -894,7 +894,9 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   // to the finest level, which matters more (c2 3.02 vs 3.17 ms, c3 277 vs 437 ms)
   // 2-D Q2 real operators with the merged small-level visits: no level in shared memory (c2 2.216 -> 2.175 ms:
   // the L1 cache serves every level better than a split); elsewhere the smallest levels within 20 KB
-  const bool flat2d_sm = c.dim == 2 && S.order == 2 && a.use_ctab && op.conv_sel == 0;
+  static const char* fc_env = std::getenv("AAO_FLAT_CONV");   // Oseen small levels flat (default on)
+  const bool flat_conv = fc_env ? std::atoi(fc_env) != 0 : true;
+  const bool flat2d_sm = c.dim == 2 && S.order == 2 && a.use_ctab && (op.conv_sel == 0 || flat_conv);
   const size_t budget = bud ? (size_t)std::atol(bud) : (flat2d_sm ? 0 : 20 * 1024);
   size_t used = tab_bytes;
   a.lsm = a.nlev;
@@ -911,7 +913,7 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   static const char* wl = std::getenv("AAO_WARP_UNKNOWNS");
   // 2-D Q2 real operators use the merged branch-free colour visits on the small levels (flat_max), which
   // run faster block-wide than in one warp (c2 precond 2.25 -> 2.22 ms); elsewhere levels <= 256 unknowns
-  const bool flat2d = c.dim == 2 && S.order == 2 && a.use_ctab && op.conv_sel == 0;
+  const bool flat2d = c.dim == 2 && S.order == 2 && a.use_ctab && (op.conv_sel == 0 || flat_conv);
   const long wmax = wl ? std::atol(wl) : (flat2d ? 0 : 256);
   a.lwarp = a.nlev;
   for (int l = 1; l < a.nlev; ++l)
@@ -940,6 +942,7 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   }
   static const char* flat_env = std::getenv("AAO_FLAT_MAX");
   a.flat_max = flat_env ? std::atoi(flat_env) : 33;   // measured: 33 best (c2 precond 2.371 -> 2.249 ms)
+  if (op.conv_sel != 0 && !flat_conv) a.flat_max = 0;
   static const char* q2c_env = std::getenv("AAO_Q2C");
   a.q2c = q2c_env ? std::atoi(q2c_env) : 0;
   // profiling only: per-level SM-cycle accounting of CTA 0, printed per launch (AAO_MG_CLOCK=1)

@@ -771,6 +771,38 @@ __device__ __forceinline__ double2 class_eval_flat2(const double* tabl, const do
   return cadd(cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])), acc[4]);
 }
 
+// Branch-free 2-D evaluation with complex class coefficients and the per-node convection stencil
+// (Oseen Q_k, Q_k^H: A = a M + b K + c N), for the small levels (as class_eval_flat2).
+__device__ __forceinline__ double2 class_eval_conv_flat2(const double2* tabl, const double* cv, double2 cc,
+                                                         const double2* x, int i, int j, int idx, int n1,
+                                                         double2& D) {
+  const int cls = (i & 1) | ((j & 1) << 1);
+  const double2* T = tabl + cls * ClassTab<2>::NT;
+  const double* cvr = cv + (long)idx * ClassTab<2>::NT;
+  const int xl = i >= 2 ? i - 2 : i, xr = i + 2 <= n1 - 1 ? i + 2 : i;
+  double2 acc[5], nac[5];
+#pragma unroll
+  for (int ob = 0; ob < 5; ++ob) {
+    int r = j + ob - 2;
+    r = r < 0 ? 0 : (r > n1 - 1 ? n1 - 1 : r);
+    const double2* row = x + r * n1;
+    const double2 v[5] = {row[xl], row[i - 1], row[i], row[i + 1], row[xr]};
+    double2 a = cmul(T[ob * 5], v[0]);
+    double2 nn = cscale(__ldg(cvr + ob * 5), v[0]);
+#pragma unroll
+    for (int oa = 1; oa < 5; ++oa) {
+      a = cadd(a, cmul(T[ob * 5 + oa], v[oa]));
+      nn = cfma(__ldg(cvr + ob * 5 + oa), v[oa], nn);
+    }
+    acc[ob] = a;
+    nac[ob] = nn;
+  }
+  D = cadd(T[12], cscale(__ldg(cvr + 12), cc));
+  const double2 A = cadd(cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])), acc[4]);
+  const double2 N = cadd(cadd(cadd(nac[0], nac[1]), cadd(nac[2], nac[3])), nac[4]);
+  return cadd(A, cmul(cc, N));
+}
+
 // ---------------------------------------------------------------- CTA-resident solvers
 // One CTA owns one problem (one frequency / slot / component) and runs the WHOLE fixed-count
 // solve -- every level, colour, transfer and V-cycle -- with block barriers only.  The problems
@@ -1180,7 +1212,18 @@ __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const d
           sor_node<DIM, ORD, CONV>(g, cf, cv, x, b, c, idx, omega);
         }
       };
-      if (ORD == 2 && TAB && !CONV && DIM == 2 && g.n1 <= flat_max) {
+      if (ORD == 2 && TAB && CONV && DIM == 2 && g.n1 <= flat_max) {
+        int st[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) st[a] = 3;
+        cta_visit<DIM>(g.n1, res, st, 1, g.n1 - 2, tid, nth, [&](const int* c, int idx) {
+          double2 D;
+          const double2 Ax = class_eval_conv_flat2(reinterpret_cast<const double2*>(tabl), cv, cf.c, x, c[0], c[1],
+                                                   idx, g.n1, D);
+          const double2 xo = x[idx], bb = b[idx];
+          x[idx] = cadd(xo, cscale(omega, cdiv(csub(bb, Ax), D)));
+        });
+      } else if (ORD == 2 && TAB && !CONV && DIM == 2 && g.n1 <= flat_max) {
         // small level: one visit of the whole colour (stride 3 in x and y), branch-free evaluation
         int st[DIM];
 #pragma unroll
@@ -1281,6 +1324,19 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
   const double* cvl = S.CV(l);
   if (TAB && !CONV && ORD == 2 && DIM == 2 && (a.q2c == 1 || (a.q2c == 2 && !W))) {
     q2c_residual<W>(tabl, xl, bl, rl, g.n1, tid, nth);
+  } else if (TAB && CONV && ORD == 2 && DIM == 2 && g.n1 <= a.flat_max) {
+    int s1[DIM], st1[DIM];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      s1[d] = 1;
+      st1[d] = 1;
+    }
+    cta_visit<DIM>(g.n1, s1, st1, 1, g.n1 - 2, tid, nth, [&](const int* c, int i) {
+      double2 D;
+      const double2 Ax = class_eval_conv_flat2(reinterpret_cast<const double2*>(tabl), cvl, cf.c, xl, c[0], c[1], i,
+                                               g.n1, D);
+      rl[i] = csub(bl[i], Ax);
+    });
   } else if (TAB && !CONV && ORD == 2 && DIM == 2 && g.n1 <= a.flat_max) {
     int s1[DIM], st1[DIM];
 #pragma unroll
