@@ -930,7 +930,12 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   a.wave_h = 0;
   const int wave_min = wmin_env ? std::atoi(wmin_env) : 257;
   const bool wave_on = wave_env ? std::atoi(wave_env) != 0 : a.g[0].n1 >= wave_min;
-  if (wave_on && c.dim == 2 && S.order == 2 && a.use_ctab && op.conv_sel == 0 && !a.perm && c.mg_mode != 1) {
+  // Oseen Q_k / Q_k^H operators: opt-in (AAO_WAVE_CONV=1; c3 precond 255 -> 330 ms: the per-node convection
+  // stencils, re-read from L2 in every band step, outweigh the saved iterate traffic)
+  static const char* wc_env = std::getenv("AAO_WAVE_CONV");
+  const bool wave_conv = wc_env ? std::atoi(wc_env) != 0 : false;
+  if (wave_on && c.dim == 2 && S.order == 2 && a.use_ctab && (op.conv_sel == 0 || wave_conv) && !a.perm &&
+      c.mg_mode != 1) {
     const int n1 = a.g[0].n1;
     static const char* wh_env = std::getenv("AAO_WAVE_H");
     const int h = wh_env ? std::atoi(wh_env) : (n1 <= 129 ? 6 : 3);

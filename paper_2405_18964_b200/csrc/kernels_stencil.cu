@@ -1089,9 +1089,32 @@ __device__ __forceinline__ double2 ring_eval(const double* T, const double2* rin
   return acc;
 }
 
-template <int H>
+template <int RR, int PY>
+__device__ __forceinline__ double2 ring_eval_conv(const double2* T, const double* cvr, double2 cc, const double2* ring,
+                                                  int r0, int i, int n1) {
+  constexpr int AY0 = PY ? 1 : 0, AY1 = PY ? 4 : 5;
+  const int xl = i >= 2 ? i - 2 : i, xr = i + 2 <= n1 - 1 ? i + 2 : i;
+  double2 acc = make_double2(0.0, 0.0), nacc = acc;
+#pragma unroll
+  for (int ob = AY0; ob < AY1; ++ob) {
+    int r = r0 + ob - 2;
+    r += r < 0 ? RR : 0;
+    r -= r >= RR ? RR : 0;
+    const double2* row = ring + r * n1;
+    const double2 v[5] = {row[xl], row[i - 1], row[i], row[i + 1], row[xr]};
+#pragma unroll
+    for (int oa = 0; oa < 5; ++oa) {
+      acc = cadd(acc, cmul(T[ob * 5 + oa], v[oa]));
+      nacc = cfma(__ldg(cvr + ob * 5 + oa), v[oa], nacc);
+    }
+  }
+  return cadd(acc, cmul(cc, nacc));
+}
+
+template <int H, bool CONV = false>
 __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __restrict__ b, double2* ring, int n1,
-                             bool reverse, double omega, int tid, int nth) {
+                             bool reverse, double omega, int tid, int nth, const double* cv = nullptr,
+                             double2 cc = make_double2(0.0, 0.0)) {
   constexpr int RR = 8 * H;   // ring rows: 8 bands
   const int nb = (n1 + H - 1) / H;
   auto band_rows = [&](int band, int& j0, int& cnt) {
@@ -1148,12 +1171,22 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
         const double2 bb = b[(long)j * n1 + i];
         const int r0 = j % RR;
         const int ccls = (i & 1) | ((j & 1) << 1);
-        const double* Tc = tabl + ccls * (ClassTab<2>::NT + 1);
-        const double invD = Tc[ClassTab<2>::NT];
-        const double2 Ax = (j & 1) ? ring_eval<RR, 1>(Tc, ring, r0, i, n1) : ring_eval<RR, 0>(Tc, ring, r0, i, n1);
         double2* xp = ring + r0 * n1 + i;
-        const double2 xo = *xp;
-        *xp = make_double2(xo.x + omega * invD * (bb.x - Ax.x), xo.y + omega * invD * (bb.y - Ax.y));
+        if constexpr (CONV) {
+          const double2* Tc = reinterpret_cast<const double2*>(tabl) + ccls * ClassTab<2>::NT;
+          const double* cvr = cv + ((long)j * n1 + i) * ClassTab<2>::NT;
+          const double2 Ax = (j & 1) ? ring_eval_conv<RR, 1>(Tc, cvr, cc, ring, r0, i, n1)
+                                     : ring_eval_conv<RR, 0>(Tc, cvr, cc, ring, r0, i, n1);
+          const double2 D = cadd(Tc[12], cscale(__ldg(cvr + 12), cc));
+          const double2 xo = *xp;
+          *xp = cadd(xo, cscale(omega, cdiv(csub(bb, Ax), D)));
+        } else {
+          const double* Tc = tabl + ccls * (ClassTab<2>::NT + 1);
+          const double invD = Tc[ClassTab<2>::NT];
+          const double2 Ax = (j & 1) ? ring_eval<RR, 1>(Tc, ring, r0, i, n1) : ring_eval<RR, 0>(Tc, ring, r0, i, n1);
+          const double2 xo = *xp;
+          *xp = make_double2(xo.x + omega * invD * (bb.x - Ax.x), xo.y + omega * invD * (bb.y - Ax.y));
+        }
       }
       __syncthreads();
     }
@@ -1170,6 +1203,17 @@ __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const d
                                           int waveH = 0, int flat_max = 0) {
   constexpr int C1 = ORD == 2 ? 3 : 2;
   constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
+  if constexpr (TAB && CONV && ORD == 2 && DIM == 2 && !W) {
+    if (ring && waveH) {
+      for (int sw = 0; sw < sweeps; ++sw) {
+        if (waveH == 6)
+          q2_wave_pass<6, true>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cf.c);
+        else
+          q2_wave_pass<3, true>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cf.c);
+      }
+      return;
+    }
+  }
   if constexpr (TAB && !CONV && ORD == 2 && DIM == 2 && !W) {
     if (ring && waveH) {
       for (int sw = 0; sw < sweeps; ++sw) {
