@@ -925,11 +925,9 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   // iterate crosses HBM once per sweep instead of once per colour -- measured c4_64 precond 43.6 -> 35.2 ms,
   // c4_128 87.8 -> 73.5 ms; slower where the level is L2-resident (c2, n1 = 129: 2.37 -> 2.73 ms).
   // AAO_WAVE=0/1 forces it off/on for every eligible level >= AAO_WAVE_MIN; AAO_WAVE_H: band height.
-  static const char* wave_env = std::getenv("AAO_WAVE");
-  static const char* wmin_env = std::getenv("AAO_WAVE_MIN");
   a.wave_h = 0;
-  const int wave_min = wmin_env ? std::atoi(wmin_env) : 257;
-  const bool wave_on = wave_env ? std::atoi(wave_env) != 0 : a.g[0].n1 >= wave_min;
+  const int wave_min = c.wave_min;   // per context (AAO_WAVE_MIN at aao_create)
+  const bool wave_on = c.wave_force >= 0 ? c.wave_force != 0 : a.g[0].n1 >= wave_min;
   // Oseen Q_k / Q_k^H operators: opt-in (AAO_WAVE_CONV=1; c3 precond 255 -> 330 ms: the per-node convection
   // stencils, re-read from L2 in every band step, outweigh the saved iterate traffic)
   static const char* wc_env = std::getenv("AAO_WAVE_CONV");
@@ -1614,6 +1612,10 @@ aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
     const char* mm = std::getenv("AAO_MG_MODE");
     ctx->c.mg_mode = mm ? std::atoi(mm) : -1;
     ctx->c.real_split_auto = std::getenv("AAO_REAL_SPLIT") != nullptr;
+    const char* we = std::getenv("AAO_WAVE");
+    ctx->c.wave_force = we ? std::atoi(we) : -1;
+    const char* wm = std::getenv("AAO_WAVE_MIN");
+    ctx->c.wave_min = wm ? std::atoi(wm) : 257;
     aao::setup(ctx->c, *cfg);
     for (auto& e : ctx->c.ev) cudaEventCreate(&e);
     cudaStreamCreateWithFlags(&ctx->c.s2, cudaStreamNonBlocking);

@@ -171,6 +171,7 @@ struct Ctx {
   // live timing of the dominant kernel class (finest-level multicolour SOR sweeps)
   cudaStream_t s2 = nullptr;               // side stream: pressure solves overlap the velocity MG
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int wave_force = -1, wave_min = 257;   // band-wavefront sweeps: AAO_WAVE (-1 auto), AAO_WAVE_MIN
   int mg_mode = -1;      // MG schedule: -1 auto, 0 CTA-resident, 1 per level/colour launches, 2 hybrid (AAO_MG_MODE)
   int tail = -1;
   bool real_split_auto = false;   // real-split MG in auto mode (AAO_REAL_SPLIT); measured slower on c2         // hybrid: first CTA-resident level of the current solve

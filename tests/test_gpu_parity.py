@@ -295,3 +295,17 @@ def test_arnoldi_hessenberg_parity(cfg):
     ritz_g = np.sort_complex(np.linalg.eigvals(Hg[:m, :m]))
     ritz_o = np.sort_complex(np.linalg.eigvals(Ho[:m, :m]))
     assert np.max(np.abs(ritz_g - ritz_o)) <= 1e-7 * np.max(np.abs(ritz_o))
+
+
+@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[1], SMALL[3]], ids=lambda c: c.name)
+def test_band_wavefront_sweeps_match_oracle(cfg, monkeypatch):
+    """The band-wavefront colour fusion (default only for n1 >= 257) forced on every small level: the same
+    map as the per-colour sweeps (ring wrap, partial last band, odd/even n_b, Oseen operators)."""
+    torch = _torch()
+    monkeypatch.setenv("AAO_WAVE", "1")
+    monkeypatch.setenv("AAO_WAVE_MIN", "9")
+    _, pc = oracle_for(cfg)
+    ctx = gpu_ctx(cfg)
+    r = synth.probe_vector(cfg)
+    z = ctx.precond_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert rel(z, pc.apply(r)) <= PRECOND_TOL
