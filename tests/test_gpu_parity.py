@@ -223,6 +223,28 @@ def test_full_size_frequency_sampled_parity(name):
             assert rel(blk[h], prob_block(cfg, Y[h], Q[h])) <= PRECOND_TOL
 
 
+def test_largest_config_sampled_parity():
+    """The largest BASELINE workload (c4 at n_t = 512: 6.05e8 DOFs, n_b = 511, 513^2 velocity level) in the
+    launch configuration bench/sweeps use (band-wavefront sweeps, 8-frequency DFT tiles): preconditioner
+    frequency blocks k = 0, 1, n_f - 1 against the oracle.  (kkt_apply at this size is covered by the
+    same kernels' full-vector parity on c4_64; the oracle's 6e8-entry product is too large for the host.)"""
+    torch = _torch()
+    cfg = synth.CONFIGS["c4_512"]
+    prob, pc = oracle_for(cfg)
+    ctx = gpu_ctx(cfg)
+    r = synth.probe_vector(cfg)
+    rd = torch.from_numpy(r).cuda()
+    ctx.precond_apply(rd)
+    torch.cuda.synchronize()
+    for k in (0, 1, cfg.n_f - 1):
+        Y, Q = pc.freq_block(r, k)
+        blk = ctx.debug_freq_block(k)
+        for h in range(2):
+            assert rel(blk[h], prob_block(cfg, Y[h], Q[h])) <= PRECOND_TOL
+    del rd
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("cfg", [SMALL[0], SMALL[3], SMALL[5]], ids=lambda c: c.name)
 def test_per_level_launch_mode_matches_oracle(cfg, monkeypatch):
     """The per-level / per-colour launch schedule (AAO_MG_MODE=1) computes the same map."""
