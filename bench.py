@@ -186,8 +186,12 @@ def run_ours(args):
         x.zero_()
         return ctx.gmres_solve(b, x, tol=1e-6, restart=30)
 
-    for _ in range(args.warmup):
+    for w in range(args.warmup):
+        if w == args.warmup - 1:
+            ctx.profile_smoother(True)      # last warm-up: creates the profiling events the timed region reuses
         _, info, hist, rc = solve()
+    ctx.profile_read()
+    ctx.profile_smoother(False)
     launches_per_step = ctx.last_launch_count()
     its = info["iterations"]
 
@@ -200,6 +204,7 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.profile_smoother(True)   # dominant kernel timed live: events around each velocity-MG launch, same stream
     e0.record(stream)
     its_total = 0
     for _ in range(args.steps):
@@ -209,6 +214,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     clocks = sampler.stop()
+    sm_ms, sm_bytes, sm_launches = ctx.profile_read()
+    ctx.profile_smoother(False)
     ms, its_all = aggregate_replicas(e0.elapsed_time(e1), its_total, world)
     ms_per_step = ms / args.steps
     value = cfg.n_dofs * its_all / (ms / 1e3)
@@ -236,11 +243,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     kkt_ms = e0.elapsed_time(e1) / n_app
 
-    # ---------------- dominant kernel class, live: finest-level multicolour SOR sweeps of one solve
-    ctx.profile_smoother(True)
-    solve()
-    sm_ms, sm_bytes, sm_launches = ctx.profile_read()
-    ctx.profile_smoother(False)
+    # ---------------- dominant kernel (velocity MG launches) over the timed region, read above
     peaks = load_peaks()
     peak = peaks["hbm_gbs"] if peaks else 6650.0
     achieved = sm_bytes / (sm_ms / 1e3) / 1e9 if sm_ms > 0 else 0.0
@@ -255,7 +258,8 @@ def run_ours(args):
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks else "fallback (B200_PROFILING.md)",
                 "traffic": traffic, "algorithmic_bytes_per_launch": sm_bytes / max(sm_launches, 1),
-                "avg_launch_us": 1e3 * sm_ms / max(sm_launches, 1), "share_of_step": sm_ms / ms_per_step}
+                "avg_launch_us": 1e3 * sm_ms / max(sm_launches, 1), "share_of_step": sm_ms / (ms_per_step * args.steps),
+                "measured": f"CUDA events around every velocity-MG launch of the {args.steps} timed solves"}
 
     # ---------------- end to end through the public API with HOST buffers (copies inside)
     bh = torch.empty(ctx.N, dtype=torch.float64).pin_memory()
