@@ -1353,7 +1353,17 @@ void gmres_alloc(Ctx& c, int m) {
   std::vector<double*> ptr(m + 1);
   for (int i = 0; i <= m; ++i) ptr[i] = c.gV + (size_t)i * N;
   c.gVptr = upload(c, ptr);
-  if (c.nonlinear) {   // FGMRES stores the preconditioned vectors Z_k = P_k^{-1} v_k
+  // FGMRES stores the preconditioned vectors Z_k = P_k^{-1} v_k; the linear mode keeps them too when the
+  // extra m vectors fit (then the restart update x += Z y needs no extra preconditioner application:
+  // Algorithm 1 is a fixed linear map, so Z y = P^{-1}(V y) up to rounding).  AAO_STORE_Z=0 disables.
+  {
+    static const char* sz = std::getenv("AAO_STORE_Z");
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t need = (size_t)m * N * sizeof(double);
+    c.store_z = c.nonlinear || ((sz ? std::atoi(sz) != 0 : true) && need < free_b / 2);
+  }
+  if (c.store_z) {
     c.gZ = dalloc<double>(c, (size_t)m * N);
     std::vector<double*> zp(m);
     for (int i = 0; i < m; ++i) zp[i] = c.gZ + (size_t)i * N;
@@ -1415,7 +1425,7 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
     auto enqueue = [&](int k) {
       double* Vk = c.gV + (size_t)k * N;
       double* w = c.gV + (size_t)(k + 1) * N;
-      double* zk = c.nonlinear ? c.gZ + (size_t)k * N : c.gz;
+      double* zk = c.store_z ? c.gZ + (size_t)k * N : c.gz;
       precond_apply(c, Vk, zk, s);
       kkt_apply(c, zk, w, s);
       double* hcol = c.gH + (size_t)k * (m + 1);
@@ -1480,7 +1490,7 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
       y[i] = acc / H[(size_t)i * m + i];
     }
     CK(cudaMemcpyAsync(c.gscal + 8, y.data(), sizeof(double) * kdone, cudaMemcpyHostToDevice, s));
-    if (c.nonlinear) {   // FGMRES: x += Z_k y
+    if (c.store_z) {     // FGMRES, or linear with stored Z: x += Z_k y
       launch_multi_axpy(c.gz, (const double* const*)c.gZptr, c.gscal + 8, kdone, N, s);
       ++launch_counter();
     } else {             // GMRES: x += P^{-1}(V_k y)
