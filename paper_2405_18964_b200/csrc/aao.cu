@@ -1355,13 +1355,14 @@ void gmres_alloc(Ctx& c, int m) {
   c.gVptr = upload(c, ptr);
   // FGMRES stores the preconditioned vectors Z_k = P_k^{-1} v_k; the linear mode keeps them too when the
   // extra m vectors fit (then the restart update x += Z y needs no extra preconditioner application:
-  // Algorithm 1 is a fixed linear map, so Z y = P^{-1}(V y) up to rounding).  AAO_STORE_Z=0 disables.
+  // Algorithm 1 is a fixed linear map, so Z y = P^{-1}(V y) up to rounding).  AAO_STORE_Z=0 (read at
+  // aao_create) disables it: summing the z_k is less accurate when P^{-1} is ill-conditioned, which limits
+  // the attainable residual of very tight solves (the nu = 1 manufactured problem stalls above 1e-9).
   {
-    static const char* sz = std::getenv("AAO_STORE_Z");
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     const size_t need = (size_t)m * N * sizeof(double);
-    c.store_z = c.nonlinear || ((sz ? std::atoi(sz) != 0 : true) && need < free_b / 2);
+    c.store_z = c.nonlinear || (c.store_z_opt && need < free_b / 2);
   }
   if (c.store_z) {
     c.gZ = dalloc<double>(c, (size_t)m * N);
@@ -1622,6 +1623,8 @@ aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
     const char* mm = std::getenv("AAO_MG_MODE");
     ctx->c.mg_mode = mm ? std::atoi(mm) : -1;
     ctx->c.real_split_auto = std::getenv("AAO_REAL_SPLIT") != nullptr;
+    const char* szo = std::getenv("AAO_STORE_Z");
+    ctx->c.store_z_opt = szo ? std::atoi(szo) != 0 : true;
     const char* we = std::getenv("AAO_WAVE");
     ctx->c.wave_force = we ? std::atoi(we) : -1;
     const char* wm = std::getenv("AAO_WAVE_MIN");

@@ -150,6 +150,7 @@ struct Ctx {
   int inner_max = 0;
   double2* debug_block_src_v = nullptr;  // frequency vector of the last NL solution (debug block)
   double2* debug_block_src_p = nullptr;
+  bool store_z_opt = true;               // AAO_STORE_Z at aao_create
   bool store_z = false;                  // GMRES keeps Z_k = P^{-1} v_k (FGMRES always; linear if it fits)
   double* gZ = nullptr;                  // FGMRES preconditioned basis
   double** gZptr = nullptr;

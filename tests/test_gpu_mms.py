@@ -60,7 +60,7 @@ def _velocity_error(cfg, x):
 
 @pytest.mark.parametrize("nc,nt,tol,xtol,etol", [(4, 8, 1e-10, 1e-5, 1e-3), (8, 16, 1e-10, 1e-5, 1e-3),
                                                     (16, 32, 1e-9, None, None)])
-def test_manufactured_solution_gpu_gmres(nc, nt, tol, xtol, etol):
+def test_manufactured_solution_gpu_gmres(nc, nt, tol, xtol, etol, monkeypatch):
     """GPU GMRES(30) with the linear preconditioner reaches the direct solution of the same discrete system;
     the system is ill-conditioned (nu = 1 on [-1,1]^2), so a residual of 1e-10 leaves ~1e-7 in x and the
     16 x 16 x 32 case (GMRES(30) stagnates below 1e-9; the oracle's sparse direct solve takes minutes there)
@@ -69,6 +69,8 @@ def test_manufactured_solution_gpu_gmres(nc, nt, tol, xtol, etol):
     from oracle.manufactured import solve_manufactured
     from paper_2405_18964_b200 import Context
     cfg = synth.mms_config(nc, nt)
+    # restart update x += P^{-1}(V y) (not the stored-Z sum): the tighter attainable accuracy at 1e-9..1e-10
+    monkeypatch.setenv("AAO_STORE_Z", "0")
     ctx = Context.from_config(cfg, None)
     b = ctx.build_rhs_general(*synth.mms_inputs(cfg))
     x, info, hist, rc = ctx.gmres_solve(b, tol=tol, restart=30, max_iters=12000)
