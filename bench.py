@@ -311,8 +311,8 @@ def run_ours(args):
                            "n_t": cfg.n_t, "beta": cfg.beta, "nu": cfg.nu, "n_dofs": cfg.n_dofs,
                            "step": "one GMRES(30) solve to 1e-6 from x0=0", "gmres_iterations": its,
                            "parallelism": f"replicas x{world}",
-                           "l2": "no flush: per-step working set (31-vector Krylov basis, "
-                                 f"{31 * cfg.n_dofs * 8 / 1e9:.2f} GB) exceeds the 126 MB L2"},
+                           "l2": "no flush: per-step working set (31-vector Krylov basis + 30 preconditioned vectors, "
+                                 f"{61 * cfg.n_dofs * 8 / 1e9:.2f} GB) exceeds the 126 MB L2"},
                 "precond_applies_per_s": 1e3 / precond_ms, "precond_ms": precond_ms,
                 "precond_dofs_per_s": cfg.n_dofs / (precond_ms / 1e3),
                 "kkt_ms": kkt_ms, "kkt_dofs_per_s": cfg.n_dofs / (kkt_ms / 1e3),
