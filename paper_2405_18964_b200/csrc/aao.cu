@@ -949,8 +949,6 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   static const char* flat_env = std::getenv("AAO_FLAT_MAX");
   a.flat_max = flat_env ? std::atoi(flat_env) : 33;   // measured: 33 best (c2 precond 2.371 -> 2.249 ms)
   if (op.conv_sel != 0 && !flat_conv) a.flat_max = 0;
-  static const char* q2c_env = std::getenv("AAO_Q2C");
-  a.q2c = q2c_env ? std::atoi(q2c_env) : 0;
   // profiling only: per-level SM-cycle accounting of CTA 0, printed per launch (AAO_MG_CLOCK=1)
   static const bool mg_clock = std::getenv("AAO_MG_CLOCK") != nullptr;
   static unsigned long long* clk_dev = nullptr;

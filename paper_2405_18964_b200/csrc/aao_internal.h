@@ -81,7 +81,6 @@ struct MGArgs {
   int wave_h, wave_min;     // band-wavefront sweeps (2-D Q2 real): band height (3 or 6), levels with n1 >= wave_min
   long ring_off;            // ring buffer offset in dynamic smem (double2 units)
   int flat_max;             // 2-D Q2 real: levels with n1 <= flat_max use merged branch-free colour visits
-  int q2c;                  // 2-D Q2 real class stencils: parity sub-lattice sweeps (AAO_Q2C)
   unsigned long long* clk;  // profiling (AAO_MG_CLOCK): CTA 0 accumulates SM cycles per [level][down, up]
 };
 

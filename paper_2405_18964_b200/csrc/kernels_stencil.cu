@@ -948,107 +948,6 @@ __device__ __forceinline__ void cta_all_unknowns(int n1, int tid, int nth, F&& f
   }
 }
 
-// ---- fast path: 2-D Q2, real class stencils (Stokes W_k, K-type operators) ----------------------
-// The nodes of one multicolour-SOR colour (residues (rx, ry) mod 3) split into four sub-lattices of
-// stride 6 with fixed (x, y) parity, i.e. a fixed class stencil: every tap offset is a compile-time
-// constant (no clamping, no zero taps, no per-node class lookup), so a node update is its loads,
-// 2 FMAs per tap and the update.  The residual pass uses the four parity sub-lattices of stride 2.
-// Node coordinates come from a float reciprocal (exact for these sizes, with an integer correction).
-template <int PX, int PY, bool RES>
-__device__ __forceinline__ void q2c_sub(const double* T, double2* x, const double2* __restrict__ b,
-                                        double2* __restrict__ r, int n1, int sx, int sy, int step, double omega,
-                                        int tid, int nth) {
-  constexpr int OA0 = PX ? 1 : 0, OA1 = PX ? 4 : 5, OB0 = PY ? 1 : 0, OB1 = PY ? 4 : 5;
-  const int hi = n1 - 2;
-  const int cx = sx > hi ? 0 : (hi - sx) / step + 1;
-  const int cy = sy > hi ? 0 : (hi - sy) / step + 1;
-  const int total = cx * cy;
-  if (total == 0) return;
-  const float rcx = 1.0f / (float)cx;
-  const double oinv = omega * T[25];
-  for (int t = tid; t < total; t += nth) {
-    int n = __float2int_rz(((float)t + 0.5f) * rcx);
-    int m = t - n * cx;
-    if (m >= cx) {
-      m -= cx;
-      ++n;
-    } else if (m < 0) {
-      m += cx;
-      --n;
-    }
-    const int idx = (sy + step * n) * n1 + sx + step * m;
-    const double2 bb = b[idx];
-    const double2* p = x + idx - 2 * n1;
-    double ax0 = 0.0, ay0 = 0.0, ax1 = 0.0, ay1 = 0.0;
-    double2 xc = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int ob = OB0; ob < OB1; ++ob) {
-      const double2* row = p + ob * n1;
-#pragma unroll
-      for (int oa = OA0; oa < OA1; ++oa) {
-        const double2 v = row[oa - 2];
-        if (ob == 2 && oa == 2) xc = v;
-        const double w = T[ob * 5 + oa];
-        if ((oa + ob) & 1) {
-          ax1 = fma(w, v.x, ax1);
-          ay1 = fma(w, v.y, ay1);
-        } else {
-          ax0 = fma(w, v.x, ax0);
-          ay0 = fma(w, v.y, ay0);
-        }
-      }
-    }
-    const double rx = bb.x - (ax0 + ax1), ry = bb.y - (ay0 + ay1);
-    if (RES)
-      r[idx] = make_double2(rx, ry);
-    else
-      x[idx] = make_double2(fma(oinv, rx, xc.x), fma(oinv, ry, xc.y));
-  }
-}
-
-template <bool RES>
-__device__ __forceinline__ void q2c_dispatch(const double* tabl, double2* x, const double2* b, double2* r, int n1,
-                                             int sx, int sy, int step, double omega, int tid, int nth) {
-  const int cls = (sx & 1) | ((sy & 1) << 1);
-  const double* T = tabl + cls * ClassTab<2>::NT + cls;   // (NT + 1) doubles per class
-  switch (cls) {
-    case 0: q2c_sub<0, 0, RES>(T, x, b, r, n1, sx, sy, step, omega, tid, nth); break;
-    case 1: q2c_sub<1, 0, RES>(T, x, b, r, n1, sx, sy, step, omega, tid, nth); break;
-    case 2: q2c_sub<0, 1, RES>(T, x, b, r, n1, sx, sy, step, omega, tid, nth); break;
-    default: q2c_sub<1, 1, RES>(T, x, b, r, n1, sx, sy, step, omega, tid, nth); break;
-  }
-}
-
-template <bool W>
-__device__ void q2c_sweep(const double* tabl, double2* x, const double2* b, int n1, int sweeps, bool reverse,
-                          double omega, int tid, int nth) {
-  for (int sw = 0; sw < sweeps; ++sw)
-    for (int cc = 0; cc < 9; ++cc) {
-      const int colour = reverse ? 8 - cc : cc;
-      const int rx = colour % 3, ry = colour / 3;
-#pragma unroll
-      for (int qy = 0; qy < 2; ++qy)
-#pragma unroll
-        for (int qx = 0; qx < 2; ++qx) {
-          int sx = rx + 3 * qx, sy = ry + 3 * qy;   // residue mod 6; node 0 is a boundary node
-          if (sx == 0) sx = 6;
-          if (sy == 0) sy = 6;
-          q2c_dispatch<false>(tabl, x, b, nullptr, n1, sx, sy, 6, omega, tid, nth);
-        }
-      gsync<W>();
-    }
-}
-
-template <bool W>
-__device__ void q2c_residual(const double* tabl, const double2* x, const double2* b, double2* r, int n1, int tid,
-                             int nth) {
-#pragma unroll
-  for (int qy = 0; qy < 2; ++qy)
-#pragma unroll
-    for (int qx = 0; qx < 2; ++qx)
-      q2c_dispatch<true>(tabl, const_cast<double2*>(x), b, r, n1, 1 + qx, 1 + qy, 2, 0.0, tid, nth);
-}
-
 // ---- band-wavefront multicolour SOR (2-D Q2, real class stencils) --------------------------------
 // The 9 colour steps of one sweep are fused into ONE pass over the grid.  Rows are grouped in bands of
 // H rows; a row j of class c = (j mod 3) (c' = 2 - c for the reversed colour order) is updated at step
@@ -1199,7 +1098,7 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
 template <int DIM, int ORD, bool CONV, bool W, bool TAB>
 __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
                                           const double2* b, int sweeps, bool reverse, double omega, int tid, int nth,
-                                          const double* tabl, int fast = 0, double2* ring = nullptr,
+                                          const double* tabl, double2* ring = nullptr,
                                           int waveH = 0, int flat_max = 0) {
   constexpr int C1 = ORD == 2 ? 3 : 2;
   constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
@@ -1224,12 +1123,6 @@ __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const d
           default: q2_wave_pass<12>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth); break;
         }
       }
-      return;
-    }
-  }
-  if constexpr (TAB && !CONV && ORD == 2 && DIM == 2) {
-    if (fast == 1 || (fast == 2 && !W)) {
-      q2c_sweep<W>(tabl, x, b, g.n1, sweeps, reverse, omega, tid, nth);
       return;
     }
   }
@@ -1361,14 +1254,12 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
     }
   };
   const bool wv = a.wave_h && l < a.lsm && g.n1 >= a.wave_min;
-  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl, a.q2c,
+  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl,
                                     wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0, a.flat_max);
   pmark(2 * MG_MAXL - 2);
   double2* rl = S.R(l);
   const double* cvl = S.CV(l);
-  if (TAB && !CONV && ORD == 2 && DIM == 2 && (a.q2c == 1 || (a.q2c == 2 && !W))) {
-    q2c_residual<W>(tabl, xl, bl, rl, g.n1, tid, nth);
-  } else if (TAB && CONV && ORD == 2 && DIM == 2 && g.n1 <= a.flat_max) {
+  if (TAB && CONV && ORD == 2 && DIM == 2 && g.n1 <= a.flat_max) {
     int s1[DIM], st1[DIM];
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
@@ -1519,7 +1410,7 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
   const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
                                                    : ClassTab<DIM>::PER_LEVEL) : nullptr;
   const bool wv = a.wave_h && l < a.lsm && g.n1 >= a.wave_min;
-  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl, a.q2c,
+  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl,
                                     wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0, a.flat_max);
 }
 
