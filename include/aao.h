@@ -117,9 +117,14 @@ const char* aao_last_error(const aao_ctx* ctx);   /* never NULL; "" when no erro
 size_t aao_vector_len(const aao_ctx* ctx);         /* N = 2 n_b (n_v + n_p) */
 size_t aao_device_bytes(const aao_ctx* ctx);       /* workspace owned by the context */
 
-/* Masked copy: out = in with masked entries (Dirichlet nodes, pinned pressure node) set to 0.
+/* Paper order -> internal layout.  The internal (layout-T) vector IS the paper's ordering
+   [half][time block][field][full-grid node] (P:118-149 block structure), so packing
+   is a masked copy: out = in with masked entries (Dirichlet nodes, pinned pressure node) set to 0.
    Device pointers; in == out allowed. */
 aao_status aao_pack(aao_ctx* ctx, const double* in, double* out, void* stream);
+
+/* Internal layout -> paper order: the same masked copy (the layouts coincide).  Device pointers. */
+aao_status aao_unpack(aao_ctx* ctx, const double* in, double* out, void* stream);
 
 /* Right-hand side for v_0 = 0, f = 0, h = 0:
    b = tau * (M_full v_d)|_interior in every adjoint-velocity block (half 0), 0 elsewhere.

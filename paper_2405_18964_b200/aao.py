@@ -45,7 +45,7 @@ class Info(ctypes.Structure):
 
 
 EXPORTS = ["aao_config_defaults", "aao_create", "aao_destroy", "aao_last_error", "aao_vector_len",
-           "aao_device_bytes", "aao_pack", "aao_build_rhs", "aao_build_rhs_general", "aao_arnoldi", "aao_kkt_apply",
+           "aao_device_bytes", "aao_pack", "aao_unpack", "aao_build_rhs", "aao_build_rhs_general", "aao_arnoldi", "aao_kkt_apply",
            "aao_precond_apply",
            "aao_gmres_solve", "aao_gmres_solve_host", "aao_debug_freq_block", "aao_set_timing",
            "aao_last_phase_ms", "aao_last_launch_count", "aao_profile_smoother", "aao_profile_read",
@@ -73,7 +73,7 @@ def load(path: str = LIB_PATH):
     L.aao_vector_len.restype = ctypes.c_size_t
     L.aao_device_bytes.argtypes = [vp]
     L.aao_device_bytes.restype = ctypes.c_size_t
-    for name in ("aao_pack", "aao_build_rhs", "aao_kkt_apply", "aao_precond_apply"):
+    for name in ("aao_pack", "aao_unpack", "aao_build_rhs", "aao_kkt_apply", "aao_precond_apply"):
         getattr(L, name).argtypes = [vp, vp, vp, vp]
         getattr(L, name).restype = st
     L.aao_arnoldi.argtypes = [vp, vp, i, dp, ctypes.POINTER(ctypes.c_int), vp]
@@ -187,6 +187,12 @@ class Context:
     def pack(self, x, out=None, stream=None):
         out = self.empty() if out is None else out
         self._check(self.L.aao_pack(self.h, _ptr(self._vec(x)), _ptr(self._vec(out)), self._stream(stream)), "pack")
+        return out
+
+    def unpack(self, x, out=None, stream=None):
+        out = self.empty() if out is None else out
+        self._check(self.L.aao_unpack(self.h, _ptr(self._vec(x)), _ptr(self._vec(out)), self._stream(stream)),
+                    "unpack")
         return out
 
     def build_rhs(self, vd_q2, out=None, stream=None):

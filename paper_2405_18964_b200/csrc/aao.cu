@@ -1668,6 +1668,10 @@ aao_status aao_pack(aao_ctx* ctx, const double* in, double* out, void* stream) {
   return AAO_OK;
 }
 
+aao_status aao_unpack(aao_ctx* ctx, const double* in, double* out, void* stream) {
+  return aao_pack(ctx, in, out, stream);
+}
+
 aao_status aao_build_rhs(aao_ctx* ctx, const double* vd, double* b, void* stream) {
   if (!ctx || !vd || !b) return AAO_ERR_SHAPE;
   ABI_GUARD(ctx, { aao::launch_rhs(ctx->c, vd, b, (cudaStream_t)stream); ++aao::launch_counter(); });

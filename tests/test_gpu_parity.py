@@ -331,3 +331,17 @@ def test_band_wavefront_sweeps_match_oracle(cfg, monkeypatch):
     r = synth.probe_vector(cfg)
     z = ctx.precond_apply(torch.from_numpy(r).cuda()).cpu().numpy()
     assert rel(z, pc.apply(r)) <= PRECOND_TOL
+
+
+def test_pack_unpack_masked_round_trip():
+    """aao_pack / aao_unpack: the internal layout is the paper's order; both are the masked
+    copy (Dirichlet nodes and the pinned pressure node -> 0, every other entry bit-identical)."""
+    torch = _torch()
+    cfg = SMALL[0]
+    ctx = gpu_ctx(cfg)
+    g = np.random.default_rng(4).standard_normal(ctx.N)
+    gd = torch.from_numpy(g).cuda()
+    p = ctx.pack(gd)
+    u = ctx.unpack(p).cpu().numpy()
+    ref = np.where(synth.full_mask(cfg), g, 0.0)
+    assert np.array_equal(p.cpu().numpy(), ref) and np.array_equal(u, ref)
