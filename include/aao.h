@@ -97,11 +97,15 @@ typedef struct {
   int breakdown;         /* 1 if h_{k+1,k} < 1e-14 ||b||                                    */
   double final_relres;   /* last recurrence residual / ||b||                                */
   double true_relres;    /* ||b - A x|| / ||b|| recomputed at exit                           */
-  int precond_applies;   /* including the x-update application per cycle                    */
+  int precond_applies;   /* Arnoldi applications, plus one per cycle when the preconditioned vectors
+                            are not stored (x += P^{-1}(V y))                                  */
   double ms_total;       /* wall time of the solve (host clock around device work)           */
   long inner_its_total;  /* nonlinear mode: inner GMRES iterations summed over frequencies and
                             preconditioner applications of this solve                        */
   int inner_its_max;     /* nonlinear mode: largest inner iteration count of one frequency    */
+  double ms_precond;     /* device time summed over the Arnoldi iterations: preconditioner,   */
+  double ms_kkt;         /*   KKT matvec and Gram-Schmidt (+ normalisation); filled only after */
+  double ms_orth;        /*   aao_set_timing(ctx, 1) (events; the speculative enqueue is off)  */
 } aao_info;
 
 /* Assemble operators and per-frequency data, allocate all device workspace (step A9).

@@ -38,7 +38,8 @@ class Info(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int), ("restarts", ctypes.c_int), ("converged", ctypes.c_int),
                 ("breakdown", ctypes.c_int), ("final_relres", ctypes.c_double),
                 ("true_relres", ctypes.c_double), ("precond_applies", ctypes.c_int),
-                ("ms_total", ctypes.c_double), ("inner_its_total", ctypes.c_long), ("inner_its_max", ctypes.c_int)]
+                ("ms_total", ctypes.c_double), ("inner_its_total", ctypes.c_long), ("inner_its_max", ctypes.c_int),
+                ("ms_precond", ctypes.c_double), ("ms_kkt", ctypes.c_double), ("ms_orth", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -283,6 +284,10 @@ class Context:
         out = (ctypes.c_double * 4)()
         self._check(self.L.aao_last_phase_ms(self.h, out), "phase_ms")
         return list(out)
+
+    def set_timing(self, on=True):
+        """aao_set_timing: per-phase device timings (precond phases; GMRES ms_precond / ms_kkt / ms_orth)."""
+        self._check(self.L.aao_set_timing(self.h, 1 if on else 0), "set_timing")
 
     def profile_smoother(self, on=True):
         self._check(self.L.aao_profile_smoother(self.h, 1 if on else 0), "profile_smoother")

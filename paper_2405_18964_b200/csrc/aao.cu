@@ -1370,6 +1370,7 @@ void gmres_alloc(Ctx& c, int m) {
   }
   CK(cudaMallocHost(&c.hostH, sizeof(double) * (m + 2) * 2));
   for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c.gm_ev[i], cudaEventDisableTiming));
+  for (int i = 0; i < 4; ++i) CK(cudaEventCreate(&c.gt_ev[i]));
   c.gm_m = m;
 }
 
@@ -1425,8 +1426,11 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
       double* Vk = c.gV + (size_t)k * N;
       double* w = c.gV + (size_t)(k + 1) * N;
       double* zk = c.store_z ? c.gZ + (size_t)k * N : c.gz;
+      if (c.timing) CK(cudaEventRecord(c.gt_ev[0], s));
       precond_apply(c, Vk, zk, s);
+      if (c.timing) CK(cudaEventRecord(c.gt_ev[1], s));
       kkt_apply(c, zk, w, s);
+      if (c.timing) CK(cudaEventRecord(c.gt_ev[2], s));
       double* hcol = c.gH + (size_t)k * (m + 1);
       int w_scaled = 0;
       CK(launch_mgs(w, (const double* const*)c.gVptr, k, N, hcol, c.gpart, s, &w_scaled));
@@ -1435,15 +1439,26 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
         launch_scale_dev(w, w, hcol + k + 1, N, s);
         ++launch_counter();
       }
+      if (c.timing) CK(cudaEventRecord(c.gt_ev[3], s));
       CK(cudaMemcpyAsync(c.hostH + (k & 1) * (m + 2), hcol, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, s));
       CK(cudaEventRecord(c.gm_ev[k & 1], s));
     };
-    const bool speculate = !c.nonlinear;   // Algorithm 2 synchronises inside precond_apply
+    // Algorithm 2 synchronises inside precond_apply; phase timing reuses one event set per iteration
+    const bool speculate = !c.nonlinear && !c.timing;
     enqueue(0);
     for (int k = 0; k < m; ++k) {
       if (speculate && k + 1 < m && it + 1 < kry.max_iters) enqueue(k + 1);
       CK(cudaEventSynchronize(c.gm_ev[k & 1]));
       inf.precond_applies++;
+      if (c.timing) {
+        float t01 = 0.f, t12 = 0.f, t23 = 0.f;
+        cudaEventElapsedTime(&t01, c.gt_ev[0], c.gt_ev[1]);
+        cudaEventElapsedTime(&t12, c.gt_ev[1], c.gt_ev[2]);
+        cudaEventElapsedTime(&t23, c.gt_ev[2], c.gt_ev[3]);
+        inf.ms_precond += t01;
+        inf.ms_kkt += t12;
+        inf.ms_orth += t23;
+      }
       const double* hh = c.hostH + (k & 1) * (m + 2);
       for (int i = 0; i <= k + 1; ++i) H[(size_t)i * m + k] = hh[i];
       // Givens rotations (same arithmetic as oracle/gmres.py)
@@ -1647,6 +1662,8 @@ void aao_destroy(aao_ctx* ctx) {
   for (void* p : ctx->c.allocs) cudaFree(p);
   if (ctx->c.hostH) cudaFreeHost(ctx->c.hostH);
   for (auto e : ctx->c.gm_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : ctx->c.gt_ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->c.ev)
     if (e) cudaEventDestroy(e);

@@ -161,6 +161,7 @@ struct Ctx {
   double *stage_b = nullptr, *stage_x = nullptr;   // device staging of aao_gmres_solve_host
   double* hostH = nullptr;   // pinned, 2 x (m + 2): Hessenberg columns of iterations k, k+1
   cudaEvent_t gm_ev[2] = {nullptr, nullptr};
+  cudaEvent_t gt_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // GMRES phase timing (aao_set_timing)
   // bookkeeping
   std::vector<void*> allocs;
   size_t bytes = 0;

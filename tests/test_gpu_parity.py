@@ -345,3 +345,19 @@ def test_pack_unpack_masked_round_trip():
     u = ctx.unpack(p).cpu().numpy()
     ref = np.where(synth.full_mask(cfg), g, 0.0)
     assert np.array_equal(p.cpu().numpy(), ref) and np.array_equal(u, ref)
+
+
+def test_gmres_phase_timings():
+    """aao_info's per-phase device times (aao_set_timing): positive, bounded by the solve's wall time, and
+    the solve itself unchanged (same iterations, same history) with the events on."""
+    _torch()
+    cfg = synth.CONFIGS["c1"]
+    ctx = gpu_ctx(cfg)
+    b = ctx.build_rhs(synth.desired_state(cfg))
+    _, info0, hist0, _ = ctx.gmres_solve(b, tol=1e-6, restart=30)
+    ctx.set_timing(True)
+    _, info1, hist1, _ = ctx.gmres_solve(b, tol=1e-6, restart=30)
+    assert info1["iterations"] == info0["iterations"] and np.array_equal(hist0, hist1)
+    for k in ("ms_precond", "ms_kkt", "ms_orth"):
+        assert info1[k] > 0.0 and info0[k] == 0.0
+    assert info1["ms_precond"] + info1["ms_kkt"] + info1["ms_orth"] <= info1["ms_total"]
