@@ -913,7 +913,9 @@ int per_thread(int count, int ky) {
 // tile width for the symmetric kernels: fits shared memory and needs at most 8 outputs per thread
 int sym_tile(const Ctx& c, int count, size_t* sf, size_t* si) {
   int TD = tile_width(c.n_b, c.n_f, sf, si);
-  while (TD > 8 && (count + 256 / TD - 1) / (256 / TD) > 8) TD /= 2;
+  // at most 4 outputs per thread on tiles wider than 16 columns (c4_128: TD 32 -> 16, 8 -> 4 outputs per thread,
+  // DFT pair 4.53 -> 3.89 ms; profiles/r01_fft_td.log), else at most 8
+  while (TD > 8 && (count + 256 / TD - 1) / (256 / TD) > (TD > 16 ? 4 : 8)) TD /= 2;
   *sf = (size_t)c.n_b * 16 + 2ull * c.n_b * TD * 8;
   *si = (size_t)c.n_b * 16 + 2ull * c.n_f * TD * 16;
   return TD;
