@@ -76,6 +76,11 @@ typedef struct {
   double inner_eps;      /* inner relative tolerance (1e-2)                      */
   int inner_maxit;       /* inner iteration cap = inner Krylov basis size (reading: 60;
                             reduced at create if the basis does not fit in memory)     */
+  int freq_chunk;        /* frequencies per velocity-MG launch; the MG level workspace is sized for
+                            freq_chunk frequencies instead of all n_f.  0 = auto: all
+                            when the workspace fits in 2 GiB, else the largest multiple of a full
+                            148-problem wave that does.  Changes no arithmetic (independent
+                            per-frequency solves).  < 0: AAO_ERR_CONFIG                  */
 } aao_config;
 
 typedef enum { AAO_PRECOND_LINEAR = 0, AAO_PRECOND_NONLINEAR = 1 } aao_pmode;
@@ -88,6 +93,11 @@ typedef struct {
   double tol;            /* relative residual target on ||b|| (reading: 1e-6)            */
   int restart;           /* GMRES restart m (30), 1 <= m <= 64                     */
   int max_iters;         /* iteration cap                                                 */
+  int store_z;           /* linear mode: 0 = restart update x += P^{-1}(V y) (the oracle's form, one
+                            extra preconditioner application per cycle); 1 = keep the m vectors
+                            Z_k = P^{-1} v_k and update x += Z y (m more vectors of device memory,
+                            AAO_ERR_OOM if they do not fit -- never a silent switch).  FGMRES
+                            (nonlinear mode) always stores Z.  Other values: AAO_ERR_SHAPE      */
 } aao_krylov;
 
 typedef struct {
@@ -106,6 +116,7 @@ typedef struct {
   double ms_precond;     /* device time summed over the Arnoldi iterations: preconditioner,   */
   double ms_kkt;         /*   KKT matvec and Gram-Schmidt (+ normalisation); filled only after */
   double ms_orth;        /*   aao_set_timing(ctx, 1) (events; the speculative enqueue is off)  */
+  int store_z;           /* 1 if the restart update used the stored Z (x += Z y)               */
 } aao_info;
 
 /* Assemble operators and per-frequency data, allocate all device workspace (step A9).
@@ -119,6 +130,8 @@ void aao_destroy(aao_ctx* ctx);
 const char* aao_last_error(const aao_ctx* ctx);   /* never NULL; "" when no error */
 
 size_t aao_vector_len(const aao_ctx* ctx);         /* N = 2 n_b (n_v + n_p) */
+/* Workspace owned by the context, bytes.  aao_gmres_solve adds (m + 1) + 1 vectors of N doubles at the first
+   solve (+ m with stored Z or in nonlinear mode); aao_gmres_solve_host 2 more (device staging of b, x). */
 size_t aao_device_bytes(const aao_ctx* ctx);       /* workspace owned by the context */
 
 /* Paper order -> internal layout.  The internal (layout-T) vector IS the paper's ordering
@@ -159,7 +172,7 @@ aao_status aao_build_rhs_general(aao_ctx* ctx, const double* vd, const double* f
    Synchronises the stream once per step.  Errors: AAO_ERR_SHAPE, AAO_ERR_CONFIG, AAO_ERR_NUMERIC. */
 aao_status aao_arnoldi(aao_ctx* ctx, const double* v0, int m, double* H, int* m_done, void* stream);
 
-/* y = A x, eq. (FinalA) (step A2).  Device pointers, x != y. */
+/* y = A x, eq. (FinalA) (step A2).  Device pointers, x != y (else AAO_ERR_SHAPE). */
 aao_status aao_kkt_apply(aao_ctx* ctx, const double* x, double* y, void* stream);
 
 /* z = Pbar_C^{-1} r, Algorithm 1 (steps A3-A8).  Device pointers, r != z.
@@ -176,8 +189,9 @@ aao_status aao_precond_apply(aao_ctx* ctx, const double* r, double* z, void* str
 aao_status aao_gmres_solve(aao_ctx* ctx, const double* b, double* x, const aao_krylov* kry,
                            aao_info* info, double* hist, int hist_cap, void* stream);
 
-/* Same solve with HOST b and x (pinned or pageable): copies b (and x0) in and x out
-   inside the call; the end-to-end entry point. */
+/* Same solve with HOST b and x (pinned or pageable; each N doubles, caller-owned, b != x): copies b and x0
+   in and x out inside the call -- the end-to-end entry point.  On an error (negative status) x_host is not
+   written.  The binding checks the host buffers' dtype / length / contiguity before the call. */
 aao_status aao_gmres_solve_host(aao_ctx* ctx, const double* b_host, double* x_host,
                                 const aao_krylov* kry, aao_info* info, double* hist,
                                 int hist_cap, void* stream);
@@ -194,14 +208,17 @@ int aao_last_inner_iterations(const aao_ctx* ctx, int* out, int cap);
 
 /* Per-phase device timings of the last aao_precond_apply, milliseconds
    (fft_fwd, velocity block solves, pressure block solves, fft_inv); requires
-   aao_set_timing(ctx, 1) beforehand (adds events; off by default). */
+   aao_set_timing(ctx, 1) beforehand (adds events; off by default) and a LINEAR-mode apply since;
+   otherwise AAO_ERR_CONFIG with ms4 zeroed. */
 aao_status aao_set_timing(aao_ctx* ctx, int on);
 aao_status aao_last_phase_ms(aao_ctx* ctx, double* ms4);
 
 /* Live timing of the dominant kernel class -- the velocity multigrid: in the default CTA-resident
    mode the k_mg_cta solve launches, in the per-level mode (env AAO_MG_MODE=1) the finest-level
    multicolour SOR sweeps -- with CUDA events on the launching stream around each launch (run).
-   aao_profile_smoother(ctx, 1) resets and enables; aao_profile_read synchronises and returns
+   aao_profile_smoother(ctx, on) resets and enables (on = 1), disables (on = 0), or enables and pre-creates the
+   events for `on` > 1 launches (so that no event is created inside a timed region); aao_profile_read
+   synchronises and returns
    out3 = {milliseconds, algorithmic bytes, number of kernel launches} accumulated since, then
    resets.  Algorithmic bytes: a sweep reads x, b and writes x once per unknown (48 B, complex128);
    a whole MG solve adds residual (48), restriction (16 + 16/coarse unknown), prolongation (32 +

@@ -75,6 +75,12 @@ class OracleNonlinearPreconditioner(OraclePreconditioner):
         self.inner_eps, self.inner_maxit = inner_eps, inner_maxit
         self.last_inner = {}
 
+    def _block_extra(self, k):            # the inner iteration count travels back from a worker process
+        return self.last_inner.get(k)
+
+    def _block_extra_set(self, k, extra):
+        self.last_inner[k] = extra
+
     # ---- the block operators, written from their displays
     def Z_apply(self, k, X):
         """Z_j of P:392-397 on X = (x1, x2, x3, x4): rows [M, X, 0, B^T], [X, -M, B^T, 0], [0, B, 0, 0], [B, 0, 0, 0],

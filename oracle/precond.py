@@ -11,6 +11,8 @@ slot 2 = half-1 velocity, slot 3 = half-0 pressure, slot 4 = half-1 pressure.
 """
 from __future__ import annotations
 
+import multiprocessing as mp
+
 import numpy as np
 
 from . import timeops
@@ -19,8 +21,9 @@ from .inner import Chebyshev, Multigrid, wathen_bounds
 
 class OraclePreconditioner:
     def __init__(self, prob, mg_cycles=4, pre=2, post=2, omega=1.0, cheb_iters=10,
-                 uzawa_iters=6, uzawa_mu=0.75, cache_blocks=None):
+                 uzawa_iters=6, uzawa_mu=0.75, cache_blocks=None, workers=1):
         self.prob = prob
+        self.workers = workers        # processes over the independent frequency blocks; 1 = in-process
         self.dim = prob.dim
         self.n_b = prob.n_b
         self.d = timeops.spectrum(prob.n_b)
@@ -193,13 +196,35 @@ class OraclePreconditioner:
         y1, y2, y3, y4 = self.block(k, Vh[0, 0], Vh[0, 1], Ph[0, 0], Ph[0, 1])
         return np.stack([y1, y2]), np.stack([y3, y4])
 
+    def _blocks(self, Vh, Ph):
+        """Solve every frequency block k < n_b; with workers > 1 the independent blocks are spread over
+        forked processes -- the same block() calls, so the same arithmetic.  Yields (k, block result, extra)."""
+        if self.workers <= 1 or self.n_b == 1:
+            for k in range(self.n_b):
+                yield k, self.block(k, Vh[k, 0], Vh[k, 1], Ph[k, 0], Ph[k, 1]), self._block_extra(k)
+            return
+        global _WORKER_PC
+        _WORKER_PC = self
+        ctx = mp.get_context("fork")
+        with ctx.Pool(min(self.workers, self.n_b)) as pool:
+            args = [(k, (Vh[k, 0], Vh[k, 1], Ph[k, 0], Ph[k, 1])) for k in range(self.n_b)]
+            for k, res, extra in pool.imap_unordered(_worker_block, args):
+                self._block_extra_set(k, extra)
+                yield k, res, extra
+        _WORKER_PC = None
+
+    def _block_extra(self, k):
+        return None
+
+    def _block_extra_set(self, k, extra):
+        pass
+
     def apply(self, r, return_imag=False):
         """z = P-bar_C^{-1} r on paper-order full vectors (Algorithm 1)."""
         Vh, Ph = self.forward(r)
         Yh = np.zeros_like(Vh)
         Qh = np.zeros_like(Ph)
-        for k in range(self.n_b):
-            y1, y2, y3, y4 = self.block(k, Vh[k, 0], Vh[k, 1], Ph[k, 0], Ph[k, 1])
+        for k, (y1, y2, y3, y4), _ in self._blocks(Vh, Ph):
             Yh[k, 0], Yh[k, 1], Qh[k, 0], Qh[k, 1] = y1, y2, y3, y4
         Y = np.moveaxis(timeops.idft(Yh), 0, 1)
         Q = np.moveaxis(timeops.idft(Qh), 0, 1)
@@ -208,3 +233,13 @@ class OraclePreconditioner:
             zi = self.prob.from_reduced(Y.imag, Q.imag)
             return z, zi
         return z
+
+
+_WORKER_PC = None
+
+
+def _worker_block(arg):
+    """Child process of OraclePreconditioner._blocks (fork: the preconditioner object is inherited)."""
+    k, R = arg
+    res = _WORKER_PC.block(k, *R)
+    return k, res, _WORKER_PC._block_extra(k)

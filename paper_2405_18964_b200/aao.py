@@ -27,11 +27,13 @@ class Config(ctypes.Structure):
                 ("wind_q2", ctypes.POINTER(ctypes.c_double)), ("mg_cycles", ctypes.c_int),
                 ("pre_sweeps", ctypes.c_int), ("post_sweeps", ctypes.c_int), ("omega", ctypes.c_double),
                 ("cheb_iters", ctypes.c_int), ("uzawa_iters", ctypes.c_int), ("uzawa_mu", ctypes.c_double),
-                ("pmode", ctypes.c_int), ("inner_eps", ctypes.c_double), ("inner_maxit", ctypes.c_int)]
+                ("pmode", ctypes.c_int), ("inner_eps", ctypes.c_double), ("inner_maxit", ctypes.c_int),
+                ("freq_chunk", ctypes.c_int)]
 
 
 class Krylov(ctypes.Structure):
-    _fields_ = [("tol", ctypes.c_double), ("restart", ctypes.c_int), ("max_iters", ctypes.c_int)]
+    _fields_ = [("tol", ctypes.c_double), ("restart", ctypes.c_int), ("max_iters", ctypes.c_int),
+                ("store_z", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -39,7 +41,8 @@ class Info(ctypes.Structure):
                 ("breakdown", ctypes.c_int), ("final_relres", ctypes.c_double),
                 ("true_relres", ctypes.c_double), ("precond_applies", ctypes.c_int),
                 ("ms_total", ctypes.c_double), ("inner_its_total", ctypes.c_long), ("inner_its_max", ctypes.c_int),
-                ("ms_precond", ctypes.c_double), ("ms_kkt", ctypes.c_double), ("ms_orth", ctypes.c_double)]
+                ("ms_precond", ctypes.c_double), ("ms_kkt", ctypes.c_double), ("ms_orth", ctypes.c_double),
+                ("store_z", ctypes.c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -116,7 +119,7 @@ class Context:
 
     def __init__(self, dim, n_cells, x_lo, x_hi, n_t, T, beta, nu, problem="stokes", wind_q2=None,
                  mg_cycles=4, pre_sweeps=2, post_sweeps=2, omega=1.0, cheb_iters=10, uzawa_iters=6,
-                 uzawa_mu=0.75, nonlinear=False, inner_eps=1e-2, inner_maxit=60):
+                 uzawa_mu=0.75, nonlinear=False, inner_eps=1e-2, inner_maxit=60, freq_chunk=0):
         import torch
         if not torch.cuda.is_available():
             raise AAOError("no CUDA device: the aao hot path has no CPU fallback")
@@ -134,6 +137,7 @@ class Context:
         cfg.mg_cycles, cfg.pre_sweeps, cfg.post_sweeps, cfg.omega = mg_cycles, pre_sweeps, post_sweeps, omega
         cfg.cheb_iters, cfg.uzawa_iters, cfg.uzawa_mu = cheb_iters, uzawa_iters, uzawa_mu
         cfg.pmode, cfg.inner_eps, cfg.inner_maxit = (1 if nonlinear else 0), inner_eps, inner_maxit
+        cfg.freq_chunk = freq_chunk
         self.nonlinear = bool(nonlinear)
         h = ctypes.c_void_p()
         rc = L.aao_create(ctypes.byref(cfg), ctypes.byref(h))
@@ -240,9 +244,10 @@ class Context:
                                              self._stream(stream)), "precond_apply")
         return out
 
-    def gmres_solve(self, b, x=None, tol=1e-6, restart=30, max_iters=2000, hist_cap=4096, stream=None):
+    def gmres_solve(self, b, x=None, tol=1e-6, restart=30, max_iters=2000, hist_cap=4096, store_z=False,
+                    stream=None):
         x = self.torch.zeros_like(b) if x is None else x
-        kry = Krylov(tol, restart, max_iters)
+        kry = Krylov(tol, restart, max_iters, 1 if store_z else 0)
         info = Info()
         hist = (ctypes.c_double * hist_cap)()
         rc = self._check(self.L.aao_gmres_solve(self.h, _ptr(self._vec(b)), _ptr(self._vec(x)), ctypes.byref(kry),
@@ -250,25 +255,35 @@ class Context:
                          "gmres_solve")
         return x, info.as_dict(), list(hist[:min(info.iterations, hist_cap)]), rc
 
+    def _host_vec(self, a, what):
+        """A HOST buffer of N float64: a C-contiguous numpy array or a contiguous CPU torch tensor."""
+        torch = self.torch
+        if isinstance(a, np.ndarray):
+            ok = a.dtype == np.float64 and a.flags["C_CONTIGUOUS"] and a.size == self.N
+            if not ok:
+                raise AAOError(f"{what}: expected a C-contiguous float64 numpy array with {self.N} entries")
+            return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        if isinstance(a, torch.Tensor):
+            ok = (a.device.type == "cpu" and a.dtype == torch.float64 and a.is_contiguous() and a.numel() == self.N)
+            if not ok:
+                raise AAOError(f"{what}: expected a contiguous CPU float64 tensor with {self.N} entries")
+            return ctypes.cast(ctypes.c_void_p(a.data_ptr()), ctypes.POINTER(ctypes.c_double))
+        raise AAOError(f"{what}: expected a numpy array or a CPU torch tensor")
+
     def gmres_solve_host(self, b_host, x_host=None, tol=1e-6, restart=30, max_iters=2000, hist_cap=4096,
-                         stream=None):
-        """End-to-end entry: HOST numpy (or pinned torch CPU) b and x; copies are inside the call."""
-        if isinstance(b_host, np.ndarray):
-            b = np.ascontiguousarray(b_host, dtype=np.float64)
-            x = np.zeros_like(b) if x_host is None else x_host
-            bp = b.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-            xp = x.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-        else:
-            b = b_host
-            x = self.torch.zeros_like(b_host) if x_host is None else x_host
-            bp = ctypes.cast(ctypes.c_void_p(b.data_ptr()), ctypes.POINTER(ctypes.c_double))
-            xp = ctypes.cast(ctypes.c_void_p(x.data_ptr()), ctypes.POINTER(ctypes.c_double))
-        kry = Krylov(tol, restart, max_iters)
+                         store_z=False, stream=None):
+        """End-to-end entry: HOST b and x (numpy float64 or CPU torch float64, pinned or pageable, N entries each);
+        the copies are inside the call.  x_host (the initial guess, overwritten by the solution) defaults to zeros."""
+        if x_host is None:
+            x_host = np.zeros(self.N) if isinstance(b_host, np.ndarray) else self.torch.zeros_like(b_host)
+        bp = self._host_vec(b_host, "b_host")
+        xp = self._host_vec(x_host, "x_host")
+        kry = Krylov(tol, restart, max_iters, 1 if store_z else 0)
         info = Info()
         hist = (ctypes.c_double * hist_cap)()
         rc = self._check(self.L.aao_gmres_solve_host(self.h, bp, xp, ctypes.byref(kry), ctypes.byref(info), hist,
                                                      hist_cap, self._stream(stream)), "gmres_solve_host")
-        return x, info.as_dict(), list(hist[:min(info.iterations, hist_cap)]), rc
+        return x_host, info.as_dict(), list(hist[:min(info.iterations, hist_cap)]), rc
 
     def debug_freq_block(self, k, stream=None):
         """y_hat_k of the last precond_apply: complex array (2, n_v + n_p)."""
@@ -276,9 +291,6 @@ class Context:
         self._check(self.L.aao_debug_freq_block(self.h, k, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                                 self._stream(stream)), "debug_freq_block")
         return (out[0::2] + 1j * out[1::2]).reshape(2, self.n_block)
-
-    def set_timing(self, on=True):
-        self._check(self.L.aao_set_timing(self.h, 1 if on else 0), "set_timing")
 
     def phase_ms(self):
         out = (ctypes.c_double * 4)()
@@ -289,8 +301,10 @@ class Context:
         """aao_set_timing: per-phase device timings (precond phases; GMRES ms_precond / ms_kkt / ms_orth)."""
         self._check(self.L.aao_set_timing(self.h, 1 if on else 0), "set_timing")
 
-    def profile_smoother(self, on=True):
-        self._check(self.L.aao_profile_smoother(self.h, 1 if on else 0), "profile_smoother")
+    def profile_smoother(self, on=True, reserve=0):
+        """Live timing of the velocity-MG launches; `reserve` pre-creates events for that many launches."""
+        self._check(self.L.aao_profile_smoother(self.h, (max(2, int(reserve)) if reserve else 1) if on else 0),
+                    "profile_smoother")
 
     def profile_read(self):
         """(ms, algorithmic bytes, launches) of the finest-level SOR sweeps since profile_smoother(True)."""

@@ -671,32 +671,30 @@ void setup(Ctx& c, const aao_config& cfg) {
   c.Cr = dalloc<double2>(c, cheb_len);
   c.Cd0 = dalloc<double2>(c, cheb_len);
   c.Cd1 = dalloc<double2>(c, cheb_len);
+  // MG level workspaces.  The velocity solves run in chunks of c.freq_chunk frequencies (aao_config.freq_chunk;
+  // 0 = auto: all frequencies when the workspace fits in 2 GiB, else the largest multiple of a full wave of
+  // 148 problems that does), so the per-level workspace is bounded independently of n_t.
+  {
+    const int ppf = nprob_v / n_f;   // velocity problems per frequency
+    double per_prob = 0;
+    for (int l = 0; l < nlev; ++l) per_prob += (l == 0 ? 1.0 : 3.0) * c.vel.grids[l].n * sizeof(double2);
+    const double per_freq = per_prob * ppf;
+    int F = cfg.freq_chunk > 0 ? std::min(cfg.freq_chunk, n_f) : n_f;
+    if (cfg.freq_chunk <= 0 && per_freq * n_f > 2.0 * (1 << 30)) {
+      F = std::max(1, (int)(2.0 * (1 << 30) / per_freq));
+      int q = 1;                       // frequencies per full wave of 148 problems (when it divides)
+      while ((q * ppf) % 148 != 0 && q < 148) ++q;
+      if (F >= q) F = F / q * q;
+    }
+    c.freq_chunk = F;
+  }
   for (int sp = 0; sp < 2; ++sp) {
     MGSpace& S = sp == 0 ? c.vel : c.pres;
-    const int np = sp == 0 ? nprob_v : nprob_p;
+    const int np = sp == 0 ? c.freq_chunk * (nprob_v / n_f) : nprob_p;
     S.nprob_max = np;
     S.x.assign(nlev, nullptr);
     S.b.assign(nlev, nullptr);
     S.r.assign(nlev, nullptr);
-    if (S.order == 2) {
-      S.px.assign(nlev, nullptr);
-      S.pb.assign(nlev, nullptr);
-      S.pr.assign(nlev, nullptr);
-      S.pstride.assign(nlev, 0);
-      for (int l = 0; l < nlev; ++l) {
-        const long st = S.grids[l].n + S.grids[l].n1 + 8;   // padding: the last tap of the last row
-        S.pstride[l] = st;
-        const long n = st * (long)np + 8;
-        S.px[l] = dalloc<double2>(c, n);
-        S.pr[l] = dalloc<double2>(c, n);
-        CK(cudaMemset(S.px[l], 0, n * sizeof(double2)));
-        CK(cudaMemset(S.pr[l], 0, n * sizeof(double2)));
-        if (l > 0) {
-          S.pb[l] = dalloc<double2>(c, n);
-          CK(cudaMemset(S.pb[l], 0, n * sizeof(double2)));
-        }
-      }
-    }
     for (int l = 0; l < nlev; ++l) {
       const long n = S.grids[l].n * (long)np;
       S.r[l] = dalloc<double2>(c, n);
@@ -780,10 +778,6 @@ long unknowns(const Grid& g) {
   return g.order == 1 ? u - 1 : u;
 }
 
-// algorithmic bytes of `sweeps` multicolour SOR sweeps on one level: x, b read and x written once per
-// unknown (complex128)
-double sweep_bytes(const Grid& g, int nprob, int sweeps) { return 48.0 * unknowns(g) * nprob * sweeps; }
-
 // algorithmic bytes of one MG solve (all cycles): per level and V-cycle, sweeps 48 B/unknown each,
 // residual 48, restriction 16 (+16 per coarse unknown), prolongation + correction 32 (+16 per coarse
 // unknown), coarsest solve 32 (~1579 B per fine unknown in 2-D)
@@ -797,32 +791,23 @@ double mg_bytes(const Ctx& c, const MGSpace& S, int nprob) {
   return b * c.cfg.mg_cycles * nprob;
 }
 
-void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double2* inv, int inv_pg, View x, View b,
-                       int nprob, int cycles, cudaStream_t s);
-
+// one V-cycle on levels >= l, one launch per level / colour (AAO_MG_MODE=1; the parity-tested reference
+// schedule of the CTA-resident solve)
 void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, int inv_pg, View x, View b, int nprob,
                cudaStream_t s) {
   const Grid& g = S.grids[l];
   auto& cnt = launch_counter();
-  if (c.tail > 0 && l == c.tail) {   // one V-cycle from zero on levels >= l, CTA-resident
-    launch_cta_levels(c, S, l, op, inv, inv_pg, x, b, nprob, 1, s);
-    return;
-  }
   if (l == S.nlev - 1) {
     launch_coarse(g, inv, inv_pg, S.coarse_unk, S.ncoarse_unk, b, x, nprob, s);
     ++cnt;
     return;
   }
   const int C = S.order == 2 ? (c.dim == 2 ? 9 : 27) : (c.dim == 2 ? 4 : 8);
-  {
-    SweepTimer tm(c, false && l == 0 && S.order == 2, s, sweep_bytes(g, nprob, c.cfg.pre_sweeps),
-                  (long)C * c.cfg.pre_sweeps);
-    for (int sw = 0; sw < c.cfg.pre_sweeps; ++sw)
-      for (int col = 0; col < C; ++col) {
-        launch_gs(g, op, x, b, nprob, col, c.cfg.omega, s);
-        ++cnt;
-      }
-  }
+  for (int sw = 0; sw < c.cfg.pre_sweeps; ++sw)
+    for (int col = 0; col < C; ++col) {
+      launch_gs(g, op, x, b, nprob, col, c.cfg.omega, s);
+      ++cnt;
+    }
   View r = contig(S.r[l], g.n);
   launch_residual(g, op, x, b, r, nprob, s);
   const Grid& gc = S.grids[l + 1];
@@ -833,8 +818,6 @@ void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, i
   mg_vcycle(c, S, l + 1, op, inv, inv_pg, xc, bc, nprob, s);
   launch_prolong(g, gc, S.transfers[l], xc, x, nprob, s);
   ++cnt;
-  SweepTimer tm(c, false && l == 0 && S.order == 2, s, sweep_bytes(g, nprob, c.cfg.post_sweeps),
-                (long)C * c.cfg.post_sweeps);
   for (int sw = 0; sw < c.cfg.post_sweeps; ++sw)
     for (int col = C - 1; col >= 0; --col) {
       launch_gs(g, op, x, b, nprob, col, c.cfg.omega, s);
@@ -842,22 +825,22 @@ void mg_vcycle(Ctx& c, MGSpace& S, int l, const OpSel& op, const double2* inv, i
     }
 }
 
-// CTA-resident solve over levels [l0, nlev): `cycles` V-cycles from x = 0 at level l0.
-void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double2* inv, int inv_pg, View x, View b,
-                       int nprob, int cycles, cudaStream_t s) {
+// CTA-resident solve: `cycles` V-cycles from x = 0, one CTA per problem, all levels in one launch.
+void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, int inv_pg, View x, View b, int nprob,
+                       int cycles, cudaStream_t s) {
   MGArgs a;
   std::memset(&a, 0, sizeof(a));
-  a.nlev = S.nlev - l0;
+  a.nlev = S.nlev;
   a.cycles = cycles;
   a.pre = c.cfg.pre_sweeps;
   a.post = c.cfg.post_sweeps;
   a.omega = c.cfg.omega;
   for (int i = 0; i < a.nlev; ++i) {
-    a.g[i] = S.grids[l0 + i];
-    a.t[i] = S.transfers[l0 + i];
-    a.xw[i] = S.x[l0 + i];
-    a.bw[i] = S.b[l0 + i];
-    a.rw[i] = S.r[l0 + i];
+    a.g[i] = S.grids[i];
+    a.t[i] = S.transfers[i];
+    a.xw[i] = S.x[i];
+    a.bw[i] = S.b[i];
+    a.rw[i] = S.r[i];
   }
   a.x0 = x;
   a.b0 = b;
@@ -866,7 +849,8 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   a.inv_pg = inv_pg;
   a.unk = S.coarse_unk;
   a.nu = S.ncoarse_unk;
-  // class stencil tables (Q2, real operators, smoothing levels need n1 >= 9): first in dynamic smem
+  // class stencil tables (Q2, smoothing levels need n1 >= 9): first in dynamic smem.  AAO_NO_CTAB=1 evaluates
+  // every stencil from the 1-D rows instead (same map, parity-tested; used to measure summation-order drift)
   static const bool no_ctab = std::getenv("AAO_NO_CTAB") != nullptr;
   size_t tab_bytes = 0;
   a.use_ctab = 0;
@@ -877,44 +861,24 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
     tab_bytes = (a.nlev - 1) * per * sizeof(double);
     tab_bytes = (tab_bytes + 15) / 16 * 16;
   }
-  // residue-blocked layout (k_mg_q2p): parity-tested but measured slower (c2 2.62 vs 2.41 ms) -> opt-in
-  static const bool want_perm = std::getenv("AAO_PERM") != nullptr;
-  a.perm = (want_perm && a.use_ctab && S.order == 2 && !S.px.empty()) ? 1 : 0;
-  if (a.perm) {
-    for (int i = 0; i < a.nlev; ++i) {
-      a.xw[i] = S.px[l0 + i];
-      a.bw[i] = S.pb[l0 + i];
-      a.rw[i] = S.pr[l0 + i];
-      a.pstride[i] = S.pstride[l0 + i];
-    }
-  }
-  // shared-memory residency: coarsest levels first while x and b fit in the budget
-  static const char* bud = std::getenv("AAO_SMEM_BUDGET");
-  // measured (tools/smem_sweep.sh): keeping only the smallest levels in shared memory leaves the L1
-  // to the finest level, which matters more (c2 3.02 vs 3.17 ms, c3 277 vs 437 ms)
-  // 2-D Q2 real operators with the merged small-level visits: no level in shared memory (c2 2.216 -> 2.175 ms:
-  // the L1 cache serves every level better than a split); elsewhere the smallest levels within 20 KB
-  static const char* fc_env = std::getenv("AAO_FLAT_CONV");   // Oseen small levels flat (default on)
-  const bool flat_conv = fc_env ? std::atoi(fc_env) != 0 : true;
-  const bool flat2d_sm = c.dim == 2 && S.order == 2 && a.use_ctab && (op.conv_sel == 0 || flat_conv);
-  const size_t budget = bud ? (size_t)std::atol(bud) : (flat2d_sm ? 0 : 20 * 1024);
+  // shared-memory residency of the coarse levels (coarsest first while x and b fit).  Measured: 2-D Q2 with the
+  // merged small-level visits keeps no level in shared memory (the L1 cache serves every level better than a
+  // split: c2 2.216 -> 2.175 ms); elsewhere the smallest levels within 20 KB (c2 3.02 vs 3.17 ms, c3 277 vs 437 ms)
+  const bool flat2d = c.dim == 2 && S.order == 2 && a.use_ctab;
+  const size_t budget = flat2d ? 0 : 20 * 1024;
   size_t used = tab_bytes;
   a.lsm = a.nlev;
   for (int l = a.nlev - 1; l >= 1; --l) {
-    const long len = a.perm ? a.pstride[l] : a.g[l].n;
-    const size_t need = 2 * len * sizeof(double2);
+    const size_t need = 2 * a.g[l].n * sizeof(double2);
     if (used + need > budget + tab_bytes) break;
     a.sm_x[l] = (long)(used / sizeof(double2));
-    a.sm_b[l] = (long)(used / sizeof(double2)) + len;
+    a.sm_b[l] = (long)(used / sizeof(double2)) + a.g[l].n;
     used += need;
     a.lsm = l;
   }
-  // the bottom levels (few unknowns) run warp-synchronously: their phases are pure latency
-  static const char* wl = std::getenv("AAO_WARP_UNKNOWNS");
-  // 2-D Q2 real operators use the merged branch-free colour visits on the small levels (flat_max), which
-  // run faster block-wide than in one warp (c2 precond 2.25 -> 2.22 ms); elsewhere levels <= 256 unknowns
-  const bool flat2d = c.dim == 2 && S.order == 2 && a.use_ctab && (op.conv_sel == 0 || flat_conv);
-  const long wmax = wl ? std::atol(wl) : (flat2d ? 0 : 256);
+  // the bottom levels (<= 256 unknowns) run warp-synchronously -- their phases are pure latency -- except for
+  // the 2-D Q2 merged branch-free visits, which run faster block-wide (c2 precond 2.25 -> 2.22 ms)
+  const long wmax = flat2d ? 0 : 256;
   a.lwarp = a.nlev;
   for (int l = 1; l < a.nlev; ++l)
     if (unknowns(a.g[l]) <= wmax) {
@@ -923,32 +887,25 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
     }
   // band-wavefront sweeps (2-D Q2 real operators) on the levels with n1 >= wave_min (default 257): the
   // iterate crosses HBM once per sweep instead of once per colour -- measured c4_64 precond 43.6 -> 35.2 ms,
-  // c4_128 87.8 -> 73.5 ms; slower where the level is L2-resident (c2, n1 = 129: 2.37 -> 2.73 ms).
-  // AAO_WAVE=0/1 forces it off/on for every eligible level >= AAO_WAVE_MIN; AAO_WAVE_H: band height.
+  // c4_128 87.8 -> 73.5 ms; slower where the level is L2-resident (c2, n1 = 129: 2.37 -> 2.73 ms) and with the
+  // stored per-node convection stencils (c3 255 -> 330 ms).  AAO_WAVE=0/1 forces it off/on for every eligible
+  // level >= AAO_WAVE_MIN (parity-tested).
   a.wave_h = 0;
-  const int wave_min = c.wave_min;   // per context (AAO_WAVE_MIN at aao_create)
-  const bool wave_on = c.wave_force >= 0 ? c.wave_force != 0 : a.g[0].n1 >= wave_min;
-  // Oseen Q_k / Q_k^H operators: opt-in (AAO_WAVE_CONV=1; c3 precond 255 -> 330 ms: the per-node convection
-  // stencils, re-read from L2 in every band step, outweigh the saved iterate traffic)
-  static const char* wc_env = std::getenv("AAO_WAVE_CONV");
-  const bool wave_conv = wc_env ? std::atoi(wc_env) != 0 : false;
-  if (wave_on && c.dim == 2 && S.order == 2 && a.use_ctab && (op.conv_sel == 0 || wave_conv) && !a.perm &&
-      c.mg_mode != 1) {
+  const bool wave_on = c.wave_force >= 0 ? c.wave_force != 0 : a.g[0].n1 >= c.wave_min;
+  const bool wave_conv = c.wave_force == 1;
+  if (wave_on && c.dim == 2 && S.order == 2 && a.use_ctab && (op.conv_sel == 0 || wave_conv)) {
     const int n1 = a.g[0].n1;
-    static const char* wh_env = std::getenv("AAO_WAVE_H");
-    const int h = wh_env ? std::atoi(wh_env) : (n1 <= 129 ? 6 : 3);
+    const int h = n1 <= 129 ? 6 : 3;
     const size_t ring = (size_t)8 * h * n1 * sizeof(double2);
     if (used + ring <= 220 * 1024) {
       a.wave_h = h;
-      a.wave_min = wave_min;
+      a.wave_min = c.wave_min;
       used = (used + 15) / 16 * 16;
       a.ring_off = (long)(used / sizeof(double2));
       used += ring;
     }
   }
-  static const char* flat_env = std::getenv("AAO_FLAT_MAX");
-  a.flat_max = flat_env ? std::atoi(flat_env) : 33;   // measured: 33 best (c2 precond 2.371 -> 2.249 ms)
-  if (op.conv_sel != 0 && !flat_conv) a.flat_max = 0;
+  a.flat_max = 33;   // measured: 33 best (c2 precond 2.371 -> 2.249 ms)
   // profiling only: per-level SM-cycle accounting of CTA 0, printed per launch (AAO_MG_CLOCK=1)
   static const bool mg_clock = std::getenv("AAO_MG_CLOCK") != nullptr;
   static unsigned long long* clk_dev = nullptr;
@@ -970,93 +927,32 @@ void launch_cta_levels(Ctx& c, MGSpace& S, int l0, const OpSel& op, const double
   }
 }
 
-// schedule: 0 = whole solve CTA-resident, 1 = one launch per level / colour, 2 = hybrid (launches on the
-// levels whose x and b do not fit in shared memory, CTA-resident tail below); -1 = automatic
-int tail_level(const Ctx& c, const MGSpace& S, int mode) {
-  if (mode == 1) return -1;
-  if (mode == 0) return 0;
-  for (int l = 1; l < S.nlev; ++l)
-    if (2 * S.grids[l].n * sizeof(double2) <= 200 * 1024) return l;
-  return S.nlev - 1;
+// problems [p0, p0 + ...) of a batch view (p0 a multiple of the view's group size)
+inline View sub_view(View v, long n, int p0) {
+  return View{v.p + (long)(p0 / v.per_group) * v.gstride + (long)(p0 % v.per_group) * n, v.per_group, v.gstride};
 }
 
-int choose_mode(const Ctx& c, const MGSpace& S) {
-  if (c.mg_mode >= 0) return c.mg_mode;
-  // measured (tools/modes_bench.sh): the CTA-resident schedule is fastest or on par for every config
-  // (c2 3.0 ms vs 4.1 hybrid; c3 277 vs 286; c4_64 60 vs 57-70; c5 254 vs 296)
-  (void)S;
-  return 0;
-}
-
-// real-split CTA-resident solve for real operators; returns false if it does not apply
-bool launch_real_split(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, int inv_pg, View x, View b,
-                       int nprob, cudaStream_t s, bool force) {
-  if (op.conv_sel != 0) return false;
-  MGRealArgs a;
-  std::memset(&a, 0, sizeof(a));
-  a.nlev = S.nlev;
-  a.cycles = c.cfg.mg_cycles;
-  a.pre = c.cfg.pre_sweeps;
-  a.post = c.cfg.post_sweeps;
-  a.omega = c.cfg.omega;
-  const size_t budget = 232448 - 2048;
-  size_t used = 0;
-  for (int l = 0; l < S.nlev; ++l) {
-    a.g[l] = S.grids[l];
-    a.t[l] = S.transfers[l];
-    a.xw[l] = l == 0 ? reinterpret_cast<double*>(S.r[0]) + (long)S.grids[0].n * nprob
-                     : reinterpret_cast<double*>(S.x[l]);
-    a.bw[l] = reinterpret_cast<double*>(S.b[l]);
-    a.rw[l] = reinterpret_cast<double*>(S.r[l]);
-    a.xsm[l] = a.bsm[l] = -1;
-  }
-  // finest iterate first, then coarse x, b from the coarsest level up
-  const size_t n0 = S.grids[0].n * sizeof(double);
-  if (n0 <= budget) {
-    a.xsm[0] = 0;
-    used = n0;
-  } else if (!force) {
-    return false;
-  }
-  for (int l = S.nlev - 1; l >= 1; --l) {
-    const size_t need = 2 * S.grids[l].n * sizeof(double);
-    if (used + need > budget) break;
-    a.xsm[l] = (long)(used / sizeof(double));
-    a.bsm[l] = a.xsm[l] + S.grids[l].n;
-    used += need;
-  }
-  a.x0 = x;
-  a.b0 = b;
-  a.op = op;
-  a.inv = inv;
-  a.inv_pg = inv_pg;
-  a.unk = S.coarse_unk;
-  a.nu = S.ncoarse_unk;
-  launch_mg_real(a, nprob, used, s);
-  ++launch_counter();
-  return true;
-}
-
-// x = MG(A; b): mg_cycles V-cycles from x = 0
+// x = MG(A; b): mg_cycles V-cycles from x = 0, in chunks of at most S.nprob_max problems
+// (the workspace size; frequency-aligned chunks, so coefficient groups and coarse inverses shift with them)
 void mg_solve(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, int inv_pg, View x, View b, int nprob,
               cudaStream_t s) {
-  const bool fits = S.grids[0].n * sizeof(double) <= 232448 - 2048;
-  if (op.conv_sel == 0 && (c.mg_mode == 3 || (c.mg_mode < 0 && fits && c.real_split_auto))) {
-    SweepTimer tm(c, S.order == 2, s, mg_bytes(c, S, nprob), 1);
-    launch_real_split(c, S, op, inv, inv_pg, x, b, nprob, s, true);
-    return;
+  const long n = S.grids[0].n;
+  for (int p0 = 0; p0 < nprob; p0 += S.nprob_max) {
+    const int np = std::min(S.nprob_max, nprob - p0);
+    OpSel opc = op;
+    if (op.per_group < (1 << 30)) opc.coef = op.coef + p0 / op.per_group;
+    const double2* invc = inv_pg < (1 << 30) ? inv + (long)(p0 / inv_pg) * S.ncoarse_unk * S.ncoarse_unk : inv;
+    const View xc = sub_view(x, n, p0), bc = sub_view(b, n, p0);
+    if (c.mg_mode == 0) {
+      SweepTimer tm(c, S.order == 2, s, mg_bytes(c, S, np), 1);
+      launch_cta_levels(c, S, opc, invc, inv_pg, xc, bc, np, c.cfg.mg_cycles, s);
+    } else {
+      SweepTimer tm(c, S.order == 2, s, mg_bytes(c, S, np), 0);
+      launch_zero(xc, n, np, s);
+      ++launch_counter();
+      for (int cyc = 0; cyc < c.cfg.mg_cycles; ++cyc) mg_vcycle(c, S, 0, opc, invc, inv_pg, xc, bc, np, s);
+    }
   }
-  const int mode = choose_mode(c, S);
-  if (mode == 0) {
-    SweepTimer tm(c, S.order == 2, s, mg_bytes(c, S, nprob), 1);
-    launch_cta_levels(c, S, 0, op, inv, inv_pg, x, b, nprob, c.cfg.mg_cycles, s);
-    return;
-  }
-  c.tail = tail_level(c, S, mode);
-  SweepTimer tm(c, S.order == 2, s, mg_bytes(c, S, nprob), 0);
-  launch_zero(x, S.grids[0].n, nprob, s);
-  ++launch_counter();
-  for (int cyc = 0; cyc < c.cfg.mg_cycles; ++cyc) mg_vcycle(c, S, 0, op, inv, inv_pg, x, b, nprob, s);
 }
 
 // x = scale * Chebyshev(M; b), Jacobi-preconditioned, Wathen bounds
@@ -1092,8 +988,7 @@ void stokes_blocks(Ctx& c, FVec in, double2* outV, double2* outPA, double2* outP
   OpSel opW{c.coefW, 2 * dim, 0};
   // pressure slots on the side stream (independent of the velocity slots): K_p^{-1} by MG and
   // M_p^{-1} by Chebyshev, combined later
-  static const bool one_stream = std::getenv("AAO_ONE_STREAM") != nullptr;
-  cudaStream_t sp = one_stream ? s : c.s2;
+  cudaStream_t sp = c.s2;
   cudaEventRecord(c.ev_fork, s);
   cudaStreamWaitEvent(sp, c.ev_fork, 0);
   OpSel opKp{c.coefKp, 1 << 30, 0};
@@ -1311,7 +1206,9 @@ void nl_precond_apply(Ctx& c, const double* r, double* z, cudaStream_t s) {
   CK(cudaStreamSynchronize(s));   // host vectors H, g, Y go out of scope
 }
 
+// r == z is allowed internally: r is read only by the forward transform, z written only by the inverse
 void precond_apply(Ctx& c, const double* r, double* z, cudaStream_t s) {
+  c.phase_valid = false;
   if (c.nonlinear) {
     nl_precond_apply(c, r, z, s);
     return;
@@ -1328,7 +1225,10 @@ void precond_apply(Ctx& c, const double* r, double* z, cudaStream_t s) {
   if (c.timing) cudaEventRecord(c.ev[3], s);
   launch_fft_inv(c, z, s);
   ++launch_counter();
-  if (c.timing) cudaEventRecord(c.ev[4], s);
+  if (c.timing) {
+    cudaEventRecord(c.ev[4], s);
+    c.phase_valid = true;
+  }
 }
 
 void kkt_apply(Ctx& c, const double* x, double* y, cudaStream_t s) {
@@ -1337,41 +1237,39 @@ void kkt_apply(Ctx& c, const double* x, double* y, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ GMRES
+// Workspace: the basis V_0..V_m and ONE work vector z (the Arnoldi z_k = P^{-1} v_k, and at a restart the update
+// u = V y and P^{-1} u in place); the residual b - A x is formed directly in V_0.  With the caller's b and x that is
+// m + 4 vectors of N doubles (c4 at n_t = 512: 34 x 4.84 GB), plus m more when the preconditioned vectors are kept.
 void gmres_alloc(Ctx& c, int m) {
   if (c.gm_m >= m) return;
   if (c.gm_m > 0) throw CudaError(AAO_ERR_CONFIG, "GMRES restart larger than the first solve's is not supported");
   const long N = c.N;
   c.gV = dalloc<double>(c, (size_t)(m + 1) * N);
   c.gz = dalloc<double>(c, N);
-  c.gu = dalloc<double>(c, N);
-  c.gr = dalloc<double>(c, N);
   c.gH = dalloc<double>(c, (size_t)(m + 2) * (m + 1));
   c.gpart = dalloc<double>(c, std::max((long)dot_blocks(), (long)(m + 3) * mgs_blocks()));
   c.gscal = dalloc<double>(c, 4 * (m + 2));
   std::vector<double*> ptr(m + 1);
   for (int i = 0; i <= m; ++i) ptr[i] = c.gV + (size_t)i * N;
   c.gVptr = upload(c, ptr);
-  // FGMRES stores the preconditioned vectors Z_k = P_k^{-1} v_k; the linear mode keeps them too when the
-  // extra m vectors fit (then the restart update x += Z y needs no extra preconditioner application:
-  // Algorithm 1 is a fixed linear map, so Z y = P^{-1}(V y) up to rounding).  AAO_STORE_Z=0 (read at
-  // aao_create) disables it: summing the z_k is less accurate when P^{-1} is ill-conditioned, which limits
-  // the attainable residual of very tight solves (the nu = 1 manufactured problem stalls above 1e-9).
-  {
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const size_t need = (size_t)m * N * sizeof(double);
-    c.store_z = c.nonlinear || (c.store_z_opt && need < free_b / 2);
-  }
-  if (c.store_z) {
-    c.gZ = dalloc<double>(c, (size_t)m * N);
-    std::vector<double*> zp(m);
-    for (int i = 0; i < m; ++i) zp[i] = c.gZ + (size_t)i * N;
-    c.gZptr = upload(c, zp);
-  }
   CK(cudaMallocHost(&c.hostH, sizeof(double) * (m + 2) * 2));
   for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&c.gm_ev[i], cudaEventDisableTiming));
   for (int i = 0; i < 4; ++i) CK(cudaEventCreate(&c.gt_ev[i]));
   c.gm_m = m;
+}
+
+// The m preconditioned vectors Z_k = P^{-1} v_k: always for FGMRES; for the linear mode only when the
+// caller asks (aao_krylov.store_z): the restart update x += Z y then needs no extra preconditioner application
+// (Algorithm 1 is a fixed linear map, so Z y = P^{-1}(V y) up to rounding).  A deterministic choice: an
+// allocation failure is AAO_ERR_OOM, never a silent switch to the other update.
+void gmres_alloc_z(Ctx& c, int m) {
+  if (c.gZ_m >= m) return;
+  if (c.gZ_m > 0) throw CudaError(AAO_ERR_CONFIG, "stored-Z restart larger than the first solve's is not supported");
+  c.gZ = dalloc<double>(c, (size_t)m * c.N);
+  std::vector<double*> zp(m);
+  for (int i = 0; i < m; ++i) zp[i] = c.gZ + (size_t)i * c.N;
+  c.gZptr = upload(c, zp);
+  c.gZ_m = m;
 }
 
 double dot_host(Ctx& c, const double* x, const double* y, int mode, cudaStream_t s) {
@@ -1386,10 +1284,13 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
                  cudaStream_t s) {
   const int m = kry.restart;
   gmres_alloc(c, m);
+  c.store_z = c.nonlinear || kry.store_z != 0;
+  if (c.store_z) gmres_alloc_z(c, m);
   const long N = c.N;
   auto t0 = std::chrono::steady_clock::now();
   aao_info inf;
   std::memset(&inf, 0, sizeof(inf));
+  inf.store_z = c.store_z ? 1 : 0;
   const long inner0 = c.inner_total;
   c.inner_max = 0;
   const double bnorm = dot_host(c, b, b, 1, s);
@@ -1401,17 +1302,17 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
     if (info) *info = inf;
     return AAO_OK;
   }
-  // r = b - A x0
-  kkt_apply(c, x, c.gz, s);
-  launch_copy_sub(c.gr, b, c.gz, N, s);
+  double* V0 = c.gV;
+  // r = b - A x0, formed in V_0
+  kkt_apply(c, x, V0, s);
+  launch_copy_sub(V0, b, V0, N, s);
   ++launch_counter();
   int it = 0;
   std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
   bool stop = false;
   for (;;) {
-    const double beta0 = dot_host(c, c.gr, c.gr, 1, s);
-    double* V0 = c.gV;
-    launch_scale_dev(V0, c.gr, c.gscal, N, s);
+    const double beta0 = dot_host(c, V0, V0, 1, s);
+    launch_scale_dev(V0, V0, c.gscal, N, s);
     ++launch_counter();
     std::fill(H.begin(), H.end(), 0.0);
     std::fill(g.begin(), g.end(), 0.0);
@@ -1452,9 +1353,9 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
       inf.precond_applies++;
       if (c.timing) {
         float t01 = 0.f, t12 = 0.f, t23 = 0.f;
-        cudaEventElapsedTime(&t01, c.gt_ev[0], c.gt_ev[1]);
-        cudaEventElapsedTime(&t12, c.gt_ev[1], c.gt_ev[2]);
-        cudaEventElapsedTime(&t23, c.gt_ev[2], c.gt_ev[3]);
+        CK(cudaEventElapsedTime(&t01, c.gt_ev[0], c.gt_ev[1]));
+        CK(cudaEventElapsedTime(&t12, c.gt_ev[1], c.gt_ev[2]));
+        CK(cudaEventElapsedTime(&t23, c.gt_ev[2], c.gt_ev[3]));
         inf.ms_precond += t01;
         inf.ms_kkt += t12;
         inf.ms_orth += t23;
@@ -1507,17 +1408,17 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
     if (c.store_z) {     // FGMRES, or linear with stored Z: x += Z_k y
       launch_multi_axpy(c.gz, (const double* const*)c.gZptr, c.gscal + 8, kdone, N, s);
       ++launch_counter();
-    } else {             // GMRES: x += P^{-1}(V_k y)
-      launch_multi_axpy(c.gu, (const double* const*)c.gVptr, c.gscal + 8, kdone, N, s);
+    } else {             // GMRES: x += P^{-1}(V_k y)  (u = V y and P^{-1} u in place, in z)
+      launch_multi_axpy(c.gz, (const double* const*)c.gVptr, c.gscal + 8, kdone, N, s);
       ++launch_counter();
-      precond_apply(c, c.gu, c.gz, s);
+      precond_apply(c, c.gz, c.gz, s);
       inf.precond_applies++;
     }
     launch_axpy(x, c.gz, 1.0, N, s);
-    kkt_apply(c, x, c.gz, s);
-    launch_copy_sub(c.gr, b, c.gz, N, s);
+    kkt_apply(c, x, V0, s);
+    launch_copy_sub(V0, b, V0, N, s);
     launch_counter() += 2;
-    inf.true_relres = dot_host(c, c.gr, c.gr, 1, s) / bnorm;
+    inf.true_relres = dot_host(c, V0, V0, 1, s) / bnorm;
     if (stop) break;
     inf.restarts++;
   }
@@ -1617,6 +1518,7 @@ void aao_config_defaults(aao_config* cfg) {
   cfg->pmode = AAO_PRECOND_LINEAR;
   cfg->inner_eps = 1e-2;
   cfg->inner_maxit = 60;
+  cfg->freq_chunk = 0;
 }
 
 aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
@@ -1629,15 +1531,13 @@ aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
       (cfg->problem == AAO_OSEEN && cfg->wind_q2 == nullptr) || cfg->mg_cycles < 1 || cfg->cheb_iters < 1 ||
       cfg->uzawa_iters < 1 || !(cfg->uzawa_mu > 0) || cfg->pre_sweeps < 0 || cfg->post_sweeps < 0 ||
       (cfg->pmode != AAO_PRECOND_LINEAR && cfg->pmode != AAO_PRECOND_NONLINEAR) ||
-      (cfg->pmode == AAO_PRECOND_NONLINEAR && (!(cfg->inner_eps > 0) || !(cfg->inner_eps < 1) || cfg->inner_maxit < 1)))
+      (cfg->pmode == AAO_PRECOND_NONLINEAR && (!(cfg->inner_eps > 0) || !(cfg->inner_eps < 1) || cfg->inner_maxit < 1)) ||
+      cfg->freq_chunk < 0)
     return AAO_ERR_CONFIG;
   aao_ctx* ctx = new aao_ctx();
   try {
     const char* mm = std::getenv("AAO_MG_MODE");
-    ctx->c.mg_mode = mm ? std::atoi(mm) : -1;
-    ctx->c.real_split_auto = std::getenv("AAO_REAL_SPLIT") != nullptr;
-    const char* szo = std::getenv("AAO_STORE_Z");
-    ctx->c.store_z_opt = szo ? std::atoi(szo) != 0 : true;
+    ctx->c.mg_mode = (mm && std::atoi(mm) == 1) ? 1 : 0;
     const char* we = std::getenv("AAO_WAVE");
     ctx->c.wave_force = we ? std::atoi(we) : -1;
     const char* wm = std::getenv("AAO_WAVE_MIN");
@@ -1722,10 +1622,14 @@ aao_status aao_precond_apply(aao_ctx* ctx, const double* r, double* z, void* str
   return AAO_OK;
 }
 
+static bool krylov_ok(const aao_krylov* kry) {
+  return kry && kry->restart >= 1 && kry->restart <= 64 && kry->tol > 0 && kry->max_iters >= 1 &&
+         (kry->store_z == 0 || kry->store_z == 1);
+}
+
 aao_status aao_gmres_solve(aao_ctx* ctx, const double* b, double* x, const aao_krylov* kry, aao_info* info,
                            double* hist, int hist_cap, void* stream) {
-  if (!ctx || !b || !x || !kry || kry->restart < 1 || kry->restart > 64 || !(kry->tol > 0) || kry->max_iters < 1)
-    return AAO_ERR_SHAPE;
+  if (!ctx || !b || !x || !krylov_ok(kry) || b == x) return AAO_ERR_SHAPE;
   aao_status st = AAO_OK;
   ABI_GUARD(ctx, { st = aao::gmres(ctx->c, b, x, *kry, info, hist, hist_cap, (cudaStream_t)stream); });
   return st;
@@ -1733,12 +1637,12 @@ aao_status aao_gmres_solve(aao_ctx* ctx, const double* b, double* x, const aao_k
 
 aao_status aao_gmres_solve_host(aao_ctx* ctx, const double* b_host, double* x_host, const aao_krylov* kry,
                                 aao_info* info, double* hist, int hist_cap, void* stream) {
-  if (!ctx || !b_host || !x_host || !kry) return AAO_ERR_SHAPE;
+  if (!ctx || !b_host || !x_host || b_host == x_host || !krylov_ok(kry)) return AAO_ERR_SHAPE;
   cudaStream_t s = (cudaStream_t)stream;
   const size_t bytes = ctx->c.N * sizeof(double);
-  aao_status st = AAO_OK;
   try {
-    if (!ctx->c.gr) aao::gmres_alloc(ctx->c, kry->restart);
+    ctx->c.err.clear();
+    aao::gmres_alloc(ctx->c, kry->restart);
     // device staging for b and x, allocated once per context (owned, freed by aao_destroy)
     if (!ctx->c.stage_b) {
       ctx->c.stage_b = aao::dalloc<double>(ctx->c, ctx->c.N);
@@ -1748,11 +1652,14 @@ aao_status aao_gmres_solve_host(aao_ctx* ctx, const double* b_host, double* x_ho
     return fail(ctx, e.st, e.what());
   }
   double *db = ctx->c.stage_b, *dx = ctx->c.stage_x;
-  cudaMemcpyAsync(db, b_host, bytes, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(dx, x_host, bytes, cudaMemcpyHostToDevice, s);
-  st = aao_gmres_solve(ctx, db, dx, kry, info, hist, hist_cap, stream);
-  cudaMemcpyAsync(x_host, dx, bytes, cudaMemcpyDeviceToHost, s);
-  cudaStreamSynchronize(s);
+  cudaError_t e1 = cudaMemcpyAsync(db, b_host, bytes, cudaMemcpyHostToDevice, s);
+  cudaError_t e2 = e1 == cudaSuccess ? cudaMemcpyAsync(dx, x_host, bytes, cudaMemcpyHostToDevice, s) : e1;
+  if (e2 != cudaSuccess) return fail(ctx, AAO_ERR_CUDA, std::string("host -> device copy: ") + cudaGetErrorString(e2));
+  const aao_status st = aao_gmres_solve(ctx, db, dx, kry, info, hist, hist_cap, stream);
+  if (st < 0) return st;   // x_host untouched on error
+  cudaError_t e3 = cudaMemcpyAsync(x_host, dx, bytes, cudaMemcpyDeviceToHost, s);
+  if (e3 == cudaSuccess) e3 = cudaStreamSynchronize(s);
+  if (e3 != cudaSuccess) return fail(ctx, AAO_ERR_CUDA, std::string("device -> host copy: ") + cudaGetErrorString(e3));
   return st;
 }
 
@@ -1785,11 +1692,18 @@ aao_status aao_set_timing(aao_ctx* ctx, int on) {
 }
 
 aao_status aao_profile_smoother(aao_ctx* ctx, int on) {
-  if (!ctx) return AAO_ERR_SHAPE;
-  ctx->c.prof = on != 0;
-  ctx->c.prof_used = 0;
-  ctx->c.prof_bytes = 0;
-  ctx->c.prof_launches = 0;
+  if (!ctx || on < 0) return AAO_ERR_SHAPE;
+  auto& c = ctx->c;
+  c.prof = on != 0;
+  c.prof_used = 0;
+  c.prof_bytes = 0;
+  c.prof_launches = 0;
+  // on > 1: create the events for `on` launches now, so that none is created inside a timed region
+  while (on > 1 && c.prof_ev.size() < 2 * (size_t)on) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return fail(ctx, AAO_ERR_CUDA, "cudaEventCreate");
+    c.prof_ev.push_back(e);
+  }
   return AAO_OK;
 }
 
@@ -1814,14 +1728,22 @@ aao_status aao_profile_read(aao_ctx* ctx, double* out3) {
 
 aao_status aao_last_phase_ms(aao_ctx* ctx, double* ms4) {
   if (!ctx || !ms4) return AAO_ERR_SHAPE;
-  if (!ctx->c.timing) return fail(ctx, AAO_ERR_CONFIG, "timing not enabled");
-  cudaEventSynchronize(ctx->c.ev[4]);
-  float t[4];
-  cudaEventElapsedTime(&t[0], ctx->c.ev[0], ctx->c.ev[1]);
-  cudaEventElapsedTime(&t[1], ctx->c.ev[1], ctx->c.ev[2]);
-  cudaEventElapsedTime(&t[2], ctx->c.ev[2], ctx->c.ev[3]);
-  cudaEventElapsedTime(&t[3], ctx->c.ev[3], ctx->c.ev[4]);
-  for (int i = 0; i < 4; ++i) ms4[i] = t[i];
+  for (int i = 0; i < 4; ++i) ms4[i] = 0.0;
+  if (!ctx->c.timing) return fail(ctx, AAO_ERR_CONFIG, "timing not enabled (aao_set_timing)");
+  if (!ctx->c.phase_valid)
+    return fail(ctx, AAO_ERR_CONFIG, "no linear precond_apply recorded with timing on since the last apply");
+  if (cudaEventSynchronize(ctx->c.ev[4]) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(ctx, AAO_ERR_CUDA, "phase event synchronisation failed");
+  }
+  for (int i = 0; i < 4; ++i) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, ctx->c.ev[i], ctx->c.ev[i + 1]) != cudaSuccess) {
+      (void)cudaGetLastError();   // leave no pending error for the next ABI call
+      return fail(ctx, AAO_ERR_CUDA, "phase event elapsed time failed");
+    }
+    ms4[i] = t;
+  }
   return AAO_OK;
 }
 

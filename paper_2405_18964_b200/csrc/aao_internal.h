@@ -74,9 +74,7 @@ struct MGArgs {
   int nu;
   int lsm;                // levels >= lsm keep x and b in shared memory (offsets below, in double2)
   int lwarp;              // levels >= lwarp run inside one warp (tiny bottom of the V-cycle)
-  int use_ctab;           // Q2 real operators: per-level class stencils at the start of dynamic smem
-  int perm;               // residue-blocked Q2 solve (k_mg_q2p): xw[0] is the finest iterate workspace
-  long pstride[MG_MAXL];  // per-problem stride of the level workspaces (n + padding)
+  int use_ctab;           // Q2 operators: per-level class stencils at the start of dynamic smem
   long sm_x[MG_MAXL], sm_b[MG_MAXL];
   int wave_h, wave_min;     // band-wavefront sweeps (2-D Q2 real): band height (3 or 6), levels with n1 >= wave_min
   long ring_off;            // ring buffer offset in dynamic smem (double2 units)
@@ -95,9 +93,7 @@ struct MGSpace {       // an MG hierarchy for one space, with batch workspace
   int nlev;
   std::vector<Grid> grids;
   std::vector<Transfer> transfers;
-  std::vector<double2*> x, b, r;     // per level (level 0 x/b external)
-  std::vector<double2*> px, pb, pr;  // residue-blocked workspaces (Q2), per-problem stride n + pad
-  std::vector<long> pstride;
+  std::vector<double2*> x, b, r;     // per level (level 0 x/b external), nprob_max problems each
   int ncoarse_unk;                   // unknowns on the coarsest grid
   int* coarse_unk;                   // device, node indices
   int nprob_max;
@@ -149,13 +145,13 @@ struct Ctx {
   int inner_max = 0;
   double2* debug_block_src_v = nullptr;  // frequency vector of the last NL solution (debug block)
   double2* debug_block_src_p = nullptr;
-  bool store_z_opt = true;               // AAO_STORE_Z at aao_create
-  bool store_z = false;                  // GMRES keeps Z_k = P^{-1} v_k (FGMRES always; linear if it fits)
-  double* gZ = nullptr;                  // FGMRES preconditioned basis
+  bool store_z = false;                  // this solve keeps Z_k = P^{-1} v_k (FGMRES always; linear on request)
+  int gZ_m = 0;                          // stored-Z vectors allocated
+  double* gZ = nullptr;                  // preconditioned basis (FGMRES, or aao_krylov.store_z)
   double** gZptr = nullptr;
-  // GMRES workspace (allocated on first solve)
+  // GMRES workspace (allocated on first solve): basis V_0..V_m and one work vector (z / update)
   int gm_m = 0;
-  double *gV = nullptr, *gz = nullptr, *gw = nullptr, *gu = nullptr, *gr = nullptr;
+  double *gV = nullptr, *gz = nullptr;
   double *gH = nullptr, *gpart = nullptr, *gscal = nullptr;
   double **gVptr = nullptr;
   double *stage_b = nullptr, *stage_x = nullptr;   // device staging of aao_gmres_solve_host
@@ -174,9 +170,9 @@ struct Ctx {
   cudaStream_t s2 = nullptr;               // side stream: pressure solves overlap the velocity MG
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int wave_force = -1, wave_min = 257;   // band-wavefront sweeps: AAO_WAVE (-1 auto), AAO_WAVE_MIN
-  int mg_mode = -1;      // MG schedule: -1 auto, 0 CTA-resident, 1 per level/colour launches, 2 hybrid (AAO_MG_MODE)
-  int tail = -1;
-  bool real_split_auto = false;   // real-split MG in auto mode (AAO_REAL_SPLIT); measured slower on c2         // hybrid: first CTA-resident level of the current solve
+  int mg_mode = 0;       // MG schedule: 0 CTA-resident (default), 1 per level / colour launches (AAO_MG_MODE=1)
+  int freq_chunk = 0;    // frequencies per velocity-MG launch (aao_config.freq_chunk; workspace sized for it)
+  bool phase_valid = false;   // ev[0..4] recorded by the last linear precond_apply (aao_last_phase_ms)
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;   // pairs (start, end)
   size_t prof_used = 0;
@@ -207,24 +203,6 @@ void launch_lincomb(const Grid& g, View out, double cb, View b, const OpSel& A1,
 void launch_axpby(const Grid& g, View y, double2 a, View x, double2 bcoef, int nprob, cudaStream_t s);
 void launch_mg_cta(const MGArgs& a, int nprob, size_t smem, cudaStream_t s);
 
-// real-split CTA-resident MG for real operators (no convection): real / imaginary parts in turn
-struct MGRealArgs {
-  int nlev, cycles, pre, post;
-  double omega;
-  Grid g[MG_MAXL];
-  Transfer t[MG_MAXL];
-  double* xw[MG_MAXL];    // global real scratch [nprob][n_l] (levels not in shared memory)
-  double* bw[MG_MAXL];
-  double* rw[MG_MAXL];
-  long xsm[MG_MAXL], bsm[MG_MAXL];   // shared-memory offsets in doubles, -1 = global
-  View x0, b0;            // complex finest-level solution / right-hand side
-  OpSel op;               // real parts of coef a, b are used
-  const double2* inv;
-  int inv_pg;
-  const int* unk;
-  int nu;
-};
-void launch_mg_real(const MGRealArgs& a, int nprob, size_t smem, cudaStream_t s);
 void launch_cheb_cta(const Grid& g, View b, View x, double2* r, double2* d0, double2* d1, double theta, double sigma,
                      double delta, int iters, double scale, int nprob, cudaStream_t s);
 // pressure: out = sb*bp + sB * sum_c B_c v_c (v: d components per problem group)

@@ -68,7 +68,8 @@ void launch_axpy_dev(double* y, const double* x, const double* alpha, double sig
   k_axpy_dev<<<DOT_BLOCKS, 256, 0, s>>>(y, x, alpha, sign, n);
 }
 
-__global__ void k_scale_dev(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ den,
+// y and x may alias (in-place scaling)
+__global__ void k_scale_dev(double* y, const double* x, const double* __restrict__ den,
                             long n) {
   const double a = 1.0 / *den;
   const long stride = (long)gridDim.x * blockDim.x;
@@ -86,7 +87,8 @@ void launch_axpy(double* y, const double* x, double alpha, long n, cudaStream_t 
   k_axpy<<<DOT_BLOCKS, 256, 0, s>>>(y, x, alpha, n);
 }
 
-__global__ void k_copy_sub(double* __restrict__ y, const double* __restrict__ b, const double* __restrict__ ax,
+// y and ax may alias (r = b - A x formed in place)
+__global__ void k_copy_sub(double* y, const double* __restrict__ b, const double* ax,
                            long n) {
   const long stride = (long)gridDim.x * blockDim.x;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) y[i] = b[i] - ax[i];
@@ -302,7 +304,7 @@ static long mgs_oc_smem(long n, long* C2out) {
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     max_smem -= 8 * 1024;   // static smem of block_sum / hs and headroom
   }
-  if (n % 2 != 0 || std::getenv("AAO_MGS_STREAM")) return -1;
+  if (n % 2 != 0) return -1;
   const long C2 = (n / 2 + mgs_blocks() - 1) / mgs_blocks();
   const long bytes = std::max(0L, C2 - (long)MGS_OC_R2 * MGS_OC_THREADS) * (long)sizeof(double2);
   if (bytes > max_smem) return -1;

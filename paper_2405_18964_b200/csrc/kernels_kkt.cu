@@ -772,8 +772,6 @@ __global__ void __launch_bounds__(256, 1) k_kkt_march3(K3Args a, KMRows R) {
 
 // true if the time-marching kernel handles this context (2-D); launched on stream s
 bool launch_kkt_march(const Ctx& c, const double* x, double* y, cudaStream_t s) {
-  static const bool off = std::getenv("AAO_KKT_TILED") != nullptr;
-  if (off) return false;
   if (c.n1q2 < 9) return false;   // generic rows need an interior vertex and midpoint (N_c >= 4)
   if (c.dim == 3 && c.oseen) return false;
   // Oseen: the per-node convection stencils (25 coefficients per node and time block, read through L2)

@@ -882,44 +882,6 @@ __device__ __forceinline__ void cta_visit(int n1, const int* s0, const int* sta,
   }
 }
 
-// Same visit, two nodes per thread per round (t and t + nth): f2(c, idx, c2, idx2, has2) lets the
-// caller issue the loads of both before either store (colour steps: no same-colour coupling).
-template <int DIM, class F2>
-__device__ __forceinline__ void cta_visit2(int n1, const int* s0, const int* sta, int lo, int hi, int tid, int nth,
-                                           F2&& f2) {
-  int cnt[DIM], start[DIM], stv[DIM];
-  int total = 1;
-#pragma unroll
-  for (int a = 0; a < DIM; ++a) {
-    int s = s0[a];
-    while (s < lo) s += sta[a];
-    start[a] = s;
-    stv[a] = sta[a];
-    cnt[a] = s > hi ? 0 : (hi - s) / sta[a] + 1;
-    total *= cnt[a];
-  }
-  if (total == 0) return;
-  auto node = [&](int t, int* c) {
-    const unsigned q = (unsigned)t / (unsigned)cnt[0];
-    c[0] = start[0] + stv[0] * (int)((unsigned)t - q * (unsigned)cnt[0]);
-    if (DIM == 2) {
-      c[1] = start[1] + stv[1] * (int)q;
-    } else {
-      const unsigned q2 = q / (unsigned)cnt[1];
-      c[1] = start[1] + stv[1] * (int)(q - q2 * (unsigned)cnt[1]);
-      c[2] = start[2] + stv[2] * (int)q2;
-    }
-    return DIM == 2 ? c[1] * n1 + c[0] : (c[2] * n1 + c[1]) * n1 + c[0];
-  };
-  for (int t = tid; t < total; t += 2 * nth) {
-    int c[DIM], c2[DIM];
-    const int idx = node(t, c);
-    const bool has2 = t + nth < total;
-    const int idx2 = node(has2 ? t + nth : t, c2);
-    f2(c, idx, c2, idx2, has2);
-  }
-}
-
 // all unknowns of a level: Q2 in y/z parity classes (uniform taps per warp), Q1 in one pass
 template <int DIM, int ORD, class F>
 __device__ __forceinline__ void cta_all_unknowns(int n1, int tid, int nth, F&& f) {
@@ -1183,20 +1145,7 @@ __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const d
             s0[a] = res[a] + 3 * ((cls >> (a - 1)) & 1);
             st[a] = 6;
           }
-          if constexpr (TAB && !CONV && false) {   // 2 nodes per thread: measured slower (2.82 vs 2.40 ms, c2)
-            cta_visit2<DIM>(g.n1, s0, st, 1, g.n1 - 2, tid, nth,
-                            [&](const int* c, int idx, const int* c2, int idx2, bool has2) {
-                              double iA, iB;
-                              const double2 A1 = class_eval<DIM>(tabl, x, c, g.n1, iA);
-                              const double2 A2 = class_eval<DIM>(tabl, x, c2, g.n1, iB);
-                              const double2 b1 = b[idx], b2 = b[idx2];
-                              const double2 x1 = x[idx], x2 = x[idx2];
-                              x[idx] = cadd(x1, cscale(omega * iA, csub(b1, A1)));
-                              if (has2) x[idx2] = cadd(x2, cscale(omega * iB, csub(b2, A2)));
-                            });
-          } else {
-            cta_visit<DIM>(g.n1, s0, st, 1, g.n1 - 2, tid, nth, upd);
-          }
+          cta_visit<DIM>(g.n1, s0, st, 1, g.n1 - 2, tid, nth, upd);
         }
       } else {
         int st[DIM];
@@ -1482,365 +1431,6 @@ __global__ void __launch_bounds__(mg_threads<DIM, TAB>(), 1) k_mg_cta(MGArgs a) 
   }
 }
 
-// ---------------------------------------------------------------- residue-blocked Q2 MG
-// Inside the CTA-resident solve every Q2 level is stored residue-blocked: within each row the
-// columns are reordered [i = 0 mod 3 | i = 1 mod 3 | i = 2 mod 3].  A multicolour SOR step updates
-// the nodes i = r + 3m of one residue r, so lane m of a warp reads tap i+o at m + K[o] (K warp-uniform):
-// every tap load is a contiguous, fully coalesced warp access (4 sectors-lines per 32 complex values
-// instead of ~9), and no tap of an interior node leaves its row, so no clamping is needed.
-// The finest iterate lives in a residue-blocked workspace and is copied to the natural output at the
-// end; the finest right-hand side is read in natural order.  Same arithmetic as k_mg_cta.
-struct RPerm {
-  int r1, r2;
-  __device__ explicit RPerm(int n1) {
-    const int c0 = (n1 + 2) / 3, c1 = (n1 + 1) / 3;
-    r1 = c0;
-    r2 = c0 + c1;
-  }
-  __device__ int roff(int r) const { return r == 0 ? 0 : (r == 1 ? r1 : r2); }
-  __device__ int col(int i) const {
-    const int q = i / 3, r = i - 3 * q;
-    return roff(r) + q;
-  }
-};
-
-// K[o] = column offset of tap i + o - 2 relative to m, for nodes i = rx + 3m
-__device__ __forceinline__ void tap_offsets(const RPerm& P, int rx, int* K) {
-#pragma unroll
-  for (int o = 0; o < 5; ++o) {
-    const int t = rx + o - 2;
-    const int q = t >= 0 ? t / 3 : -1;
-    K[o] = P.roff(t - 3 * q) + q;
-  }
-}
-
-// class-stencil evaluation on the residue-blocked layout; rowbase(z, y) = (z n1 + y) n1
-template <int DIM, bool CONV>
-__device__ __forceinline__ double2 p_eval(const double* tabl, const double* cv, double2 cc, const double2* x,
-                                          const int* c, int m, const int* K, int n1, double& invD, double2& Dc) {
-  using CT = ClassTab<DIM>;
-  const int cls = (c[0] & 1) | ((c[1] & 1) << 1) | (DIM == 3 ? ((c[2] & 1) << 2) : 0);
-  const int py = c[1] & 1, pz = DIM == 3 ? (c[2] & 1) : 0;
-  const int ob0 = py ? 1 : 0, ob1 = py ? 4 : 5;
-  const int oc0 = DIM == 3 ? (pz ? 1 : 0) : 2, oc1 = DIM == 3 ? (pz ? 4 : 5) : 3;
-  double2 acc = make_double2(0.0, 0.0), nacc = acc;
-  const int nat = DIM == 2 ? c[1] * n1 + c[0] : (c[2] * n1 + c[1]) * n1 + c[0];
-  if (CONV) {
-    const double2* T = reinterpret_cast<const double2*>(tabl) + cls * CT::NT;
-    const double* cvr = cv + (long)nat * CT::NT;
-    for (int oc = oc0; oc < oc1; ++oc)
-#pragma unroll
-      for (int ob = 0; ob < 5; ++ob) {
-        if (ob < ob0 || ob >= ob1) continue;
-        const double2* row = x + ((DIM == 3 ? (c[2] + oc - 2) * n1 : 0) + c[1] + ob - 2) * n1 + m;
-        const int t0 = ((DIM == 3 ? oc * 5 : 0) + ob) * 5;
-#pragma unroll
-        for (int oa = 0; oa < 5; ++oa) {
-          const double2 v = row[K[oa]];
-          acc = cadd(acc, cmul(T[t0 + oa], v));
-          nacc = cfma(__ldg(cvr + t0 + oa), v, nacc);
-        }
-      }
-    const int centre = DIM == 2 ? 12 : 62;
-    Dc = cadd(T[centre], cscale(__ldg(cvr + centre), cc));
-    invD = 0.0;
-    return cadd(acc, cmul(cc, nacc));
-  } else {
-    const double* T = tabl + cls * (CT::NT + 1);
-    invD = T[CT::NT];
-    for (int oc = oc0; oc < oc1; ++oc)
-#pragma unroll
-      for (int ob = 0; ob < 5; ++ob) {
-        if (ob < ob0 || ob >= ob1) continue;
-        const double2* row = x + ((DIM == 3 ? (c[2] + oc - 2) * n1 : 0) + c[1] + ob - 2) * n1 + m;
-        const double* t = T + ((DIM == 3 ? oc * 5 : 0) + ob) * 5;
-#pragma unroll
-        for (int oa = 0; oa < 5; ++oa) acc = cfma(t[oa], row[K[oa]], acc);
-      }
-    return acc;
-  }
-}
-
-struct PLevels {
-  const MGArgs& a;
-  double2* smem;
-  int p;
-  double* ctab;
-  __device__ double2* X(int l) const {   // residue-blocked iterate (level 0: workspace)
-    if (l == 0) return a.xw[0] + (long)p * a.pstride[0];
-    return l >= a.lsm ? smem + a.sm_x[l] : a.xw[l] + (long)p * a.pstride[l];
-  }
-  __device__ double2* B(int l) const {   // residue-blocked rhs, l >= 1
-    return l >= a.lsm ? smem + a.sm_b[l] : a.bw[l] + (long)p * a.pstride[l];
-  }
-  __device__ double2* R(int l) const { return a.rw[l] + (long)p * a.pstride[l]; }
-  __device__ const double* CV(int l) const { return a.op.conv_sel == 1 ? a.g[l].conv : a.g[l].convT; }
-  __device__ const double* TAB(int l, bool conv) const {
-    return ctab + l * (conv ? 2 * ClassTab<2>::NCL * ClassTab<2>::NT : ClassTab<2>::PER_LEVEL);
-  }
-};
-
-template <int DIM, bool CONV>
-__device__ __forceinline__ const double* p_tab(const PLevels& S, int l) {
-  using CT = ClassTab<DIM>;
-  return S.ctab + l * (CONV ? 2 * CT::NCL * CT::NT : CT::PER_LEVEL);
-}
-
-// one SOR sweep set (or the residual when RES) over residue-blocked level l
-template <int DIM, bool CONV, bool W, bool RES>
-__device__ void p_pass(const PLevels& S, const Coef& cf, int l, const double2* bnat, int sweeps, bool reverse,
-                       int tid, int nth) {
-  const MGArgs& a = S.a;
-  const Grid g = a.g[l];
-  const int n1 = g.n1;
-  const RPerm P(n1);
-  double2* x = S.X(l);
-  const double2* b = l == 0 ? bnat : S.B(l);
-  double2* r = S.R(l);
-  const double* tabl = p_tab<DIM, CONV>(S, l);
-  const double* cv = S.CV(l);
-  const double omega = a.omega;
-  constexpr int NC = DIM == 2 ? 9 : 27;
-  const int nsteps = RES ? 3 : sweeps * NC;   // residual: one pass per x-residue
-  for (int st = 0; st < nsteps; ++st) {
-    int res[DIM];
-    if (RES) {
-      res[0] = st;
-    } else {
-      const int cc = st % NC;
-      int col = reverse ? NC - 1 - cc : cc;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        res[d] = col % 3;
-        col /= 3;
-      }
-    }
-    int K[5];
-    tap_offsets(P, res[0], K);
-    const int xo = P.roff(res[0]);
-    const int ncls = 1 << (DIM - 1);
-    for (int cls = 0; cls < ncls; ++cls) {
-      int s0[DIM], sta[DIM];
-      s0[0] = res[0];
-      sta[0] = 3;
-#pragma unroll
-      for (int d = 1; d < DIM; ++d) {
-        if (RES) {
-          s0[d] = ((cls >> (d - 1)) & 1) ? 1 : 2;
-          sta[d] = 2;
-        } else {
-          s0[d] = res[d] + 3 * ((cls >> (d - 1)) & 1);
-          sta[d] = 6;
-        }
-      }
-      cta_visit<DIM>(n1, s0, sta, 1, n1 - 2, tid, nth, [&](const int* c, int) {
-        const int m = (c[0] - res[0]) / 3;
-        const int rowb = (DIM == 2 ? c[1] : c[2] * n1 + c[1]) * n1;
-        const int own = rowb + xo + m;
-        double invD;
-        double2 Dc;
-        const double2 Ax = p_eval<DIM, CONV>(tabl, cv, cf.c, x, c, m, K, n1, invD, Dc);
-        const double2 bb = l == 0 ? b[rowb + c[0]] : b[own];
-        if (RES) {
-          r[own] = csub(bb, Ax);
-        } else if (CONV) {
-          x[own] = cadd(x[own], cscale(omega, cdiv(csub(bb, Ax), Dc)));
-        } else {
-          x[own] = cadd(x[own], cscale(omega * invD, csub(bb, Ax)));
-        }
-      });
-    }
-    gsync<W>();
-  }
-}
-
-template <int DIM, bool CONV, bool W>
-__device__ void p_down(const PLevels& S, const Coef& cf, int l, const double2* bnat, int tid, int nth) {
-  const MGArgs& a = S.a;
-  const Grid g = a.g[l];
-  if (l > 0) {
-    double2* xl = S.X(l);
-    for (int i = tid; i < (int)a.pstride[l]; i += nth) xl[i] = make_double2(0.0, 0.0);
-    gsync<W>();
-  }
-  p_pass<DIM, CONV, W, false>(S, cf, l, bnat, a.pre, false, tid, nth);
-  p_pass<DIM, CONV, W, true>(S, cf, l, bnat, 0, false, tid, nth);
-  // restriction b_{l+1} = P^T r_l (coarse natural iteration, both layouts residue-blocked)
-  const Grid gc = a.g[l + 1];
-  const Transfer t = a.t[l];
-  const RPerm Pf(g.n1), Pc(gc.n1);
-  const double2* rl = S.R(l);
-  double2* bn = S.B(l + 1);
-  for (int I = tid; I < (int)gc.n; I += nth) {
-    int c[DIM];
-    coords<DIM>(I, gc.n1, c);
-    const int crow = (DIM == 2 ? c[1] : c[2] * gc.n1 + c[1]) * gc.n1;
-    if (masked<DIM, 2>(c, I, gc.n1)) {
-      bn[crow + Pc.col(c[0])] = make_double2(0.0, 0.0);
-      continue;
-    }
-    double w[DIM][7];
-#pragma unroll
-    for (int d = 0; d < DIM; ++d)
-#pragma unroll
-      for (int o = 0; o < 7; ++o) w[d][o] = __ldg(t.tR + c[d] * 7 + o);
-    int fc[7];
-#pragma unroll
-    for (int oa = 0; oa < 7; ++oa) {
-      const int f = 2 * c[0] + oa - 3;
-      fc[oa] = (f >= 0 && f < g.n1) ? Pf.col(f) : 0;
-    }
-    double2 acc = make_double2(0.0, 0.0);
-    const int n1 = g.n1;
-    for (int oc = 0; oc < (DIM == 3 ? 7 : 1); ++oc) {
-      if (DIM == 3 && w[DIM == 3 ? 2 : 0][oc] == 0.0) continue;
-      for (int ob = 0; ob < 7; ++ob) {
-        if (w[1][ob] == 0.0) continue;
-        const double wzy = (DIM == 3 ? w[DIM == 3 ? 2 : 0][oc] : 1.0) * w[1][ob];
-        const double2* rrow = rl + ((DIM == 3 ? (2 * c[DIM == 3 ? 2 : 0] + oc - 3) * n1 : 0) + 2 * c[1] + ob - 3) * n1;
-#pragma unroll
-        for (int oa = 0; oa < 7; ++oa)
-          if (w[0][oa] != 0.0) acc = cfma(wzy * w[0][oa], rrow[fc[oa]], acc);
-      }
-    }
-    bn[crow + Pc.col(c[0])] = acc;
-  }
-  gsync<W>();
-}
-
-template <int DIM, bool W>
-__device__ void p_coarse(const PLevels& S, int tid, int nth) {
-  const MGArgs& a = S.a;
-  const int L = a.nlev;
-  const Grid g = a.g[L - 1];
-  const RPerm P(g.n1);
-  double2* xL = S.X(L - 1);
-  const double2* bL = S.B(L - 1);
-  for (int i = tid; i < (int)a.pstride[L - 1]; i += nth) xL[i] = make_double2(0.0, 0.0);
-  gsync<W>();
-  const double2* A = a.inv + (long)(S.p / a.inv_pg) * a.nu * a.nu;
-  auto pm = [&](int nat) {
-    int c[DIM];
-    coords<DIM>(nat, g.n1, c);
-    return (DIM == 2 ? c[1] : c[2] * g.n1 + c[1]) * g.n1 + P.col(c[0]);
-  };
-  for (int i = tid; i < a.nu; i += nth) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int j = 0; j < a.nu; ++j) acc = cadd(acc, cmul(A[(long)i * a.nu + j], bL[pm(a.unk[j])]));
-    xL[pm(a.unk[i])] = acc;
-  }
-  gsync<W>();
-}
-
-template <int DIM, bool CONV, bool W>
-__device__ void p_up(const PLevels& S, const Coef& cf, int l, const double2* bnat, int tid, int nth) {
-  const MGArgs& a = S.a;
-  const Grid g = a.g[l];
-  const Grid gc = a.g[l + 1];
-  const Transfer t = a.t[l];
-  const RPerm Pf(g.n1), Pc(gc.n1);
-  double2* xl = S.X(l);
-  const double2* xc = S.X(l + 1);
-  cta_all_unknowns<DIM, 2>(g.n1, tid, nth, [&](const int* c, int) {
-    int base[DIM];
-    double w[DIM][3];
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-      base[d] = (int)__ldg(t.tP + c[d] * 4);
-#pragma unroll
-      for (int o = 0; o < 3; ++o) w[d][o] = __ldg(t.tP + c[d] * 4 + 1 + o);
-    }
-    const int n1c = gc.n1;
-    int cc[3];
-#pragma unroll
-    for (int oa = 0; oa < 3; ++oa) cc[oa] = Pc.col(base[0] + oa);
-    double2 acc = make_double2(0.0, 0.0);
-    for (int oc = 0; oc < (DIM == 3 ? 3 : 1); ++oc) {
-      const double wz = DIM == 3 ? w[DIM == 3 ? 2 : 0][oc] : 1.0;
-      if (wz == 0.0) continue;
-#pragma unroll
-      for (int ob = 0; ob < 3; ++ob) {
-        const double wzy = wz * w[1][ob];
-        if (wzy == 0.0) continue;
-        const double2* crow = xc + ((DIM == 3 ? (base[DIM == 3 ? 2 : 0] + oc) * n1c : 0) + base[1] + ob) * n1c;
-#pragma unroll
-        for (int oa = 0; oa < 3; ++oa)
-          if (w[0][oa] != 0.0) acc = cfma(wzy * w[0][oa], crow[cc[oa]], acc);
-      }
-    }
-    const int own = (DIM == 2 ? c[1] : c[2] * g.n1 + c[1]) * g.n1 + Pf.col(c[0]);
-    xl[own] = cadd(xl[own], acc);
-  });
-  gsync<W>();
-  p_pass<DIM, CONV, W, false>(S, cf, l, bnat, a.post, true, tid, nth);
-}
-
-template <int DIM, bool CONV>
-__global__ void __launch_bounds__(MG_THREADS_TAB, 1) k_mg_q2p(MGArgs a) {
-  extern __shared__ double2 smem[];
-  const int p = blockIdx.x;
-  const int L = a.nlev;
-  const Coef cf = a.op.coef[p / a.op.per_group];
-  const int tid = threadIdx.x, nth = blockDim.x;
-  double* ctab = reinterpret_cast<double*>(smem);
-  for (int l = 0; l < L - 1; ++l) {
-    if (CONV)
-      build_class_tab_c<DIM>(a.g[l], cf.a, cf.b,
-                             reinterpret_cast<double2*>(ctab) + l * ClassTab<DIM>::NCL * ClassTab<DIM>::NT, tid, nth);
-    else
-      build_class_tab<DIM>(a.g[l], cf.a.x, cf.b.x, ctab + l * ClassTab<DIM>::PER_LEVEL, tid, nth);
-  }
-  const PLevels S{a, smem, p, ctab};
-  const double2* bnat = a.b0.p + voff(a.b0, p, a.g[0].n);
-  {
-    double2* x0 = S.X(0);
-    for (int i = tid; i < (int)a.pstride[0]; i += nth) x0[i] = make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  const int lw = a.lwarp;
-  const bool clk = a.clk != nullptr && blockIdx.x == 0 && tid == 0;
-  unsigned long long t0 = clk ? clock64() : 0ull;
-  auto mark = [&](int slot) {
-    if (clk) {
-      const unsigned long long t1 = clock64();
-      a.clk[slot] += t1 - t0;
-      t0 = t1;
-    }
-  };
-  for (int cyc = 0; cyc < a.cycles; ++cyc) {
-    for (int l = 0; l < lw && l < L - 1; ++l) {
-      p_down<DIM, CONV, false>(S, cf, l, bnat, tid, nth);
-      mark(2 * l);
-    }
-    if (lw < L) {
-      if (tid < 32) {
-        for (int l = lw; l < L - 1; ++l) p_down<DIM, CONV, true>(S, cf, l, bnat, tid, 32);
-        p_coarse<DIM, true>(S, tid, 32);
-        for (int l = L - 2; l >= lw; --l) p_up<DIM, CONV, true>(S, cf, l, bnat, tid, 32);
-      }
-      __syncthreads();
-    } else {
-      p_coarse<DIM, false>(S, tid, nth);
-    }
-    mark(2 * MG_MAXL - 1);
-    for (int l = (lw < L ? lw : L - 1) - 1; l >= 0; --l) {
-      p_up<DIM, CONV, false>(S, cf, l, bnat, tid, nth);
-      mark(2 * l + 1);
-    }
-  }
-  // natural-order output of the finest iterate (masked entries are 0)
-  const Grid g0 = a.g[0];
-  const RPerm P0(g0.n1);
-  const double2* xp = S.X(0);
-  double2* xo = a.x0.p + voff(a.x0, p, g0.n);
-  for (int i = tid; i < (int)g0.n; i += nth) {
-    int c[DIM];
-    coords<DIM>(i, g0.n1, c);
-    const int rowb = (DIM == 2 ? c[1] : c[2] * g0.n1 + c[1]) * g0.n1;
-    xo[i] = xp[rowb + P0.col(c[0])];
-  }
-}
-
 // Chebyshev semi-iteration on a mass matrix, one CTA per problem
 template <int DIM, int ORD>
 __global__ void __launch_bounds__(MG_THREADS, 1) k_cheb_cta(Grid g, View bv, View xv, double2* rw, double2* d0w, double2* d1w,
@@ -1904,325 +1494,6 @@ __global__ void __launch_bounds__(MG_THREADS, 1) k_cheb_cta(Grid g, View bv, Vie
     rho = rho1;
   }
   for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) x[i] = cscale(scale, cadd(x[i], d0[i]));
-}
-
-// ---------------------------------------------------------------- real-split CTA-resident MG
-// For real operators (Stokes W_k = (1+c1)M + c2 nu K and K_p) the real and imaginary parts of a
-// complex right-hand side are two independent real problems.  Solving them in turn halves every
-// array, so the finest level of c1/c2-sized problems lives in shared memory with all coarse levels:
-// the whole 4-V-cycle solve then touches global memory only for b, the finest residual and the
-// result.  Same arithmetic as k_mg_cta per component.
-template <int DIM, int PY, int PZ>
-__device__ __forceinline__ void q2_MK_real(const Grid& g, const double* x, const int* c, double& Mx, double& Kx,
-                                           double& dM, double& dK) {
-  constexpr int AY0 = PY ? 1 : 0, AY1 = PY ? 4 : 5;
-  constexpr int AZ0 = DIM == 3 ? (PZ ? 1 : 0) : 2, AZ1 = DIM == 3 ? (PZ ? 4 : 5) : 3;
-  const int n1 = g.n1;
-  double mx[5], kx[5];
-#pragma unroll
-  for (int oa = 0; oa < 5; ++oa) {
-    mx[oa] = __ldg(g.tM + c[0] * 5 + oa);
-    kx[oa] = __ldg(g.tK + c[0] * 5 + oa);
-  }
-  const int xl = c[0] >= 2 ? c[0] - 2 : c[0], xr = c[0] + 2 <= n1 - 1 ? c[0] + 2 : c[0];
-  Mx = Kx = 0.0;
-  double mzc = 1.0, kzc = 0.0, myc = 0.0, kyc = 0.0;
-#pragma unroll
-  for (int oc = AZ0; oc < AZ1; ++oc) {
-    double mz = 1.0, kz = 0.0;
-    int zrow = 0;
-    if (DIM == 3) {
-      mz = __ldg(g.tM + c[2] * 5 + oc);
-      kz = __ldg(g.tK + c[2] * 5 + oc);
-      zrow = (c[2] + oc - 2) * n1;
-      if (oc == 2) {
-        mzc = mz;
-        kzc = kz;
-      }
-    }
-#pragma unroll
-    for (int ob = AY0; ob < AY1; ++ob) {
-      const double my = __ldg(g.tM + c[1] * 5 + ob);
-      const double ky = __ldg(g.tK + c[1] * 5 + ob);
-      if (ob == 2) {
-        myc = my;
-        kyc = ky;
-      }
-      const double* row = x + (zrow + c[1] + ob - 2) * n1;
-      double rm = 0.0, rk = 0.0;
-#pragma unroll
-      for (int oa = 0; oa < 5; ++oa) {
-        const double v = row[oa == 0 ? xl : (oa == 4 ? xr : c[0] + oa - 2)];
-        rm = fma(mx[oa], v, rm);
-        rk = fma(kx[oa], v, rk);
-      }
-      const double mzy = mz * my, kzy = kz * my + mz * ky;
-      Mx = fma(mzy, rm, Mx);
-      Kx = fma(kzy, rm, fma(mzy, rk, Kx));
-    }
-  }
-  dM = mzc * myc * mx[2];
-  dK = kzc * myc * mx[2] + mzc * kyc * mx[2] + mzc * myc * kx[2];
-}
-
-template <int DIM>
-__device__ __forceinline__ void q1_MK_real(const Grid& g, const double* x, const int* c, double& Mx, double& Kx,
-                                           double& dM, double& dK) {
-  const int n1 = g.n1;
-  double mx[3], kx[3];
-#pragma unroll
-  for (int o = 0; o < 3; ++o) {
-    mx[o] = __ldg(g.tM + c[0] * 3 + o);
-    kx[o] = __ldg(g.tK + c[0] * 3 + o);
-  }
-  const int xl = c[0] >= 1 ? c[0] - 1 : c[0], xr = c[0] + 1 <= n1 - 1 ? c[0] + 1 : c[0];
-  Mx = Kx = 0.0;
-  double mzc = 1.0, kzc = 0.0, myc = 0.0, kyc = 0.0;
-  const int nz = DIM == 3 ? 3 : 1;
-#pragma unroll
-  for (int oc = 0; oc < nz; ++oc) {
-    double mz = 1.0, kz = 0.0;
-    int zrow = 0;
-    if (DIM == 3) {
-      mz = __ldg(g.tM + c[2] * 3 + oc);
-      kz = __ldg(g.tK + c[2] * 3 + oc);
-      zrow = clampi(c[2] + oc - 1, 0, n1 - 1) * n1;
-      if (oc == 1) {
-        mzc = mz;
-        kzc = kz;
-      }
-    }
-#pragma unroll
-    for (int ob = 0; ob < 3; ++ob) {
-      const double my = __ldg(g.tM + c[1] * 3 + ob);
-      const double ky = __ldg(g.tK + c[1] * 3 + ob);
-      if (ob == 1) {
-        myc = my;
-        kyc = ky;
-      }
-      const double* row = x + (zrow + clampi(c[1] + ob - 1, 0, n1 - 1)) * n1;
-      const double v0 = row[xl], v1 = row[c[0]], v2 = row[xr];
-      const double rm = fma(mx[0], v0, fma(mx[1], v1, mx[2] * v2));
-      const double rk = fma(kx[0], v0, fma(kx[1], v1, kx[2] * v2));
-      const double mzy = mz * my, kzy = kz * my + mz * ky;
-      Mx = fma(mzy, rm, Mx);
-      Kx = fma(kzy, rm, fma(mzy, rk, Kx));
-    }
-  }
-  dM = mzc * myc * mx[1];
-  dK = kzc * myc * mx[1] + mzc * kyc * mx[1] + mzc * myc * kx[1];
-}
-
-// (A x)_i, A_ii for A = a M + b K on a real vector
-template <int DIM, int ORD>
-__device__ __forceinline__ void apply_real(const Grid& g, double ca, double cb, const double* x, const int* c,
-                                           double& Ax, double& D) {
-  double Mx, Kx, dM, dK;
-  if (ORD == 2) {
-    const int cls = (c[1] & 1) | (DIM == 3 ? ((c[2] & 1) << 1) : 0);
-    switch (cls) {
-      case 0: q2_MK_real<DIM, 0, 0>(g, x, c, Mx, Kx, dM, dK); break;
-      case 1: q2_MK_real<DIM, 1, 0>(g, x, c, Mx, Kx, dM, dK); break;
-      case 2: q2_MK_real<DIM, 0, 1>(g, x, c, Mx, Kx, dM, dK); break;
-      default: q2_MK_real<DIM, 1, 1>(g, x, c, Mx, Kx, dM, dK); break;
-    }
-  } else {
-    q1_MK_real<DIM>(g, x, c, Mx, Kx, dM, dK);
-  }
-  Ax = ca * Mx + cb * Kx;
-  D = ca * dM + cb * dK;
-}
-
-template <int DIM, int ORD>
-__device__ __forceinline__ void cta_sweep_real(const Grid& g, double ca, double cb, double* x, const double* b,
-                                               int bs, int sweeps, bool reverse, double omega) {
-  constexpr int C1 = ORD == 2 ? 3 : 2;
-  constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
-  for (int sw = 0; sw < sweeps; ++sw)
-    for (int cc = 0; cc < NC; ++cc) {
-      const int colour = reverse ? NC - 1 - cc : cc;
-      int res[DIM];
-      int col = colour;
-#pragma unroll
-      for (int a = 0; a < DIM; ++a) {
-        res[a] = col % C1;
-        col /= C1;
-      }
-      auto upd = [&](const int* c, int idx) {
-        double Ax, D;
-        apply_real<DIM, ORD>(g, ca, cb, x, c, Ax, D);
-        x[idx] += omega * (b[(long)idx * bs] - Ax) / D;
-      };
-      if (ORD == 2) {
-        for (int cls = 0; cls < (1 << (DIM - 1)); ++cls) {
-          int s0[DIM], st[DIM];
-          s0[0] = res[0];
-          st[0] = 3;
-#pragma unroll
-          for (int a = 1; a < DIM; ++a) {
-            s0[a] = res[a] + 3 * ((cls >> (a - 1)) & 1);
-            st[a] = 6;
-          }
-          cta_visit<DIM>(g.n1, s0, st, 1, g.n1 - 2, threadIdx.x, blockDim.x, upd);
-        }
-      } else {
-        int st[DIM];
-#pragma unroll
-        for (int a = 0; a < DIM; ++a) st[a] = 2;
-        cta_visit<DIM>(g.n1, res, st, 0, g.n1 - 1, threadIdx.x, blockDim.x, [&](const int* c, int idx) {
-          if (idx != 0) upd(c, idx);
-        });
-      }
-      __syncthreads();
-    }
-}
-
-template <int DIM, int ORD>
-__global__ void __launch_bounds__(MG_THREADS, 1) k_mg_real(MGRealArgs a) {
-  extern __shared__ double dsm[];
-  constexpr int R = ORD == 2 ? 3 : 1;
-  constexpr int WR = 2 * R + 1;
-  constexpr int NW = ORD == 2 ? 3 : 2;
-  const int p = blockIdx.x;
-  const int L = a.nlev;
-  const Coef cf = a.op.coef[p / a.op.per_group];
-  const double ca = cf.a.x, cb = cf.b.x;
-  const double* inv = reinterpret_cast<const double*>(a.inv + (long)(p / a.inv_pg) * a.nu * a.nu);  // (re, im) pairs
-  double2* xc0 = a.x0.p + voff(a.x0, p, a.g[0].n);
-  const double2* bc0 = a.b0.p + voff(a.b0, p, a.g[0].n);
-  auto X = [&](int l) -> double* { return a.xsm[l] >= 0 ? dsm + a.xsm[l] : a.xw[l] + (long)p * a.g[l].n; };
-  auto B = [&](int l) -> double* { return a.bsm[l] >= 0 ? dsm + a.bsm[l] : a.bw[l] + (long)p * a.g[l].n; };
-  auto Rr = [&](int l) -> double* { return a.rw[l] + (long)p * a.g[l].n; };
-  for (int part = 0; part < 2; ++part) {
-    const double* b0 = reinterpret_cast<const double*>(bc0) + part;   // stride 2
-    {
-      double* x0 = X(0);
-      for (int i = threadIdx.x; i < (int)a.g[0].n; i += blockDim.x) x0[i] = 0.0;
-    }
-    __syncthreads();
-    for (int cyc = 0; cyc < a.cycles; ++cyc) {
-      for (int l = 0; l < L - 1; ++l) {
-        const Grid g = a.g[l];
-        double* xl = X(l);
-        const double* bl = l == 0 ? b0 : B(l);
-        const int bs = l == 0 ? 2 : 1;
-        if (l > 0) {
-          for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) xl[i] = 0.0;
-          __syncthreads();
-        }
-        cta_sweep_real<DIM, ORD>(g, ca, cb, xl, bl, bs, a.pre, false, a.omega);
-        double* rl = Rr(l);
-        cta_all_unknowns<DIM, ORD>(g.n1, threadIdx.x, blockDim.x, [&](const int* c, int i) {
-          double Ax, D;
-          apply_real<DIM, ORD>(g, ca, cb, xl, c, Ax, D);
-          rl[i] = bl[(long)i * bs] - Ax;
-        });
-        __syncthreads();
-        const Grid gc = a.g[l + 1];
-        const Transfer t = a.t[l];
-        const int o7 = ORD == 2 ? 0 : 2;
-        double* bn = B(l + 1);
-        for (int I = threadIdx.x; I < (int)gc.n; I += blockDim.x) {
-          int c[DIM];
-          coords<DIM>(I, gc.n1, c);
-          if (masked<DIM, ORD>(c, I, gc.n1)) {
-            bn[I] = 0.0;
-            continue;
-          }
-          double w[DIM][WR];
-#pragma unroll
-          for (int d = 0; d < DIM; ++d)
-#pragma unroll
-            for (int o = 0; o < WR; ++o) w[d][o] = __ldg(t.tR + c[d] * 7 + o7 + o);
-          double acc = 0.0;
-          const int n1 = g.n1;
-          if constexpr (DIM == 2) {
-#pragma unroll
-            for (int ob = 0; ob < WR; ++ob) {
-              if (w[1][ob] == 0.0) continue;
-              const double* rrow = rl + (2 * c[1] + ob - R) * n1 + 2 * c[0] - R;
-#pragma unroll
-              for (int oa = 0; oa < WR; ++oa)
-                if (w[0][oa] != 0.0) acc = fma(w[1][ob] * w[0][oa], rrow[oa], acc);
-            }
-          } else {
-            for (int oc = 0; oc < WR; ++oc) {
-              if (w[2][oc] == 0.0) continue;
-              for (int ob = 0; ob < WR; ++ob) {
-                if (w[1][ob] == 0.0) continue;
-                const double* rrow = rl + ((2 * c[2] + oc - R) * n1 + 2 * c[1] + ob - R) * n1 + 2 * c[0] - R;
-#pragma unroll
-                for (int oa = 0; oa < WR; ++oa)
-                  if (w[0][oa] != 0.0) acc = fma(w[2][oc] * w[1][ob] * w[0][oa], rrow[oa], acc);
-              }
-            }
-          }
-          bn[I] = acc;
-        }
-        __syncthreads();
-      }
-      {
-        double* xL = X(L - 1);
-        const double* bL = B(L - 1);
-        for (int i = threadIdx.x; i < (int)a.g[L - 1].n; i += blockDim.x) xL[i] = 0.0;
-        __syncthreads();
-        for (int i = threadIdx.x; i < a.nu; i += blockDim.x) {
-          double acc = 0.0;
-          for (int j = 0; j < a.nu; ++j) acc = fma(inv[2 * ((long)i * a.nu + j)], bL[a.unk[j]], acc);
-          xL[a.unk[i]] = acc;
-        }
-        __syncthreads();
-      }
-      for (int l = L - 2; l >= 0; --l) {
-        const Grid g = a.g[l];
-        const Grid gc = a.g[l + 1];
-        const Transfer t = a.t[l];
-        double* xl = X(l);
-        const double* xcl = X(l + 1);
-        cta_all_unknowns<DIM, ORD>(g.n1, threadIdx.x, blockDim.x, [&](const int* c, int i) {
-          int base[DIM];
-          double w[DIM][NW];
-#pragma unroll
-          for (int d = 0; d < DIM; ++d) {
-            base[d] = (int)__ldg(t.tP + c[d] * 4);
-#pragma unroll
-            for (int o = 0; o < NW; ++o) w[d][o] = __ldg(t.tP + c[d] * 4 + 1 + o);
-          }
-          const int n1 = gc.n1;
-          double acc = 0.0;
-          if constexpr (DIM == 2) {
-#pragma unroll
-            for (int ob = 0; ob < NW; ++ob)
-#pragma unroll
-              for (int oa = 0; oa < NW; ++oa) {
-                const double ww = w[1][ob] * w[0][oa];
-                if (ww != 0.0) acc = fma(ww, xcl[(base[1] + ob) * n1 + base[0] + oa], acc);
-              }
-          } else {
-#pragma unroll
-            for (int oc = 0; oc < NW; ++oc)
-#pragma unroll
-              for (int ob = 0; ob < NW; ++ob)
-#pragma unroll
-                for (int oa = 0; oa < NW; ++oa) {
-                  const double ww = w[2][oc] * w[1][ob] * w[0][oa];
-                  if (ww != 0.0) acc = fma(ww, xcl[((base[2] + oc) * n1 + base[1] + ob) * n1 + base[0] + oa], acc);
-                }
-          }
-          xl[i] += acc;
-        });
-        __syncthreads();
-        cta_sweep_real<DIM, ORD>(g, ca, cb, xl, l == 0 ? b0 : B(l), l == 0 ? 2 : 1, a.post, true, a.omega);
-      }
-    }
-    // write this component of the solution (masked entries are 0 in x)
-    {
-      const double* x0 = X(0);
-      double* out = reinterpret_cast<double*>(xc0) + part;
-      for (int i = threadIdx.x; i < (int)a.g[0].n; i += blockDim.x) out[2L * i] = x0[i];
-    }
-    __syncthreads();
-  }
 }
 
 // ---------------------------------------------------------------- launchers
@@ -2348,18 +1619,7 @@ static void mgcta_t(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
     }
     attr = true;
   }
-  static bool attr2 = false;
-  if (ORD == 2 && !attr2) {
-    cudaFuncSetAttribute(k_mg_q2p<DIM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_mg_q2p<DIM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr2 = true;
-  }
-  if (ORD == 2 && a.use_ctab && a.perm) {
-    if (a.op.conv_sel != 0)
-      k_mg_q2p<DIM, true><<<nprob, MG_THREADS_TAB, smem, s>>>(a);
-    else
-      k_mg_q2p<DIM, false><<<nprob, MG_THREADS_TAB, smem, s>>>(a);
-  } else if (a.op.conv_sel != 0 && ORD == 2 && a.use_ctab)
+  if (a.op.conv_sel != 0 && ORD == 2 && a.use_ctab)
     k_mg_cta<DIM, ORD, true, (ORD == 2)><<<nprob, mg_threads<DIM, true>(), smem, s>>>(a);
   else if (a.op.conv_sel != 0)
     k_mg_cta<DIM, ORD, true, false><<<nprob, mg_threads<DIM, false>(), smem, s>>>(a);
@@ -2380,19 +1640,6 @@ static void chcta_t(const Grid& g, View b, View x, double2* r, double2* d0, doub
 void launch_cheb_cta(const Grid& g, View b, View x, double2* r, double2* d0, double2* d1, double theta, double sigma,
                      double delta, int iters, double scale, int nprob, cudaStream_t s) {
   SWITCH_DO(g, chcta_t, g, b, x, r, d0, d1, theta, sigma, delta, iters, scale, nprob, s);
-}
-
-template <int DIM, int ORD>
-static void mgreal_t(const MGRealArgs& a, int nprob, size_t smem, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_mg_real<DIM, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    attr = true;
-  }
-  k_mg_real<DIM, ORD><<<nprob, MG_THREADS, smem, s>>>(a);
-}
-void launch_mg_real(const MGRealArgs& a, int nprob, size_t smem, cudaStream_t s) {
-  SWITCH_DO(a.g[0], mgreal_t, a, nprob, smem, s);
 }
 
 void launch_Bv(const Grid& g2, const Grid& g1, const double* tPm, const double* tGm, View v, View bp, View out,

@@ -379,116 +379,10 @@ struct KKTTab {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-// velocity rows: half 0  y1v_t = M(tau v_t + lam_t - lam_{t+1}) + tau L^T lam_t + tau B^T mu_t
-//                half 1  y2v_t = M(v_t - v_{t-1} - tau/beta lam_t) + tau L v_t + tau B^T p_t
-// (eq. FinalA expanded block-row by block-row, with E (x) M = backward-Euler difference)
-template <int DIM>
-__global__ void k_kkt_vel(Geo G, KKTTab T, const double* __restrict__ x, double* __restrict__ y, int oseen) {
-  const long col = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= G.n_v) return;
-  const int row = blockIdx.y;  // h * n_b + t
-  const int h = row / G.n_b, t = row % G.n_b;
-  const long comp = col / G.n_s, node = col % G.n_s;
-  const int n1 = G.n1q2;
-  int c[3];
-  c[0] = (int)(node % n1);
-  c[1] = (int)((node / n1) % n1);
-  c[2] = DIM == 3 ? (int)(node / ((long)n1 * n1)) : 0;
-  double* yo = y + (long)row * G.nblk + col;
-  bool interior = true;
-  for (int a = 0; a < DIM; ++a) interior = interior && c[a] > 0 && c[a] < n1 - 1;
-  if (!interior) {
-    *yo = 0.0;
-    return;
-  }
-  const long nblk = G.nblk, n_b = G.n_b;
-  const double tau = G.tau;
-  // slices (all at component comp): A = the M-combined input, Bk = the L-input
-  const double* xv = x + (long)t * nblk + comp * G.n_s;                    // v_t
-  const double* xl = x + (long)(n_b + t) * nblk + comp * G.n_s;            // lam_t
-  const double* xo = nullptr;                                              // lam_{t+1} or v_{t-1}
-  double cA, cB, cO;  // w = cA*v_t + cB*lam_t + cO*other
-  const double* xL;   // operand of L (or L^T)
-  if (h == 0) {
-    cA = tau; cB = 1.0; cO = -1.0;
-    if (t + 1 < n_b) xo = x + (long)(n_b + t + 1) * nblk + comp * G.n_s;
-    xL = xl;
-  } else {
-    cA = 1.0; cB = -tau / G.beta; cO = -1.0;
-    if (t >= 1) xo = x + (long)(t - 1) * nblk + comp * G.n_s;
-    xL = xv;
-  }
-  double m[DIM][5], k[DIM][5];
-  for (int a = 0; a < DIM; ++a)
-    for (int o = 0; o < 5; ++o) {
-      m[a][o] = __ldg(T.tM + c[a] * 5 + o);
-      k[a][o] = __ldg(T.tK + c[a] * 5 + o);
-    }
-  const double* cv = oseen ? ((h == 0 ? T.convT : T.conv) + node * (DIM == 2 ? 25 : 125)) : nullptr;
-  double Mw = 0, KL = 0, CL = 0;
-  const int nz = DIM == 3 ? 5 : 1;
-  for (int oc = 0; oc < nz; ++oc) {
-    const int kk = DIM == 3 ? clampi(c[2] + oc - 2, 0, n1 - 1) : 0;
-    const double mz = DIM == 3 ? m[DIM == 3 ? 2 : 0][oc] : 1.0;
-    const double kz = DIM == 3 ? k[DIM == 3 ? 2 : 0][oc] : 0.0;
-    for (int ob = 0; ob < 5; ++ob) {
-      const int jj = clampi(c[1] + ob - 2, 0, n1 - 1);
-      const double mzy = mz * m[1][ob];
-      const double kzy = kz * m[1][ob] + mz * k[1][ob];
-#pragma unroll
-      for (int oa = 0; oa < 5; ++oa) {
-        const int ii = clampi(c[0] + oa - 2, 0, n1 - 1);
-        const long nb = ((long)kk * n1 + jj) * n1 + ii;
-        const double mm = mzy * m[0][oa];
-        const double kc = kzy * m[0][oa] + mzy * k[0][oa];
-        double w = cA * __ldg(xv + nb) + cB * __ldg(xl + nb);
-        if (xo) w += cO * __ldg(xo + nb);
-        Mw = fma(mm, w, Mw);
-        const double uL = __ldg(xL + nb);
-        KL = fma(kc, uL, KL);
-        if (oseen) CL = fma(__ldg(cv + (oc * 5 + ob) * 5 + oa), uL, CL);
-      }
-    }
-  }
-  // B^T q: q = mu_t (half 0) or p_t (half 1); B_c = -(prod of Pm, with Gm on axis c), pinned node skipped
-  const double* q = x + (long)(h == 0 ? (n_b + t) : t) * nblk + G.n_v;
-  double P[DIM][3], Gd[DIM][3];
-  int I0[DIM];
-  for (int a = 0; a < DIM; ++a) {
-    I0[a] = (c[a] - 1 >= 0) ? (c[a] - 1) / 2 : -1;
-    for (int o = 0; o < 3; ++o) {
-      P[a][o] = __ldg(T.tPmT + c[a] * 3 + o);
-      Gd[a][o] = __ldg(T.tGmT + c[a] * 3 + o);
-    }
-  }
-  const int m1 = G.n1q1;
-  double BTq = 0;
-  for (int oc = 0; oc < (DIM == 3 ? 3 : 1); ++oc) {
-    double fz = 1.0;
-    int Kz = 0;
-    if (DIM == 3) {
-      fz = (comp == 2 ? Gd[2][oc] : P[2][oc]);
-      Kz = I0[2] + oc;
-      if (fz == 0.0 || Kz < 0 || Kz >= m1) continue;
-    }
-    for (int ob = 0; ob < 3; ++ob) {
-      const double fy = (comp == 1 ? Gd[1][ob] : P[1][ob]);
-      const int J = I0[1] + ob;
-      if (fy == 0.0 || J < 0 || J >= m1) continue;
-      for (int oa = 0; oa < 3; ++oa) {
-        const double fx = (comp == 0 ? Gd[0][oa] : P[0][oa]);
-        const int I = I0[0] + oa;
-        if (fx == 0.0 || I < 0 || I >= m1) continue;
-        const long pn = ((long)Kz * m1 + J) * m1 + I;
-        if (pn == 0) continue;  // pinned pressure node: eliminated column
-        BTq = fma(-fz * fy * fx, __ldg(q + pn), BTq);
-      }
-    }
-  }
-  *yo = Mw + tau * (G.nu * KL + CL) + tau * BTq;
-}
-
-// Tiled version of the velocity rows (same formulas).  A CTA owns a TX x TY (x TZ) tile of one
+// Velocity rows of eq. (FinalA) expanded block-row by block-row (E (x) M = backward-Euler difference):
+//   half 0  y1v_t = M(tau v_t + lam_t - lam_{t+1}) + tau L^T lam_t + tau B^T mu_t
+//   half 1  y2v_t = M(v_t - v_{t-1} - tau/beta lam_t) + tau L v_t + tau B^T p_t
+// (used for Oseen and as the fallback of the time-marching kernels).  A CTA owns a TX x TY (x TZ) tile of one
 // (half, t, component) slice; it forms the mass operand w = cA v_t + cB lam_t + cO other and the
 // L-operand u once per node of the tile + 2-halo in shared memory (masked / outside nodes = 0,
 // which is exactly the elimination), plus the pressure tile for B^T.
@@ -1022,25 +916,15 @@ void launch_kkt(const Ctx& c, const double* x, double* y, cudaStream_t s) {
   T.tPm = c.tPm;
   T.tGm = c.tGm;
   const Geo G = geo_of(c);
-  dim3 gv((unsigned)((c.n_v + 127) / 128), 2 * c.n_b);
   dim3 gp((unsigned)((c.n_p + 127) / 128), 2 * c.n_b);
-  static const bool untiled = std::getenv("AAO_KKT_UNTILED") != nullptr;
   if (c.dim == 2) {
-    if (untiled) {
-      k_kkt_vel<2><<<gv, 128, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0);
-    } else {
-      const int tx = (c.n1q2 + KT<2>::TX - 1) / KT<2>::TX, ty = (c.n1q2 + KT<2>::TY - 1) / KT<2>::TY;
-      k_kkt_vel_tiled<2><<<dim3(tx * ty, 2 * c.n_b, 2), 256, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0, tx, ty);
-    }
+    const int tx = (c.n1q2 + KT<2>::TX - 1) / KT<2>::TX, ty = (c.n1q2 + KT<2>::TY - 1) / KT<2>::TY;
+    k_kkt_vel_tiled<2><<<dim3(tx * ty, 2 * c.n_b, 2), 256, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0, tx, ty);
     k_kkt_pres<2><<<gp, 128, 0, s>>>(G, T, x, y);
   } else {
-    if (untiled) {
-      k_kkt_vel<3><<<gv, 128, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0);
-    } else {
-      const int tx = (c.n1q2 + KT<3>::TX - 1) / KT<3>::TX, ty = (c.n1q2 + KT<3>::TY - 1) / KT<3>::TY;
-      const int tz = (c.n1q2 + KT<3>::TZ - 1) / KT<3>::TZ;
-      k_kkt_vel_tiled<3><<<dim3(tx * ty * tz, 2 * c.n_b, 3), 256, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0, tx, ty);
-    }
+    const int tx = (c.n1q2 + KT<3>::TX - 1) / KT<3>::TX, ty = (c.n1q2 + KT<3>::TY - 1) / KT<3>::TY;
+    const int tz = (c.n1q2 + KT<3>::TZ - 1) / KT<3>::TZ;
+    k_kkt_vel_tiled<3><<<dim3(tx * ty * tz, 2 * c.n_b, 3), 256, 0, s>>>(G, T, x, y, c.oseen ? 1 : 0, tx, ty);
     k_kkt_pres<3><<<gp, 128, 0, s>>>(G, T, x, y);
   }
 }

@@ -31,7 +31,13 @@ CASES = {
     "nl_stokes_small": synth.small_config("nl_stokes_small", 2, 8, 10, beta=1e-2, nu=1e-2, index=1),
     "nl_oseen_small": synth.small_config("nl_oseen_small", 2, 8, 8, problem="oseen", lo=-1.0, hi=1.0,
                                          beta=1e-3, nu=1.0 / 20.0, index=3),
+    # full-size BASELINE configs (round 2): c4 at n_t = 32 in the linear mode; c3 and c5, where linear
+    # GMRES(30) stagnates (reading 16 / risk H7), with Algorithm 2 + FGMRES(10)
+    "c4_32": synth.CONFIGS["c4_32"],
+    "nl_c3": synth.CONFIGS["c3"],
+    "nl_c5": synth.CONFIGS["c5"],
 }
+WORKERS = int(os.environ.get("ORACLE_WORKERS", "1"))   # processes over the frequency blocks (same arithmetic)
 
 
 def run(name):
@@ -40,14 +46,23 @@ def run(name):
     prob = Problem(cfg, synth.wind(cfg))
     b = kkt.build_rhs(prob, synth.desired_state(cfg))
     if name.startswith("nl_"):
-        pc = OracleNonlinearPreconditioner(prob, inner_eps=1e-2, inner_maxit=60)
-        x, hist, info = fgmres(lambda v: kkt.kkt_apply(prob, v), pc.apply, b, tol=1e-6, restart=10)
+        pc = OracleNonlinearPreconditioner(prob, inner_eps=1e-2, inner_maxit=60, cache_blocks=False, workers=WORKERS)
+        inner = []
+
+        def apply_P(v):
+            z = pc.apply(v)
+            inner.append([int(pc.last_inner[k]) for k in range(prob.n_b // 2 + 1)])
+            print(f"  {name}: precond {len(inner)} inner {inner[-1]} {time.time() - t0:.0f}s", flush=True)
+            return z
+        x, hist, info = fgmres(lambda v: kkt.kkt_apply(prob, v), apply_P, b, tol=1e-6, restart=10)
+        info["inner"] = inner
     else:
-        pc = precond.OraclePreconditioner(prob)
+        pc = precond.OraclePreconditioner(prob, cache_blocks=False if WORKERS > 1 else None, workers=WORKERS)
         x, hist, info = gmres.gmres(lambda v: kkt.kkt_apply(prob, v), pc.apply, b, tol=1e-6, restart=30)
     out = dict(case=name, config=cfg.__dict__, iterations=info["iterations"], restarts=info["restarts"],
                converged=info["converged"], true_relres=[float(v) for v in info["true_relres"]],
-               hist=[float(h) for h in hist], oracle_seconds=time.time() - t0,
+               hist=[float(h) for h in hist], oracle_seconds=time.time() - t0, oracle_workers=WORKERS,
+               inner_per_apply=info.get("inner"),
                generator="tests/golden/gen_oracle_refs.py (oracle only)")
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"gmres_{name}.json")
     with open(path, "w") as f:

@@ -167,3 +167,27 @@ def test_dof_counts_match_baseline_json():
         c = synth.CONFIGS[name]
         assert (c.n_v, c.n_p) == (nv, npr)
     assert synth.CONFIGS["c2"].n_dofs == 4725882          # = paper's 4.73e6 row (h_f, n_t = 63)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_pressure_convection_closed_form(dim):
+    """N_p (P:241, C.2 #9) against a closed form: for a bilinear (Q1) wind w and the coordinate functions
+    x_a (in Q1), int psi_i (w . grad x_a) = int psi_i w_a, i.e. N_p x_a = M_p w_a (exact); N_p 1 = 0.
+    Pins the scale, sign and quadrature of conv_q1 (a dropped h-power or a factor on N_p fails)."""
+    n = 4 if dim == 2 else 2
+    L = fem.Level(dim, n, -1.0, 1.0)
+    X2, X1 = _q2_xyz(L), _q1_xyz(L)
+    lin = lambda X, a: 0.3 + 0.7 * X[0] - 0.4 * X[dim - 1] + (0.9 + a) * X[0] * X[dim - 1]
+    w = np.stack([lin(X2, a) for a in range(dim)])              # Q2 nodal values of a Q1 field
+    wp = np.stack([lin(X1, a) for a in range(dim)])             # the same field at the Q1 nodes
+    Np, Mp = L.conv_q1(w), L.mass_q1()
+    for a in range(dim):
+        np.testing.assert_allclose(Np @ X1[a], Mp @ wp[a], atol=1e-13)
+    assert np.abs(Np @ np.ones(L.n_p)).max() < 1e-13
+    # Galerkin identity for the pressure convection on the eliminated spaces (coarse wind = injection)
+    Lc = fem.Level(dim, n // 2, -1.0, 1.0)
+    wc = fem.inject_wind(w, dim, n)
+    P1 = transfer.prolongation(dim, n // 2, 1, L.q1_unknowns(), Lc.q1_unknowns())
+    Nf = fem.restrict(Np, L.q1_unknowns(), L.q1_unknowns())
+    Nc = fem.restrict(Lc.conv_q1(wc), Lc.q1_unknowns(), Lc.q1_unknowns())
+    assert np.abs((P1.T @ Nf @ P1 - Nc).toarray()).max() <= 1e-13 * np.abs(Nc.toarray()).max()

@@ -88,3 +88,43 @@ def test_fgmres_with_nonlinear_preconditioner_converges_fast(problem):
     lin = precond.OraclePreconditioner(prob)
     _, _, info_lin = gmres.gmres(lambda v: kkt.kkt_apply(prob, v), lin.apply, b, tol=1e-6, restart=30)
     assert info["iterations"] < info_lin["iterations"]
+
+
+def test_Pt_apply_equals_dense_blockdiag_with_exact_inner_solves():
+    """Pt_apply (Algorithm 2's inner preconditioner P~_j^{-1}) with exact inner solves equals the
+    dense blkdiag(W, W, S~, S~)^{-1}, W = (1 + c1) M + c2 L, S~^{-1} = (1 + c1) K_p^{-1} + nu c2 M_p^{-1}
+    (P:424), built here from dense_ops' spatial matrices; and with the multigrid inner solves it is the
+    Algorithm-1 block between the T transforms: T_r^{-1} Pt_apply(T_l^{-1} r) = stokes_block(r)."""
+    prob = make("stokes", n=2, n_t=6)
+    pc = OracleNonlinearPreconditioner(prob)
+    s = dense_ops.spatial(prob)
+    rng = np.random.default_rng(9)
+    nI, npu = prob.fine.nI, prob.fine.npu
+    S = (rng.standard_normal((prob.dim, nI)) + 1j * rng.standard_normal((prob.dim, nI)),
+         rng.standard_normal((prob.dim, nI)) + 1j * rng.standard_normal((prob.dim, nI)),
+         rng.standard_normal(npu) + 1j * rng.standard_normal(npu),
+         rng.standard_normal(npu) + 1j * rng.standard_normal(npu))
+    for k in (1, 2):
+        # multigrid inner solves: consistency with the (pinned) Algorithm-1 Stokes block
+        d = pc.d[k]
+        sl = pc.tl_inv(d, prob.tau, prob.beta, *S)
+        got = pc.tr_inv(d, prob.tau, prob.beta, *pc.Pt_apply(k, sl))
+        ref = pc.stokes_block(k, *S)
+        for g_, r_ in zip(got, ref):
+            np.testing.assert_allclose(g_, r_, atol=1e-13 * np.abs(r_).max())
+    # exact inner solves
+    pe = OracleNonlinearPreconditioner(prob)
+    Ms, Ks = prob.fine.Ms.toarray(), prob.nu * prob.fine.Ks.toarray()
+    for k in (1, 2):
+        c1, c2 = timeops.stokes_constants(pe.d[k], prob.tau, prob.beta)
+        Wk = (1.0 + c1) * Ms + c2 * Ks
+        pe.W_solver = lambda kk, Wk=Wk: dense_ops.DenseSolve(Wk)
+        pe.Kp_solver = lambda: dense_ops.DenseSolve(s["Kp"])
+        pe.Mp_solver = lambda: dense_ops.DenseSolve(s["Mp"])
+        got = pe.Pt_apply(k, S)
+        Wd = (1.0 + c1) * s["M"] + c2 * s["L"]
+        Sinv = (1.0 + c1) * np.linalg.inv(s["Kp"]) + prob.nu * c2 * np.linalg.inv(s["Mp"])
+        ref = (np.linalg.solve(Wd, S[0].reshape(-1)).reshape(prob.dim, -1),
+               np.linalg.solve(Wd, S[1].reshape(-1)).reshape(prob.dim, -1), Sinv @ S[2], Sinv @ S[3])
+        for g_, r_ in zip(got, ref):
+            np.testing.assert_allclose(g_, r_, atol=1e-11 * np.abs(r_).max())

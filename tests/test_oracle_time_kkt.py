@@ -129,3 +129,20 @@ def test_exact_solve_divergence_free_and_zero_data(tiny):
     assert np.abs(np.linalg.solve(A, np.zeros(A.shape[0]))).max() == 0.0
     # the RHS touches only the adjoint-velocity rows (v0 = f = 0)
     assert np.abs(Pb).max() == 0.0 and np.abs(Vb[1]).max() == 0.0
+
+
+@pytest.mark.parametrize("problem", ["stokes", "oseen"])
+def test_build_rhs_equals_general_rhs_with_constant_data(problem):
+    """kkt.build_rhs (C.1 O5) is the time-constant, zero-forcing, homogeneous-Dirichlet case of
+    manufactured.rhs_with_data, which is pinned by the manufactured-solution convergence test
+    (tests/test_oracle_gmres_mms.py): every row must agree, so a wrong factor on tau M v_d fails."""
+    from oracle import manufactured
+    lo, hi = (-1.0, 1.0) if problem == "oseen" else (0.0, 1.0)
+    cfg = synth.small_config("rhs", 2, 4, 7, problem=problem, lo=lo, hi=hi, beta=1e-2, nu=0.05)
+    w = synth.wind(cfg)
+    prob = Problem(cfg, w)
+    vd = np.random.default_rng(8).standard_normal((cfg.dim, prob.n_s))
+    b = kkt.build_rhs(prob, vd)
+    ref = manufactured.rhs_with_data(prob, np.repeat(vd[None], prob.n_b, axis=0), None, None, None, wind=w)
+    np.testing.assert_allclose(b, ref, rtol=0, atol=1e-15 * np.abs(ref).max())
+    assert np.abs(ref).max() > 0
