@@ -320,6 +320,241 @@ __global__ void __launch_bounds__(256) k_fft_inv_sym(Geo G, InvSrc S, double* __
   }
 }
 
+// ------------------------------------------------------------------ prime-factor (Good-Thomas) transforms
+// n_b = P Q with gcd(P, Q) = 1 (511 = 7 x 73, 255 = 15 x 17, 63 = 7 x 9, 15 = 3 x 5): the DFT of P:332-344,
+//   r_hat_k = sum_t r_t omega^{k t},  omega = exp(-2 pi i / n_b),
+// is evaluated exactly (up to rounding order) as a 2-D DFT through the index maps
+//   t = (Q t1 + P t2) mod n_b,   k = (k1 Q (Q^-1 mod P) + k2 P (P^-1 mod Q)) mod n_b,
+// for which omega^{k t} = omega_P^{k1 t1} omega_Q^{k2 t2} (no twiddle factors):
+//   stage A: Y[t1][k2] = sum_t2 r[t(t1, t2)] omega_Q^{k2 t2}   (real input: k2 <= (Q-1)/2, pair sums/differences)
+//   stage B: X[k1][k2] = sum_t1 Y[t1][k2] omega_P^{k1 t1}
+// and the Hermitian half X[n_b - k] = conj(X[k]) covers every k < n_f.  Work per series ~ n_b (Q/2 + P) multiply-
+// adds instead of the dense sum's ~n_b^2/2 (c4 at n_t = 512: 43 n_b vs 255 n_b).
+// Thread layout: a CTA owns 16 spatial columns x 2 halves = 32 series (lane = column + 16 half, warp w = t1 for
+// stage A); every thread loads its Q inputs straight from global memory (rows t(t1, .) of its column: 2 x 128-byte
+// segments per warp load), keeps the pair sums in registers, and exchanges Y through shared memory in blocks of P
+// values of k2.  T_l^{-1} (Stokes) is applied at the store; the halves meet by a lane shuffle.
+template <int P, int Q>
+struct Pfa {
+  static constexpr int HQ = (Q - 1) / 2;           // pairs t2, Q - t2
+  static constexpr int NK2 = HQ + 1;               // k2 = 0..HQ
+  static constexpr int KB = P < NK2 ? P : NK2;     // k2 per block (one per warp in stage B)
+  static constexpr int NBLK = (NK2 + KB - 1) / KB;
+  static constexpr int THREADS = 32 * P;
+};
+
+struct PfaMap {
+  int QA, PB;   // Q (Q^-1 mod P), P (P^-1 mod Q)
+};
+
+__device__ __forceinline__ double2 cj(double2 a) { return make_double2(a.x, -a.y); }
+
+// T_l^{-1} of one column at frequency k with the two halves (s0: half 0, s1: half 1); returns half h
+__device__ __forceinline__ double2 tl_inv_half(const Geo& G, const FreqConst& f, long col, double2 s0, double2 s1,
+                                               int stokes, int h) {
+  if (!stokes) return h ? s1 : s0;
+  const double st = sqrt(G.tau);
+  if (col < G.n_v) {
+    const double2 q1 = make_double2(s0.x / st, s0.y / st);
+    if (h == 0) return q1;
+    const double a = f.dc / st, g = f.c2 / st;
+    return make_double2((s1.x + a * q1.y) * g, (s1.y - a * q1.x) * g);
+  }
+  const double den = st * f.c2;
+  const double2 q3 = make_double2(s0.x / den, s0.y / den);
+  if (h == 0) return q3;
+  const double a = f.dc * f.c2 / st;
+  return make_double2((s1.x + a * q3.y) / st, (s1.y - a * q3.x) / st);
+}
+
+template <int P, int Q>
+__global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_fwd_pfa(Geo G, const double* __restrict__ r,
+                                                                    double2* __restrict__ Fv, double2* __restrict__ Fp,
+                                                                    const FreqConst* __restrict__ fc,
+                                                                    const double2* __restrict__ tw, PfaMap mp,
+                                                                    int stokes) {
+  using PF = Pfa<P, Q>;
+  constexpr int n = P * Q;
+  extern __shared__ double2 pfa_sm[];    // twQ[Q], twP[P], Ys[KB][P][32] ([k2 - block start][t1][series])
+  double2* twQ = pfa_sm;
+  double2* twP = twQ + Q;
+  double2 (*Ys)[P][32] = reinterpret_cast<double2 (*)[P][32]>(twP + P);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int h = lane >> 4;
+  const long col = (long)blockIdx.x * 16 + (lane & 15);
+  for (int m = threadIdx.x; m < Q; m += PF::THREADS) twQ[m] = tw[m * P];   // exp(-2 pi i m / Q) = tw[m P]
+  for (int m = threadIdx.x; m < P; m += PF::THREADS) twP[m] = tw[m * Q];
+  const bool valid = col < G.nblk;
+  const bool msk = !valid || col_masked(G, col);
+  // stage A inputs of series (col, h), t1 = w: y[t2] = r[h][t(w, t2)][col]; pair sums / differences in registers
+  const double* rc = r + (long)h * n * G.nblk + col;
+  double ps[PF::HQ], pd[PF::HQ];
+  auto ld = [&](int t2) { return msk ? 0.0 : __ldg(rc + (long)((Q * w + P * t2) % n) * G.nblk); };
+  const double y0 = ld(0);
+#pragma unroll
+  for (int j = 0; j < PF::HQ; ++j) {
+    const double a = ld(1 + j), b = ld(Q - 1 - j);
+    ps[j] = a + b;
+    pd[j] = a - b;
+  }
+  __syncthreads();
+  for (int blk = 0; blk < PF::NBLK; ++blk) {
+    // stage A: Y[w][k2] for the KB values k2 = blk KB + i:  Re = y0 + sum ps cos, Im = -sum pd sin
+    for (int i = 0; i < PF::KB; ++i) {
+      const int k2 = blk * PF::KB + i;
+      if (k2 > PF::HQ) break;
+      double re = y0, im = 0.0;
+      int m = 0;
+#pragma unroll
+      for (int j = 0; j < PF::HQ; ++j) {
+        m += k2;
+        if (m >= Q) m -= Q;
+        const double2 wq = twQ[m];     // (cos, sin)(2 pi k2 (j + 1) / Q); warp-uniform
+        re = fma(ps[j], wq.x, re);
+        im = fma(-pd[j], wq.y, im);
+      }
+      Ys[i][w][lane] = make_double2(re, im);
+    }
+    __syncthreads();
+    // stage B for k2 = blk KB + w: X[k1] = sum_t1 Y[t1] omega_P^{k1 t1}, k1 = 0..P-1; then T_l^{-1} and the store
+    const int k2 = blk * PF::KB + w;
+    if (w < PF::KB && k2 <= PF::HQ) {
+      double2 yv[P];
+#pragma unroll
+      for (int t1 = 0; t1 < P; ++t1) yv[t1] = Ys[w][t1][lane];
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) {
+        double2 x = yv[0];
+#pragma unroll
+        for (int t1 = 1; t1 < P; ++t1) {
+          const double2 wp = twP[(k1 * t1) % P];   // exp(-2 pi i k1 t1 / P) = (cos, -sin)
+          x.x += yv[t1].x * wp.x + yv[t1].y * wp.y;
+          x.y += yv[t1].y * wp.x - yv[t1].x * wp.y;
+        }
+        int k = (k1 * mp.QA + k2 * mp.PB) % n;
+        bool cjg = false;
+        if (k >= G.n_f) {               // X[n - k] = conj(X[k]); k2 = 0 entries above n_f are their own mirror
+          if (k2 == 0) continue;
+          k = n - k;
+          cjg = true;
+        }
+        if (cjg) x = cj(x);
+        double2 other;
+        other.x = __shfl_xor_sync(0xffffffffu, x.x, 16);
+        other.y = __shfl_xor_sync(0xffffffffu, x.y, 16);
+        if (!valid) continue;
+        const double2 s0 = h ? other : x, s1 = h ? x : other;
+        const double2 out = tl_inv_half(G, fc[k], col, s0, s1, stokes, h);
+        if (col < G.n_v) {
+          const long comp = col / G.n_s, node = col % G.n_s;
+          Fv[(((long)k * 2 + h) * G.dim + comp) * G.n_s + node] = out;
+        } else {
+          Fp[((long)k * 2 + h) * G.n_p + (col - G.n_v)] = out;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Inverse (step A8): y_t = (1/n_b) sum_k y_hat_k omega^{-k t} with y_hat_{n_b - k} = conj(y_hat_k), through the same
+// maps:  Z[t1][k2] = sum_k1 Yh[k1][k2] omega_P^{-k1 t1}  (k2 <= HQ; Yh gathered from the half spectrum after
+// T_r^{-1}),  y[t1][t2] = (1/n_b) [Z[t1][0] + 2 sum_{k2 >= 1} Re(Z[t1][k2] omega_Q^{-k2 t2})]  (pairs t2, Q - t2).
+template <int P, int Q>
+__global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_inv_pfa(Geo G, InvSrc S, double* __restrict__ z,
+                                                                    const FreqConst* __restrict__ fc,
+                                                                    const double2* __restrict__ tw, PfaMap mp) {
+  using PF = Pfa<P, Q>;
+  constexpr int n = P * Q;
+  extern __shared__ double2 pfa_sm[];    // twQ[Q], twP[P], Hs[KB][P][32] (gathered spectrum, [k2][k1][series]),
+  double2* twQ = pfa_sm;                 // Zs[KB][P][32] ([k2][t1][series])
+  double2* twP = twQ + Q;
+  double2 (*Hs)[P][32] = reinterpret_cast<double2 (*)[P][32]>(twP + P);
+  double2 (*Zs)[P][32] = Hs + PF::KB;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int h = lane >> 4;
+  const long col = (long)blockIdx.x * 16 + (lane & 15);
+  for (int m = threadIdx.x; m < Q; m += PF::THREADS) twQ[m] = tw[m * P];
+  for (int m = threadIdx.x; m < P; m += PF::THREADS) twP[m] = tw[m * Q];
+  const bool valid = col < G.nblk;
+  const bool msk = !valid || col_masked(G, col);
+  double a0 = 0.0, s0 = 0.0;            // Z[w][0].re and sum_{k2>=1} Re Z[w][k2] (t2 = 0)
+  double C[PF::HQ], Sn[PF::HQ];
+#pragma unroll
+  for (int j = 0; j < PF::HQ; ++j) C[j] = Sn[j] = 0.0;
+  __syncthreads();
+  for (int blk = 0; blk < PF::NBLK; ++blk) {
+    // gather: Yh[k1][k2] for k2 = blk KB + w (T_r^{-1} applied, both halves read, own half kept)
+    const int k2g = blk * PF::KB + w;
+    const bool mine = w < PF::KB && k2g <= PF::HQ;
+    if (mine) {
+      for (int k1 = 0; k1 < P; ++k1) {
+        int k = (k1 * mp.QA + k2g * mp.PB) % n;
+        bool cjg = false;
+        if (k >= G.n_f) {
+          k = n - k;
+          cjg = true;
+        }
+        double2 v0 = make_double2(0.0, 0.0), v1 = v0;
+        if (!msk) slot_values(G, S, fc[k], k, col, v0, v1);
+        const double2 v = h ? v1 : v0;
+        Hs[w][k1][lane] = cjg ? cj(v) : v;
+      }
+    }
+    __syncthreads();
+    // stage B^-1 for k2 = blk KB + w: Z[t1] = sum_k1 Yh[k1] omega_P^{-k1 t1}
+    if (mine) {
+      double2 hv[P];
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) hv[k1] = Hs[w][k1][lane];
+#pragma unroll
+      for (int t1 = 0; t1 < P; ++t1) {
+        double2 x = hv[0];
+#pragma unroll
+        for (int k1 = 1; k1 < P; ++k1) {
+          const double2 wp = twP[(k1 * t1) % P];   // omega_P^{-k1 t1} = (cos, +sin)
+          x.x += hv[k1].x * wp.x - hv[k1].y * wp.y;
+          x.y += hv[k1].y * wp.x + hv[k1].x * wp.y;
+        }
+        Zs[w][t1][lane] = x;
+      }
+    }
+    __syncthreads();
+    // stage A^-1 partial sums for t1 = w over this block's k2
+    for (int i = 0; i < PF::KB; ++i) {
+      const int k2 = blk * PF::KB + i;
+      if (k2 > PF::HQ) break;
+      const double2 zz = Zs[i][w][lane];
+      if (k2 == 0) {
+        a0 = zz.x;
+        continue;
+      }
+      s0 += zz.x;
+      int m = 0;
+#pragma unroll
+      for (int j = 0; j < PF::HQ; ++j) {
+        m += k2;
+        if (m >= Q) m -= Q;
+        const double2 wq = twQ[m];      // cos, sin of 2 pi k2 (j + 1) / Q
+        C[j] = fma(zz.x, wq.x, C[j]);
+        Sn[j] = fma(zz.y, wq.y, Sn[j]);
+      }
+    }
+    __syncthreads();
+  }
+  if (!valid) return;
+  const double inv_n = 1.0 / n;
+  double* zc = z + (long)h * n * G.nblk + col;
+  zc[(long)((Q * w) % n) * G.nblk] = msk ? 0.0 : (a0 + 2.0 * s0) * inv_n;
+#pragma unroll
+  for (int j = 0; j < PF::HQ; ++j) {
+    const int t2 = j + 1;
+    const int ta = (Q * w + P * t2) % n, tb = (Q * w + P * (Q - t2)) % n;
+    zc[(long)ta * G.nblk] = msk ? 0.0 : (a0 + 2.0 * (C[j] - Sn[j])) * inv_n;
+    zc[(long)tb * G.nblk] = msk ? 0.0 : (a0 + 2.0 * (C[j] + Sn[j])) * inv_n;
+  }
+}
+
 // ------------------------------------------------------------------ inverse transform
 __global__ void k_fft_inv(Geo G, InvSrc S, double* __restrict__ z, const FreqConst* __restrict__ fc,
                           const double2* __restrict__ tw, int TD) {
@@ -835,7 +1070,74 @@ void launch_inv_sym(const Ctx& c, const InvSrc& S, double* z, cudaStream_t s) {
 }
 }  // namespace
 
+// prime-factor plan n_b = P Q (gcd 1) for the instantiated pairs; false: the dense symmetric kernels
+static bool pfa_plan(int n_b, int* P, int* Q, PfaMap* mp) {
+  static const int pairs[][2] = {{7, 73}, {15, 17}, {7, 9}, {3, 5}};
+  for (auto& pq : pairs) {
+    if (pq[0] * pq[1] != n_b) continue;
+    *P = pq[0];
+    *Q = pq[1];
+    int a = 1, b = 1;
+    while ((pq[1] * a) % pq[0] != 1) ++a;   // Q^-1 mod P
+    while ((pq[0] * b) % pq[1] != 1) ++b;   // P^-1 mod Q
+    mp->QA = pq[1] * a;
+    mp->PB = pq[0] * b;
+    return true;
+  }
+  return false;
+}
+static bool pfa_off() {
+  static const bool off = std::getenv("AAO_FFT_DENSE") != nullptr;
+  return off;
+}
+template <int P, int Q>
+static void fwd_pfa_t(const Ctx& c, const double* r, PfaMap mp, cudaStream_t s) {
+  const size_t sm = (Q + P + (size_t)Pfa<P, Q>::KB * P * 32) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fft_fwd_pfa<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  k_fft_fwd_pfa<P, Q><<<(unsigned)((c.nblk + 15) / 16), Pfa<P, Q>::THREADS, sm, s>>>(geo_of(c), r, c.Fv, c.Fp, c.fc,
+                                                                                      c.tw, mp, c.oseen ? 0 : 1);
+}
+template <int P, int Q>
+static void inv_pfa_t(const Ctx& c, const InvSrc& S, double* z, PfaMap mp, cudaStream_t s) {
+  const size_t sm = (Q + P + 2 * (size_t)Pfa<P, Q>::KB * P * 32) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_fft_inv_pfa<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    attr = true;
+  }
+  k_fft_inv_pfa<P, Q><<<(unsigned)((c.nblk + 15) / 16), Pfa<P, Q>::THREADS, sm, s>>>(geo_of(c), S, z, c.fc, c.tw, mp);
+}
+static bool launch_pfa_fwd(const Ctx& c, const double* r, cudaStream_t s) {
+  int P, Q;
+  PfaMap mp;
+  if (pfa_off() || !pfa_plan(c.n_b, &P, &Q, &mp)) return false;
+  switch (P * 1000 + Q) {
+    case 7073: fwd_pfa_t<7, 73>(c, r, mp, s); break;
+    case 15017: fwd_pfa_t<15, 17>(c, r, mp, s); break;
+    case 7009: fwd_pfa_t<7, 9>(c, r, mp, s); break;
+    default: fwd_pfa_t<3, 5>(c, r, mp, s); break;
+  }
+  return true;
+}
+static bool launch_pfa_inv(const Ctx& c, const InvSrc& S, double* z, cudaStream_t s) {
+  int P, Q;
+  PfaMap mp;
+  if (pfa_off() || !pfa_plan(c.n_b, &P, &Q, &mp)) return false;
+  switch (P * 1000 + Q) {
+    case 7073: inv_pfa_t<7, 73>(c, S, z, mp, s); break;
+    case 15017: inv_pfa_t<15, 17>(c, S, z, mp, s); break;
+    case 7009: inv_pfa_t<7, 9>(c, S, z, mp, s); break;
+    default: inv_pfa_t<3, 5>(c, S, z, mp, s); break;
+  }
+  return true;
+}
+
 void launch_fft_fwd(const Ctx& c, const double* r, cudaStream_t s) {
+  if (launch_pfa_fwd(c, r, s)) return;
   size_t sf, si;
   const int TD = tile_width(c.n_b, c.n_f, &sf, &si);
   dim3 blk(TD, 256 / TD);
@@ -860,6 +1162,7 @@ void launch_fft_fwd(const Ctx& c, const double* r, cudaStream_t s) {
 }
 
 void launch_fft_inv(const Ctx& c, double* z, cudaStream_t s) {
+  if (launch_pfa_inv(c, src_of(c), z, s)) return;
   if (!dense_fft(c)) {
     launch_inv_sym(c, src_of(c), z, s);
     return;
@@ -892,6 +1195,7 @@ void launch_debug_block(const Ctx& c, int k, double2* out, cudaStream_t s) {
 }
 
 void launch_fft_inv_from(const Ctx& c, FVec x, double* z, cudaStream_t s) {
+  if (launch_pfa_inv(c, src_of_fvec(c, x), z, s)) return;
   if (!dense_fft(c)) {
     launch_inv_sym(c, src_of_fvec(c, x), z, s);
     return;

@@ -448,3 +448,15 @@ def test_phase_ms_requires_a_timed_linear_apply():
     ctx.precond_apply(r)
     ms = ctx.phase_ms()
     assert len(ms) == 4 and min(ms) >= 0.0 and sum(ms) > 0.0
+
+
+@pytest.mark.parametrize("cfg", [synth.CONFIGS["c1"], SMALL[7], SMALL[9]], ids=lambda c: c.name)
+def test_dense_transform_path_matches_oracle(cfg, monkeypatch):
+    """AAO_FFT_DENSE=1: the dense symmetric DFT kernels (used for prime / even n_b) on lengths that default to the
+    prime-factor transform (n_b = 15 = 3 x 5, 255 = 15 x 17, Oseen 255): same map as the oracle's naive DFT."""
+    torch = _torch()
+    monkeypatch.setenv("AAO_FFT_DENSE", "1")
+    _, pc = oracle_for(cfg)
+    r = synth.probe_vector(cfg)
+    z = gpu_ctx(cfg).precond_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert close(z, pc.apply(r), PRECOND_TOL)
