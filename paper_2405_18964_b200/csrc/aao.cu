@@ -569,6 +569,7 @@ void setup(Ctx& c, const aao_config& cfg) {
     f.dc = d[k].imag();
     f.c1 = f.dr / std::sqrt(tau * tau / beta + f.dc * f.dc);       // squared reading (C.2 #1)
     f.c2 = 1.0 / std::sqrt(1.0 / beta + f.dc * f.dc / (tau * tau));
+    f.rc2 = 1.0 / f.c2;
   }
   c.fc = upload(c, c.fch);
   std::vector<double2> tw(n_b);
@@ -896,8 +897,8 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
   if (wave_on && c.dim == 2 && S.order == 2 && a.use_ctab && (op.conv_sel == 0 || wave_conv)) {
     const int n1 = a.g[0].n1;
     const int h = n1 <= 129 ? 6 : 3;
-    const size_t ring = (size_t)8 * h * n1 * sizeof(double2);
-    if (used + ring <= 220 * 1024) {
+    const size_t ring = (size_t)8 * h * n1 * sizeof(double2);   // 8 bands of h rows
+    if (used + ring <= (size_t)MG_SMEM_MAX) {
       a.wave_h = h;
       a.wave_min = c.wave_min;
       used = (used + 15) / 16 * 16;

@@ -54,10 +54,13 @@ struct Transfer {
 struct FreqConst {
   double c1, c2;       // c_{k,1}, c_{k,2} (squared reading)
   double dr, dc;       // Re d_k, Im d_k
+  double rc2;          // 1 / c_{k,2} (the T transforms multiply instead of dividing)
 };
 
 // Arguments of the CTA-resident multigrid solve (one CTA per problem, all levels and cycles).
 constexpr int MG_MAXL = 12;
+constexpr int MG_WAVE_THREADS = 512;   // threads per CTA of the 2-D Q2 class-stencil MG (band-wavefront sweeps)
+constexpr int MG_SMEM_MAX = 232448;    // dynamic shared memory per CTA (227 KB opt-in on sm_100)
 struct MGArgs {
   int nlev, cycles, pre, post;
   double omega;

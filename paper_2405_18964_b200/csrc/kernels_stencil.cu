@@ -18,6 +18,7 @@ namespace aao {
 #ifndef MG_THREADS_TAB
 #define MG_THREADS_TAB 512
 #endif
+static_assert(MG_THREADS_TAB == MG_WAVE_THREADS, "wave staging slots are sized for MG_WAVE_THREADS");
 
 // ---------------------------------------------------------------- complex helpers
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -975,7 +976,8 @@ __device__ __forceinline__ double2 ring_eval_conv(const double2* T, const double
 template <int H, bool CONV = false>
 __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __restrict__ b, double2* ring, int n1,
                              bool reverse, double omega, int tid, int nth, const double* cv = nullptr,
-                             double2 cc = make_double2(0.0, 0.0)) {
+                             double2 cc = make_double2(0.0, 0.0), double2* rout = nullptr) {
+  static_assert(H % 3 == 0, "band height must be a multiple of the 3 row classes");
   constexpr int RR = 8 * H;   // ring rows: 8 bands
   const int nb = (n1 + H - 1) / H;
   auto band_rows = [&](int band, int& j0, int& cnt) {
@@ -999,7 +1001,30 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
   };
   load_async(0);
   if (nb > 1) load_async(1);
+  // Work items of x-colour step q (x residue i0 = i0s[rx]): t = p per + kk cx + m covers the three active bands
+  // T - 2p (p = 0, 1, 2; row class cls = p, reversed 2 - p), rows band H + cls + 3 kk (kk < H / 3), columns
+  // i0 + 3 m.  H is a multiple of 3, so a work item keeps its (p, row offset, column) from one band step to the next
+  // and only its band advances: the mapping is decoded once per thread (at most 2 items per thread and step:
+  // 3 H cx <= 2 nth for every level that uses the wavefront) and packed as i | off << 11 | p << 20.
   const int i0s[3] = {3, 1, 2};
+  int item[3][2];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int i0 = i0s[reverse ? 2 - q : q];
+    const int cx = i0 > n1 - 2 ? 0 : (n1 - 2 - i0) / 3 + 1;
+    const int per = (H / 3) * cx;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int t = tid + u * nth;
+      item[q][u] = -1;
+      if (t < 3 * per) {
+        const int p = t / per, rem = t - p * per;
+        const int kk = rem / cx, m = rem - kk * cx;
+        const int cls = reverse ? 2 - p : p;
+        item[q][u] = (i0 + 3 * m) | ((cls + 3 * kk) << 11) | (p << 20);
+      }
+    }
+  }
   for (int T = 0; T <= nb + 3; ++T) {
     cp_wait_all();
     __syncthreads();
@@ -1008,27 +1033,16 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
       __syncthreads();
     }
     if (T + 2 < nb) load_async(T + 2);
+#pragma unroll
     for (int q = 0; q < 3; ++q) {
-      const int rx = reverse ? 2 - q : q;
-      const int i0 = i0s[rx];
-      const int cx = i0 > n1 - 2 ? 0 : (n1 - 2 - i0) / 3 + 1;
-      const int per = (H / 3) * cx;
-      const int total = 3 * per;
-      const float rper = 1.0f / (float)max(per, 1), rcx = 1.0f / (float)max(cx, 1);
-      for (int t = tid; t < total; t += nth) {
-        int p = __float2int_rz(((float)t + 0.5f) * rper);
-        int rem = t - p * per;
-        if (rem >= per) { rem -= per; ++p; } else if (rem < 0) { rem += per; --p; }
-        const int band = T - 2 * p;
-        if (band < 0 || band >= nb) continue;
-        const int cls = reverse ? 2 - p : p;   // row class j mod 3 of pair p
-        int kk = __float2int_rz(((float)rem + 0.5f) * rcx);
-        int m = rem - kk * cx;
-        if (m >= cx) { m -= cx; ++kk; } else if (m < 0) { m += cx; --kk; }
-        const int k0 = ((cls - band * H) % 3 + 3) % 3;
-        const int j = band * H + k0 + 3 * kk;
-        if (j < 1 || j > n1 - 2) continue;
-        const int i = i0 + 3 * m;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int it = item[q][u];
+        if (it < 0) continue;
+        const int band = T - 2 * (it >> 20);
+        const int j = band * H + ((it >> 11) & 511);
+        if (band < 0 || band >= nb || j < 1 || j > n1 - 2) continue;
+        const int i = it & 2047;
         const double2 bb = b[(long)j * n1 + i];
         const int r0 = j % RR;
         const int ccls = (i & 1) | ((j & 1) << 1);
@@ -1051,41 +1065,58 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
       }
       __syncthreads();
     }
+    // fused residual (last pre-smoothing sweep, forward colour order): band T - 4 has had its last row class
+    // updated in this step, and every row its stencils reach is final (band T - 5 and the first two row classes of
+    // band T - 3); r = b - A x on its interior nodes, from the ring (same taps, same order as the separate pass)
+    if (rout != nullptr) {
+      const int F = T - 4;
+      if (F >= 0 && F < nb) {
+        const int j0 = max(1, F * H), j1 = min(n1 - 2, F * H + H - 1);
+        const int w = n1 - 2, cnt = (j1 - j0 + 1) * w;
+        for (int e = tid; e < cnt; e += nth) {
+          const int jj = e / w, j = j0 + jj, i = 1 + (e - jj * w);
+          const int r0 = j % RR;
+          const double2 bb = b[(long)j * n1 + i];
+          const int ccls = (i & 1) | ((j & 1) << 1);
+          double2 Ax;
+          if constexpr (CONV) {
+            const double2* Tc = reinterpret_cast<const double2*>(tabl) + ccls * ClassTab<2>::NT;
+            const double* cvr = cv + ((long)j * n1 + i) * ClassTab<2>::NT;
+            Ax = (j & 1) ? ring_eval_conv<RR, 1>(Tc, cvr, cc, ring, r0, i, n1)
+                         : ring_eval_conv<RR, 0>(Tc, cvr, cc, ring, r0, i, n1);
+          } else {
+            const double* Tc = tabl + ccls * (ClassTab<2>::NT + 1);
+            Ax = (j & 1) ? ring_eval<RR, 1>(Tc, ring, r0, i, n1) : ring_eval<RR, 0>(Tc, ring, r0, i, n1);
+          }
+          rout[(long)j * n1 + i] = csub(bb, Ax);
+        }
+      }
+    }
   }
   for (int band = max(0, nb - 2); band < nb; ++band)
     if (band + 6 > nb + 3) writeback(band);
   __syncthreads();
 }
 
+// Returns true if the band-wavefront path also wrote the residual b - A x of the final iterate to rout.
 template <int DIM, int ORD, bool CONV, bool W, bool TAB>
-__device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
+__device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
                                           const double2* b, int sweeps, bool reverse, double omega, int tid, int nth,
                                           const double* tabl, double2* ring = nullptr,
-                                          int waveH = 0, int flat_max = 0) {
+                                          int waveH = 0, int flat_max = 0, double2* rout = nullptr) {
   constexpr int C1 = ORD == 2 ? 3 : 2;
   constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
-  if constexpr (TAB && CONV && ORD == 2 && DIM == 2 && !W) {
+  if constexpr (TAB && ORD == 2 && DIM == 2 && !W) {
     if (ring && waveH) {
+      const double2 cc = CONV ? cf.c : make_double2(0.0, 0.0);
       for (int sw = 0; sw < sweeps; ++sw) {
+        double2* rr = (sw == sweeps - 1 && !reverse) ? rout : nullptr;
         if (waveH == 6)
-          q2_wave_pass<6, true>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cf.c);
+          q2_wave_pass<6, CONV>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cc, rr);
         else
-          q2_wave_pass<3, true>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cf.c);
+          q2_wave_pass<3, CONV>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cc, rr);
       }
-      return;
-    }
-  }
-  if constexpr (TAB && !CONV && ORD == 2 && DIM == 2 && !W) {
-    if (ring && waveH) {
-      for (int sw = 0; sw < sweeps; ++sw) {
-        switch (waveH) {
-          case 3: q2_wave_pass<3>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth); break;
-          case 6: q2_wave_pass<6>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth); break;
-          case 9: q2_wave_pass<9>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth); break;
-          default: q2_wave_pass<12>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth); break;
-        }
-      }
-      return;
+      return rout != nullptr && sweeps > 0 && !reverse;
     }
   }
   for (int sw = 0; sw < sweeps; ++sw)
@@ -1157,6 +1188,28 @@ __device__ __forceinline__ void cta_sweep(const Grid& g, const Coef& cf, const d
       }
       gsync<W>();
     }
+  return false;
+}
+
+// Q2 transfer weights in closed form (nodal interpolation between N_c and 2 N_c cells, reading 12): the
+// same values as the host tables tP / tR (every product of them is exact in binary), without their loads.
+// Restriction row of coarse node I (fine offsets -3..3 around 2 I): vertex (even I) {-1/8, 0, 3/8, 1, 3/8, 0, -1/8},
+// midpoint (odd I) {0, 0, 3/4, 1, 3/4, 0, 0}.
+__device__ __forceinline__ void q2_rrow(int I, double* w) {
+  const bool mid = I & 1;
+  w[0] = w[6] = mid ? 0.0 : -0.125;
+  w[1] = w[5] = 0.0;
+  w[2] = w[4] = mid ? 0.75 : 0.375;
+  w[3] = 1.0;
+}
+// Prolongation of fine node f (interior): coarse nodes 2 (f >> 2) + {0, 1, 2}; f mod 4 = 0: {1, 0, 0}, 1: {3/8, 3/4,
+// -1/8}, 2: {0, 1, 0}, 3: {-1/8, 3/4, 3/8}
+__device__ __forceinline__ int q2_prow(int f, double* w) {
+  const int r = f & 3;
+  w[0] = r == 0 ? 1.0 : (r == 1 ? 0.375 : (r == 3 ? -0.125 : 0.0));
+  w[1] = (r & 1) ? 0.75 : (r == 2 ? 1.0 : 0.0);
+  w[2] = r == 1 ? -0.125 : (r == 3 ? 0.375 : 0.0);
+  return 2 * (f >> 2);
 }
 
 // level storage of one problem inside the CTA-resident MG
@@ -1203,12 +1256,15 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
     }
   };
   const bool wv = a.wave_h && l < a.lsm && g.n1 >= a.wave_min;
-  cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl,
-                                    wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0, a.flat_max);
-  pmark(2 * MG_MAXL - 2);
   double2* rl = S.R(l);
+  const bool fused = cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl,
+                                                       wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0,
+                                                       a.flat_max, wv ? rl : nullptr);
+  pmark(2 * MG_MAXL - 2);
   const double* cvl = S.CV(l);
-  if (TAB && CONV && ORD == 2 && DIM == 2 && g.n1 <= a.flat_max) {
+  if (fused) {
+    // residual written by the last wavefront sweep
+  } else if (TAB && CONV && ORD == 2 && DIM == 2 && g.n1 <= a.flat_max) {
     int s1[DIM], st1[DIM];
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
@@ -1257,39 +1313,54 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
   const Transfer t = a.t[l];
   const int o7 = ORD == 2 ? 0 : 2;
   double2* bn = S.B(l + 1);
-  for (int I = tid; I < (int)gc.n; I += nth) {
+  const int n1 = g.n1;
+  // b_{l+1}[I] = (P^T r_l)[I]; two coarse nodes per thread and round so that their gathers overlap
+  auto restrict_node = [&](int I) -> double2 {
     int c[DIM];
     coords<DIM>(I, gc.n1, c);
-    if (masked<DIM, ORD>(c, I, gc.n1)) {
-      bn[I] = make_double2(0.0, 0.0);
-      continue;
-    }
+    if (masked<DIM, ORD>(c, I, gc.n1)) return make_double2(0.0, 0.0);
     double w[DIM][WR];
 #pragma unroll
-    for (int d = 0; d < DIM; ++d)
+    for (int d = 0; d < DIM; ++d) {
+      if constexpr (ORD == 2) {
+        q2_rrow(c[d], w[d]);
+      } else {
 #pragma unroll
-      for (int o = 0; o < WR; ++o) w[d][o] = __ldg(t.tR + c[d] * 7 + o7 + o);
+        for (int o = 0; o < WR; ++o) w[d][o] = __ldg(t.tR + c[d] * 7 + o7 + o);
+      }
+    }
     double2 acc = make_double2(0.0, 0.0);
-    const int n1 = g.n1;
     if constexpr (DIM == 2) {
+#pragma unroll
       for (int ob = 0; ob < WR; ++ob) {
         if (w[1][ob] == 0.0) continue;
         const double2* rrow = rl + (2 * c[1] + ob - R) * n1 + 2 * c[0] - R;
+#pragma unroll
         for (int oa = 0; oa < WR; ++oa)
           if (w[0][oa] != 0.0) acc = cfma(w[1][ob] * w[0][oa], rrow[oa], acc);
       }
     } else {
       for (int oc = 0; oc < WR; ++oc) {
         if (w[2][oc] == 0.0) continue;
+#pragma unroll
         for (int ob = 0; ob < WR; ++ob) {
           if (w[1][ob] == 0.0) continue;
           const double2* rrow = rl + ((2 * c[2] + oc - R) * n1 + 2 * c[1] + ob - R) * n1 + 2 * c[0] - R;
+#pragma unroll
           for (int oa = 0; oa < WR; ++oa)
             if (w[0][oa] != 0.0) acc = cfma(w[2][oc] * w[1][ob] * w[0][oa], rrow[oa], acc);
         }
       }
     }
-    bn[I] = acc;
+    return acc;
+  };
+  const int ncn = (int)gc.n;
+  for (int I = tid; I < ncn; I += 2 * nth) {
+    const int I2 = I + nth;
+    const double2 v1 = restrict_node(I);
+    const double2 v2 = I2 < ncn ? restrict_node(I2) : make_double2(0.0, 0.0);
+    bn[I] = v1;
+    if (I2 < ncn) bn[I2] = v2;
   }
   gsync<W>();
   pmark(2 * MG_MAXL - 4);
@@ -1328,9 +1399,13 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
     double w[DIM][NW];
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
-      base[d] = (int)__ldg(t.tP + c[d] * 4);
+      if constexpr (ORD == 2) {
+        base[d] = q2_prow(c[d], w[d]);
+      } else {
+        base[d] = (int)__ldg(t.tP + c[d] * 4);
 #pragma unroll
-      for (int o = 0; o < NW; ++o) w[d][o] = __ldg(t.tP + c[d] * 4 + 1 + o);
+        for (int o = 0; o < NW; ++o) w[d][o] = __ldg(t.tP + c[d] * 4 + 1 + o);
+      }
     }
     const int n1 = gc.n1;
     double2 acc = make_double2(0.0, 0.0);
@@ -1611,11 +1686,11 @@ template <int DIM, int ORD>
 static void mgcta_t(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_mg_cta<DIM, ORD, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_mg_cta<DIM, ORD, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_mg_cta<DIM, ORD, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, MG_SMEM_MAX);
+    cudaFuncSetAttribute(k_mg_cta<DIM, ORD, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, MG_SMEM_MAX);
     if (ORD == 2) {
-      cudaFuncSetAttribute(k_mg_cta<DIM, ORD, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-      cudaFuncSetAttribute(k_mg_cta<DIM, ORD, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      cudaFuncSetAttribute(k_mg_cta<DIM, ORD, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, MG_SMEM_MAX);
+      cudaFuncSetAttribute(k_mg_cta<DIM, ORD, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, MG_SMEM_MAX);
     }
     attr = true;
   }

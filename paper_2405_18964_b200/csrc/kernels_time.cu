@@ -11,6 +11,7 @@
 // load/store is a coalesced row segment, the time DFT runs along the tile in
 // shared memory, and the frequency layout [k][half][field][node] (space
 // contiguous again) falls out of the same tile.  No separate transpose pass.
+#include <cmath>
 #include <cstdlib>
 
 #include "aao_internal.h"
@@ -44,21 +45,23 @@ struct Geo {
   int dim, n1q2, n1q1, n_b, n_f;
   long n_s, n_v, n_p, nblk;
   double tau, nu, beta;
+  double rst;          // 1 / sqrt(tau)
 };
 
 // slot values y_h0, y_h1 of column `col` at frequency k (after T_r^{-1} for Stokes)
 __device__ __forceinline__ void slot_values(const Geo& G, const InvSrc& S, const FreqConst& f, int k, long col,
                                             double2& y0, double2& y1) {
-  const double st = sqrt(G.tau);
+  const double rs = G.rst;   // 1 / sqrt(tau)
   if (col < G.n_v) {
     const long comp = col / G.n_s, node = col % G.n_s;
     const double2 x1 = S.v1[k * S.vstride + comp * G.n_s + node];
     const double2 x2 = S.v2[k * S.vstride + comp * G.n_s + node];
     if (S.stokes) {
       // T_r^{-1}: y2 = x2 c2 / sqrt(tau); y1 = (x1 + i (dc/sqrt(tau)) y2) / sqrt(tau)
-      const double2 yy2 = make_double2(x2.x * f.c2 / st, x2.y * f.c2 / st);
-      const double a = f.dc / st;
-      y0 = make_double2((x1.x - a * yy2.y) / st, (x1.y + a * yy2.x) / st);
+      const double g = f.c2 * rs;
+      const double2 yy2 = make_double2(x2.x * g, x2.y * g);
+      const double a = f.dc * rs;
+      y0 = make_double2((x1.x - a * yy2.y) * rs, (x1.y + a * yy2.x) * rs);
       y1 = yy2;
     } else {
       y0 = x1;
@@ -79,9 +82,9 @@ __device__ __forceinline__ void slot_values(const Geo& G, const InvSrc& S, const
         x4 = make_double2(ca * a1.x + cb * b1.x, ca * a1.y + cb * b1.y);
       }
       // T_r^{-1}: y4 = x4 / sqrt(tau); y3 = (x3 + i (dc c2 / sqrt(tau)) y4) / (sqrt(tau) c2)
-      const double2 yy4 = make_double2(x4.x / st, x4.y / st);
-      const double a = f.dc * f.c2 / st, den = st * f.c2;
-      y0 = make_double2((x3.x - a * yy4.y) / den, (x3.y + a * yy4.x) / den);
+      const double2 yy4 = make_double2(x4.x * rs, x4.y * rs);
+      const double a = f.dc * f.c2 * rs, rden = rs * f.rc2;
+      y0 = make_double2((x3.x - a * yy4.y) * rden, (x3.y + a * yy4.x) * rden);
       y1 = yy4;
     } else {
       y0 = make_double2(S.pscale * a0.x, S.pscale * a0.y);
@@ -96,6 +99,36 @@ __device__ __forceinline__ bool col_masked(const Geo& G, long col) {
 }
 
 // ------------------------------------------------------------------ forward transform
+// store T_l^{-1} r_hat_k of one column (Stokes; Oseen: no T transform) in the frequency layout
+__device__ __forceinline__ void fwd_store(const Geo& G, double2* __restrict__ Fv, double2* __restrict__ Fp,
+                                          const FreqConst& f, int k, long col, double2 s0, double2 s1, int stokes) {
+  const double rs = G.rst;
+  if (col < G.n_v) {
+    if (stokes) {
+      // T_l^{-1}: s1 = r1/sqrt(tau); s2 = (r2 - i (dc/sqrt(tau)) s1) c2 / sqrt(tau)
+      const double2 q1 = make_double2(s0.x * rs, s0.y * rs);
+      const double a = f.dc * rs, g = f.c2 * rs;
+      s1 = make_double2((s1.x + a * q1.y) * g, (s1.y - a * q1.x) * g);
+      s0 = q1;
+    }
+    const long comp = col / G.n_s, node = col % G.n_s;
+    Fv[(((long)k * 2 + 0) * G.dim + comp) * G.n_s + node] = s0;
+    Fv[(((long)k * 2 + 1) * G.dim + comp) * G.n_s + node] = s1;
+  } else {
+    if (stokes) {
+      // s3 = r3 / (sqrt(tau) c2); s4 = (r4 - i (dc c2 / sqrt(tau)) s3) / sqrt(tau)
+      const double rden = rs * f.rc2;
+      const double2 q3 = make_double2(s0.x * rden, s0.y * rden);
+      const double a = f.dc * f.c2 * rs;
+      s1 = make_double2((s1.x + a * q3.y) * rs, (s1.y - a * q3.x) * rs);
+      s0 = q3;
+    }
+    const long node = col - G.n_v;
+    Fp[((long)k * 2 + 0) * G.n_p + node] = s0;
+    Fp[((long)k * 2 + 1) * G.n_p + node] = s1;
+  }
+}
+
 __global__ void k_fft_fwd(Geo G, const double* __restrict__ r, double2* __restrict__ Fv, double2* __restrict__ Fp,
                           const FreqConst* __restrict__ fc, const double2* __restrict__ tw, int TD, int stokes) {
   extern __shared__ double sm[];
@@ -127,32 +160,7 @@ __global__ void k_fft_fwd(Geo G, const double* __restrict__ r, double2* __restri
       m += k;
       if (m >= n_b) m -= n_b;
     }
-    double2 s0 = make_double2(a0r, a0i), s1 = make_double2(a1r, a1i);
-    const FreqConst f = fc[k];
-    if (col < G.n_v) {
-      if (stokes) {
-        // T_l^{-1}: s1 = r1/sqrt(tau); s2 = (r2 - i (dc/sqrt(tau)) s1) c2 / sqrt(tau)
-        const double2 q1 = make_double2(s0.x / st, s0.y / st);
-        const double a = f.dc / st, g = f.c2 / st;
-        s1 = make_double2((s1.x + a * q1.y) * g, (s1.y - a * q1.x) * g);
-        s0 = q1;
-      }
-      const long comp = col / G.n_s, node = col % G.n_s;
-      Fv[(((long)k * 2 + 0) * G.dim + comp) * G.n_s + node] = s0;
-      Fv[(((long)k * 2 + 1) * G.dim + comp) * G.n_s + node] = s1;
-    } else {
-      if (stokes) {
-        // s3 = r3 / (sqrt(tau) c2); s4 = (r4 - i (dc c2 / sqrt(tau)) s3) / sqrt(tau)
-        const double den = st * f.c2;
-        const double2 q3 = make_double2(s0.x / den, s0.y / den);
-        const double a = f.dc * f.c2 / st;
-        s1 = make_double2((s1.x + a * q3.y) / st, (s1.y - a * q3.x) / st);
-        s0 = q3;
-      }
-      const long node = col - G.n_v;
-      Fp[((long)k * 2 + 0) * G.n_p + node] = s0;
-      Fp[((long)k * 2 + 1) * G.n_p + node] = s1;
-    }
+    fwd_store(G, Fv, Fp, fc[k], k, col, make_double2(a0r, a0i), make_double2(a1r, a1i), stokes);
   }
 }
 
@@ -162,33 +170,6 @@ __global__ void k_fft_fwd(Geo G, const double* __restrict__ r, double2* __restri
 // -- half the multiply-adds of the plain sum.  The pair sums/differences are formed in place in shared
 // memory; every thread keeps KB frequencies of one column in registers, so each staged value is read
 // once per KB outputs and each twiddle load is a warp broadcast.
-__device__ __forceinline__ void fwd_store(const Geo& G, double2* __restrict__ Fv, double2* __restrict__ Fp,
-                                          const FreqConst& f, int k, long col, double2 s0, double2 s1, int stokes) {
-  const double st = sqrt(G.tau);
-  if (col < G.n_v) {
-    if (stokes) {
-      const double2 q1 = make_double2(s0.x / st, s0.y / st);
-      const double a = f.dc / st, g = f.c2 / st;
-      s1 = make_double2((s1.x + a * q1.y) * g, (s1.y - a * q1.x) * g);
-      s0 = q1;
-    }
-    const long comp = col / G.n_s, node = col % G.n_s;
-    Fv[(((long)k * 2 + 0) * G.dim + comp) * G.n_s + node] = s0;
-    Fv[(((long)k * 2 + 1) * G.dim + comp) * G.n_s + node] = s1;
-  } else {
-    if (stokes) {
-      const double den = st * f.c2;
-      const double2 q3 = make_double2(s0.x / den, s0.y / den);
-      const double a = f.dc * f.c2 / st;
-      s1 = make_double2((s1.x + a * q3.y) / st, (s1.y - a * q3.x) / st);
-      s0 = q3;
-    }
-    const long node = col - G.n_v;
-    Fp[((long)k * 2 + 0) * G.n_p + node] = s0;
-    Fp[((long)k * 2 + 1) * G.n_p + node] = s1;
-  }
-}
-
 template <int KB>
 __global__ void __launch_bounds__(256) k_fft_fwd_sym(Geo G, const double* __restrict__ r, double2* __restrict__ Fv,
                                                      double2* __restrict__ Fp, const FreqConst* __restrict__ fc,
@@ -338,9 +319,16 @@ template <int P, int Q>
 struct Pfa {
   static constexpr int HQ = (Q - 1) / 2;           // pairs t2, Q - t2
   static constexpr int NK2 = HQ + 1;               // k2 = 0..HQ
-  static constexpr int KB = P < NK2 ? P : NK2;     // k2 per block (one per warp in stage B)
+  // k2 per block: stage A computes 4 k2 at a time (4 independent accumulator pairs per pass over the pairs)
+  static constexpr int KB = (NK2 + 3) / 4 * 4 <= 12 ? (NK2 + 3) / 4 * 4 : 8;
   static constexpr int NBLK = (NK2 + KB - 1) / KB;
   static constexpr int THREADS = 32 * P;
+  // dynamic shared memory (double2 units): twiddles omega_Q^{k2 (j + 1)} [NK2][HQ], omega_P [P], frequency
+  // constants [n_f] (FreqConst = 5 doubles, rounded to 3 double2), then the exchange buffers
+  static constexpr int TW2 = NK2 * HQ;
+  static size_t smem(int n_f, int nbuf) {
+    return (size_t)(TW2 + P + 3 * n_f + nbuf * KB * P * 32) * sizeof(double2);
+  }
 };
 
 struct PfaMap {
@@ -353,18 +341,32 @@ __device__ __forceinline__ double2 cj(double2 a) { return make_double2(a.x, -a.y
 __device__ __forceinline__ double2 tl_inv_half(const Geo& G, const FreqConst& f, long col, double2 s0, double2 s1,
                                                int stokes, int h) {
   if (!stokes) return h ? s1 : s0;
-  const double st = sqrt(G.tau);
+  const double rs = G.rst;
   if (col < G.n_v) {
-    const double2 q1 = make_double2(s0.x / st, s0.y / st);
+    const double2 q1 = make_double2(s0.x * rs, s0.y * rs);
     if (h == 0) return q1;
-    const double a = f.dc / st, g = f.c2 / st;
+    const double a = f.dc * rs, g = f.c2 * rs;
     return make_double2((s1.x + a * q1.y) * g, (s1.y - a * q1.x) * g);
   }
-  const double den = st * f.c2;
-  const double2 q3 = make_double2(s0.x / den, s0.y / den);
+  const double rden = rs * f.rc2;
+  const double2 q3 = make_double2(s0.x * rden, s0.y * rden);
   if (h == 0) return q3;
-  const double a = f.dc * f.c2 / st;
-  return make_double2((s1.x + a * q3.y) / st, (s1.y - a * q3.x) / st);
+  const double a = f.dc * f.c2 * rs;
+  return make_double2((s1.x + a * q3.y) * rs, (s1.y - a * q3.x) * rs);
+}
+
+// shared tables of the prime-factor kernels: tw2[k2][j] = (cos, sin)(2 pi k2 (j + 1) / Q), twP[m] = (cos, sin)(2 pi m / P),
+// fcs[k] = the frequency constants (k < n_f)
+template <int P, int Q>
+__device__ __forceinline__ void pfa_tables(const Geo& G, const double2* __restrict__ tw, const FreqConst* __restrict__ fc,
+                                           double2* tw2, double2* twP, FreqConst* fcs) {
+  using PF = Pfa<P, Q>;
+  for (int e = threadIdx.x; e < PF::TW2; e += PF::THREADS) {
+    const int k2 = e / PF::HQ, j = e - k2 * PF::HQ;
+    tw2[e] = tw[((k2 * (j + 1)) % Q) * P];          // exp(2 pi i m / Q) = tw[m P] (tw: n_b-th roots)
+  }
+  for (int m = threadIdx.x; m < P; m += PF::THREADS) twP[m] = tw[m * Q];
+  for (int k = threadIdx.x; k < G.n_f; k += PF::THREADS) fcs[k] = fc[k];
 }
 
 template <int P, int Q>
@@ -375,15 +377,15 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_fwd_pfa(Geo G, const
                                                                     int stokes) {
   using PF = Pfa<P, Q>;
   constexpr int n = P * Q;
-  extern __shared__ double2 pfa_sm[];    // twQ[Q], twP[P], Ys[KB][P][32] ([k2 - block start][t1][series])
-  double2* twQ = pfa_sm;
-  double2* twP = twQ + Q;
-  double2 (*Ys)[P][32] = reinterpret_cast<double2 (*)[P][32]>(twP + P);
+  extern __shared__ double2 pfa_sm[];
+  double2* tw2 = pfa_sm;
+  double2* twP = tw2 + PF::TW2;
+  FreqConst* fcs = reinterpret_cast<FreqConst*>(twP + P);
+  double2 (*Ys)[P][32] = reinterpret_cast<double2 (*)[P][32]>(twP + P + 3 * G.n_f);   // [k2 - block start][t1][series]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int h = lane >> 4;
   const long col = (long)blockIdx.x * 16 + (lane & 15);
-  for (int m = threadIdx.x; m < Q; m += PF::THREADS) twQ[m] = tw[m * P];   // exp(-2 pi i m / Q) = tw[m P]
-  for (int m = threadIdx.x; m < P; m += PF::THREADS) twP[m] = tw[m * Q];
+  pfa_tables<P, Q>(G, tw, fc, tw2, twP, fcs);
   const bool valid = col < G.nblk;
   const bool msk = !valid || col_masked(G, col);
   // stage A inputs of series (col, h), t1 = w: y[t2] = r[h][t(w, t2)][col]; pair sums / differences in registers
@@ -399,29 +401,39 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_fwd_pfa(Geo G, const
   }
   __syncthreads();
   for (int blk = 0; blk < PF::NBLK; ++blk) {
-    // stage A: Y[w][k2] for the KB values k2 = blk KB + i:  Re = y0 + sum ps cos, Im = -sum pd sin
-    for (int i = 0; i < PF::KB; ++i) {
-      const int k2 = blk * PF::KB + i;
-      if (k2 > PF::HQ) break;
-      double re = y0, im = 0.0;
-      int m = 0;
+    // stage A: Y[w][k2] for k2 = blk KB + i, four at a time:  Re = y0 + sum_j ps_j cos, Im = -sum_j pd_j sin
+#pragma unroll 1
+    for (int i0 = 0; i0 < PF::KB; i0 += 4) {
+      const int kb = blk * PF::KB + i0;
+      double re[4], im[4];
+      const double2* tr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        re[u] = y0;
+        im[u] = 0.0;
+        tr[u] = tw2 + min(kb + u, PF::HQ) * PF::HQ;   // rows past HQ are computed but never stored
+      }
 #pragma unroll
       for (int j = 0; j < PF::HQ; ++j) {
-        m += k2;
-        if (m >= Q) m -= Q;
-        const double2 wq = twQ[m];     // (cos, sin)(2 pi k2 (j + 1) / Q); warp-uniform
-        re = fma(ps[j], wq.x, re);
-        im = fma(-pd[j], wq.y, im);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double2 wq = tr[u][j];                  // warp-uniform broadcast
+          re[u] = fma(ps[j], wq.x, re[u]);
+          im[u] = fma(-pd[j], wq.y, im[u]);
+        }
       }
-      Ys[i][w][lane] = make_double2(re, im);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (kb + u <= PF::HQ) Ys[i0 + u][w][lane] = make_double2(re[u], im[u]);
     }
     __syncthreads();
-    // stage B for k2 = blk KB + w: X[k1] = sum_t1 Y[t1] omega_P^{k1 t1}, k1 = 0..P-1; then T_l^{-1} and the store
-    const int k2 = blk * PF::KB + w;
-    if (w < PF::KB && k2 <= PF::HQ) {
+    // stage B: X[k1][k2] = sum_t1 Y[t1][k2] omega_P^{k1 t1}, k1 = 0..P-1; then T_l^{-1} and the store
+    for (int i = w; i < PF::KB; i += P) {
+      const int k2 = blk * PF::KB + i;
+      if (k2 > PF::HQ) break;
       double2 yv[P];
 #pragma unroll
-      for (int t1 = 0; t1 < P; ++t1) yv[t1] = Ys[w][t1][lane];
+      for (int t1 = 0; t1 < P; ++t1) yv[t1] = Ys[i][t1][lane];
 #pragma unroll
       for (int k1 = 0; k1 < P; ++k1) {
         double2 x = yv[0];
@@ -432,19 +444,17 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_fwd_pfa(Geo G, const
           x.y += yv[t1].y * wp.x - yv[t1].x * wp.y;
         }
         int k = (k1 * mp.QA + k2 * mp.PB) % n;
-        bool cjg = false;
         if (k >= G.n_f) {               // X[n - k] = conj(X[k]); k2 = 0 entries above n_f are their own mirror
           if (k2 == 0) continue;
           k = n - k;
-          cjg = true;
+          x = cj(x);
         }
-        if (cjg) x = cj(x);
         double2 other;
         other.x = __shfl_xor_sync(0xffffffffu, x.x, 16);
         other.y = __shfl_xor_sync(0xffffffffu, x.y, 16);
         if (!valid) continue;
         const double2 s0 = h ? other : x, s1 = h ? x : other;
-        const double2 out = tl_inv_half(G, fc[k], col, s0, s1, stokes, h);
+        const double2 out = tl_inv_half(G, fcs[k], col, s0, s1, stokes, h);
         if (col < G.n_v) {
           const long comp = col / G.n_s, node = col % G.n_s;
           Fv[(((long)k * 2 + h) * G.dim + comp) * G.n_s + node] = out;
@@ -466,16 +476,16 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_inv_pfa(Geo G, InvSr
                                                                     const double2* __restrict__ tw, PfaMap mp) {
   using PF = Pfa<P, Q>;
   constexpr int n = P * Q;
-  extern __shared__ double2 pfa_sm[];    // twQ[Q], twP[P], Hs[KB][P][32] (gathered spectrum, [k2][k1][series]),
-  double2* twQ = pfa_sm;                 // Zs[KB][P][32] ([k2][t1][series])
-  double2* twP = twQ + Q;
-  double2 (*Hs)[P][32] = reinterpret_cast<double2 (*)[P][32]>(twP + P);
-  double2 (*Zs)[P][32] = Hs + PF::KB;
+  extern __shared__ double2 pfa_sm[];
+  double2* tw2 = pfa_sm;
+  double2* twP = tw2 + PF::TW2;
+  FreqConst* fcs = reinterpret_cast<FreqConst*>(twP + P);
+  double2 (*Hs)[P][32] = reinterpret_cast<double2 (*)[P][32]>(twP + P + 3 * G.n_f);   // gathered spectrum [k2][k1][s]
+  double2 (*Zs)[P][32] = Hs + PF::KB;                                                  // [k2][t1][s]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int h = lane >> 4;
   const long col = (long)blockIdx.x * 16 + (lane & 15);
-  for (int m = threadIdx.x; m < Q; m += PF::THREADS) twQ[m] = tw[m * P];
-  for (int m = threadIdx.x; m < P; m += PF::THREADS) twP[m] = tw[m * Q];
+  pfa_tables<P, Q>(G, tw, fc, tw2, twP, fcs);
   const bool valid = col < G.nblk;
   const bool msk = !valid || col_masked(G, col);
   double a0 = 0.0, s0 = 0.0;            // Z[w][0].re and sum_{k2>=1} Re Z[w][k2] (t2 = 0)
@@ -484,29 +494,29 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_inv_pfa(Geo G, InvSr
   for (int j = 0; j < PF::HQ; ++j) C[j] = Sn[j] = 0.0;
   __syncthreads();
   for (int blk = 0; blk < PF::NBLK; ++blk) {
-    // gather: Yh[k1][k2] for k2 = blk KB + w (T_r^{-1} applied, both halves read, own half kept)
-    const int k2g = blk * PF::KB + w;
-    const bool mine = w < PF::KB && k2g <= PF::HQ;
-    if (mine) {
+    // gather: Yh[k1][k2] for the block's k2 (T_r^{-1} applied, both halves read, own half kept)
+    for (int i = w; i < PF::KB; i += P) {
+      const int k2g = blk * PF::KB + i;
+      if (k2g > PF::HQ) break;
+#pragma unroll
       for (int k1 = 0; k1 < P; ++k1) {
         int k = (k1 * mp.QA + k2g * mp.PB) % n;
-        bool cjg = false;
-        if (k >= G.n_f) {
-          k = n - k;
-          cjg = true;
-        }
+        const bool cjg = k >= G.n_f;
+        if (cjg) k = n - k;
         double2 v0 = make_double2(0.0, 0.0), v1 = v0;
-        if (!msk) slot_values(G, S, fc[k], k, col, v0, v1);
+        if (!msk) slot_values(G, S, fcs[k], k, col, v0, v1);
         const double2 v = h ? v1 : v0;
-        Hs[w][k1][lane] = cjg ? cj(v) : v;
+        Hs[i][k1][lane] = cjg ? cj(v) : v;
       }
     }
     __syncthreads();
-    // stage B^-1 for k2 = blk KB + w: Z[t1] = sum_k1 Yh[k1] omega_P^{-k1 t1}
-    if (mine) {
+    // stage B^-1: Z[t1] = sum_k1 Yh[k1] omega_P^{-k1 t1}
+    for (int i = w; i < PF::KB; i += P) {
+      const int k2g = blk * PF::KB + i;
+      if (k2g > PF::HQ) break;
       double2 hv[P];
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) hv[k1] = Hs[w][k1][lane];
+      for (int k1 = 0; k1 < P; ++k1) hv[k1] = Hs[i][k1][lane];
 #pragma unroll
       for (int t1 = 0; t1 < P; ++t1) {
         double2 x = hv[0];
@@ -516,7 +526,7 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_inv_pfa(Geo G, InvSr
           x.x += hv[k1].x * wp.x - hv[k1].y * wp.y;
           x.y += hv[k1].y * wp.x + hv[k1].x * wp.y;
         }
-        Zs[w][t1][lane] = x;
+        Zs[i][t1][lane] = x;
       }
     }
     __syncthreads();
@@ -530,12 +540,10 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_inv_pfa(Geo G, InvSr
         continue;
       }
       s0 += zz.x;
-      int m = 0;
+      const double2* tr = tw2 + k2 * PF::HQ;
 #pragma unroll
       for (int j = 0; j < PF::HQ; ++j) {
-        m += k2;
-        if (m >= Q) m -= Q;
-        const double2 wq = twQ[m];      // cos, sin of 2 pi k2 (j + 1) / Q
+        const double2 wq = tr[j];        // cos, sin of 2 pi k2 (j + 1) / Q
         C[j] = fma(zz.x, wq.x, C[j]);
         Sn[j] = fma(zz.y, wq.y, Sn[j]);
       }
@@ -986,6 +994,7 @@ Geo geo_of(const Ctx& c) {
   g.tau = c.tau;
   g.nu = c.nu;
   g.beta = c.beta;
+  g.rst = 1.0 / std::sqrt(c.tau);
   return g;
 }
 
@@ -1092,7 +1101,7 @@ static bool pfa_off() {
 }
 template <int P, int Q>
 static void fwd_pfa_t(const Ctx& c, const double* r, PfaMap mp, cudaStream_t s) {
-  const size_t sm = (Q + P + (size_t)Pfa<P, Q>::KB * P * 32) * sizeof(double2);
+  const size_t sm = Pfa<P, Q>::smem(c.n_f, 1);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fft_fwd_pfa<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1103,7 +1112,7 @@ static void fwd_pfa_t(const Ctx& c, const double* r, PfaMap mp, cudaStream_t s) 
 }
 template <int P, int Q>
 static void inv_pfa_t(const Ctx& c, const InvSrc& S, double* z, PfaMap mp, cudaStream_t s) {
-  const size_t sm = (Q + P + 2 * (size_t)Pfa<P, Q>::KB * P * 32) * sizeof(double2);
+  const size_t sm = Pfa<P, Q>::smem(c.n_f, 2);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fft_inv_pfa<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
