@@ -897,7 +897,9 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
   if (wave_on && c.dim == 2 && S.order == 2 && a.use_ctab && (op.conv_sel == 0 || wave_conv)) {
     const int n1 = a.g[0].n1;
     const int h = n1 <= 129 ? 6 : 3;
-    const size_t ring = (size_t)8 * h * n1 * sizeof(double2);   // 8 bands of h rows
+    // 8 bands of h rows.  (Staging b one step ahead by cp.async into 3 more slots per thread was measured slower:
+    // c4_512 velocity MG 228 -> 236 ms -- the extra 24 KB of shared memory comes out of the L1 cache.)
+    const size_t ring = (size_t)8 * h * n1 * sizeof(double2);
     if (used + ring <= (size_t)MG_SMEM_MAX) {
       a.wave_h = h;
       a.wave_min = c.wave_min;
@@ -907,6 +909,9 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
     }
   }
   a.flat_max = 33;   // measured: 33 best (c2 precond 2.371 -> 2.249 ms)
+  // 3-D: z-band wavefront sweeps on the levels whose iterate does not stay in L2 across the 27 colour steps
+  // (n1 >= 65 by default; AAO_WAVE=1 forces every level >= AAO_WAVE_MIN, AAO_WAVE=0 none)
+  a.zwave_min = c.wave_force == 0 ? (1 << 30) : (c.wave_force == 1 ? c.wave_min : 65);
   // profiling only: per-level SM-cycle accounting of CTA 0, printed per launch (AAO_MG_CLOCK=1)
   static const bool mg_clock = std::getenv("AAO_MG_CLOCK") != nullptr;
   static unsigned long long* clk_dev = nullptr;

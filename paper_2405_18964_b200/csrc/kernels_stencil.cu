@@ -930,6 +930,27 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_commit_all() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
+// Q2 transfer weights in closed form (nodal interpolation between N_c and 2 N_c cells, DESIGN.md reading 12): the
+// same values as the host tables tP / tR (every product of them is exact in binary), without their loads.
+// Restriction row of coarse node I (fine offsets -3..3 around 2 I): vertex (even I) {-1/8, 0, 3/8, 1, 3/8, 0, -1/8},
+// midpoint (odd I) {0, 0, 3/4, 1, 3/4, 0, 0}.
+__device__ __forceinline__ void q2_rrow(int I, double* w) {
+  const bool mid = I & 1;
+  w[0] = w[6] = mid ? 0.0 : -0.125;
+  w[1] = w[5] = 0.0;
+  w[2] = w[4] = mid ? 0.75 : 0.375;
+  w[3] = 1.0;
+}
+// Prolongation of fine node f (interior): coarse nodes 2 (f >> 2) + {0, 1, 2}; f mod 4 = 0: {1, 0, 0}, 1: {3/8, 3/4,
+// -1/8}, 2: {0, 1, 0}, 3: {-1/8, 3/4, 3/8}
+__device__ __forceinline__ int q2_prow(int f, double* w) {
+  const int r = f & 3;
+  w[0] = r == 0 ? 1.0 : (r == 1 ? 0.375 : (r == 3 ? -0.125 : 0.0));
+  w[1] = (r & 1) ? 0.75 : (r == 2 ? 1.0 : 0.0);
+  w[2] = r == 1 ? -0.125 : (r == 3 ? 0.375 : 0.0);
+  return 2 * (f >> 2);
+}
+
 template <int RR, int PY>
 __device__ __forceinline__ double2 ring_eval(const double* T, const double2* ring, int r0, int i, int n1) {
   constexpr int AY0 = PY ? 1 : 0, AY1 = PY ? 4 : 5;
@@ -976,7 +997,8 @@ __device__ __forceinline__ double2 ring_eval_conv(const double2* T, const double
 template <int H, bool CONV = false>
 __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __restrict__ b, double2* ring, int n1,
                              bool reverse, double omega, int tid, int nth, const double* cv = nullptr,
-                             double2 cc = make_double2(0.0, 0.0), double2* rout = nullptr) {
+                             double2 cc = make_double2(0.0, 0.0), double2* rout = nullptr,
+                             const double2* xcoarse = nullptr, int n1c = 0) {
   static_assert(H % 3 == 0, "band height must be a multiple of the 3 row classes");
   constexpr int RR = 8 * H;   // ring rows: 8 bands
   const int nb = (n1 + H - 1) / H;
@@ -984,13 +1006,37 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
     j0 = band * H;
     cnt = (min(n1, j0 + H) - j0) * n1;
   };
+  // stream a band of the iterate into the ring; with xcoarse (first post-smoothing sweep) the coarse-grid
+  // correction x += P x_c (nodal interpolation, mg_up's arithmetic) is applied on the way in instead of in a
+  // separate pass over the level
   auto load_async = [&](int band) {
     int j0, cnt;
     band_rows(band, j0, cnt);
     double2* dst = ring + (j0 % RR) * n1;
     const double2* src = x + (long)j0 * n1;
-    for (int e = tid; e < cnt; e += nth) cp_async16(dst + e, src + e);
-    cp_commit_all();
+    if (xcoarse == nullptr) {
+      for (int e = tid; e < cnt; e += nth) cp_async16(dst + e, src + e);
+      cp_commit_all();
+      return;
+    }
+    for (int e = tid; e < cnt; e += nth) {
+      const int jj = e / n1, j = j0 + jj, i = e - jj * n1;
+      double2 v = src[e];
+      if (j >= 1 && j <= n1 - 2 && i >= 1 && i <= n1 - 2) {
+        double wy[3], wx[3];
+        const int by = q2_prow(j, wy), bx = q2_prow(i, wx);
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int ob = 0; ob < 3; ++ob)
+#pragma unroll
+          for (int oa = 0; oa < 3; ++oa) {
+            const double ww = wy[ob] * wx[oa];
+            if (ww != 0.0) acc = cfma(ww, xcoarse[(by + ob) * n1c + bx + oa], acc);
+          }
+        v = cadd(v, acc);
+      }
+      dst[e] = v;
+    }
   };
   auto writeback = [&](int band) {
     int j0, cnt;
@@ -1103,7 +1149,8 @@ template <int DIM, int ORD, bool CONV, bool W, bool TAB>
 __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
                                           const double2* b, int sweeps, bool reverse, double omega, int tid, int nth,
                                           const double* tabl, double2* ring = nullptr,
-                                          int waveH = 0, int flat_max = 0, double2* rout = nullptr) {
+                                          int waveH = 0, int flat_max = 0, double2* rout = nullptr,
+                                          const double2* xcoarse = nullptr, int n1c = 0, bool zwave = false) {
   constexpr int C1 = ORD == 2 ? 3 : 2;
   constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
   if constexpr (TAB && ORD == 2 && DIM == 2 && !W) {
@@ -1111,12 +1158,63 @@ __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const d
       const double2 cc = CONV ? cf.c : make_double2(0.0, 0.0);
       for (int sw = 0; sw < sweeps; ++sw) {
         double2* rr = (sw == sweeps - 1 && !reverse) ? rout : nullptr;
+        const double2* xcs = sw == 0 ? xcoarse : nullptr;
         if (waveH == 6)
-          q2_wave_pass<6, CONV>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cc, rr);
+          q2_wave_pass<6, CONV>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cc, rr, xcs, n1c);
         else
-          q2_wave_pass<3, CONV>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cc, rr);
+          q2_wave_pass<3, CONV>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cc, rr, xcs, n1c);
       }
       return rout != nullptr && sweeps > 0 && !reverse;
+    }
+  }
+  if constexpr (DIM == 3 && ORD == 2 && TAB && !W) {
+    if (zwave) {
+      // z-band wavefront (3-D Q2): planes are grouped in bands of 3 (one plane per z-colour class); at band step T
+      // the bands T, T - 2, T - 4 update their plane of z-class 0, 1, 2 (colour order), and within a step the 9
+      // xy-colours run in order.  Planes within the stencil reach (2) of each other are updated in exactly the
+      // order of the 27 colour steps (as q2_wave_pass for rows), so the sweep is the same map -- but it moves
+      // through the volume once, touching a window of ~21 planes, instead of streaming the whole level once per
+      // colour (27 times per sweep).
+      const int n1 = g.n1;
+      const int nbz = (n1 + 2) / 3;
+      for (int sw = 0; sw < sweeps; ++sw)
+        for (int T = 0; T <= nbz + 3; ++T)
+          for (int q = 0; q < 9; ++q) {
+            const int xy = reverse ? 8 - q : q;
+            const int cx = xy % 3, cy = xy / 3;
+            const int ni = cx > n1 - 2 ? 0 : (n1 - 2 - (cx ? cx : 3)) / 3 + 1;   // i = cx + 3m in [1, n1 - 2]
+            const int i0 = cx ? cx : 3;
+            const int j0 = cy ? cy : 3;
+            const int nj = j0 > n1 - 2 ? 0 : (n1 - 2 - j0) / 3 + 1;
+            // rows of one plane ordered by parity (uniform taps per warp): even-m rows first, then odd-m rows
+            const int per_plane = ni * nj;
+            const int total = 3 * per_plane;
+            const int nje = (nj + 1) / 2;
+            for (int t = tid; t < total; t += nth) {
+              const int pp = t / per_plane, rem = t - pp * per_plane;
+              const int band = T - 2 * pp;
+              if (band < 0 || band >= nbz) continue;
+              const int cz = reverse ? 2 - pp : pp;
+              const int k = 3 * band + cz;
+              if (k < 1 || k > n1 - 2) continue;
+              const int rr = rem / ni, mi = rem - rr * ni;
+              const int mj = rr < nje ? 2 * rr : 2 * (rr - nje) + 1;
+              int c[DIM] = {i0 + 3 * mi, j0 + 3 * mj, k};
+              const int idx = (k * n1 + c[1]) * n1 + c[0];
+              if constexpr (CONV) {
+                double2 D;
+                const double2 Ax = class_eval_conv<DIM>(reinterpret_cast<const double2*>(tabl), cv, cf.c, x, c, idx,
+                                                        n1, D);
+                x[idx] = cadd(x[idx], cscale(omega, cdiv(csub(b[idx], Ax), D)));
+              } else {
+                double invD;
+                const double2 Ax = class_eval<DIM>(tabl, x, c, n1, invD);
+                x[idx] = cadd(x[idx], cscale(omega * invD, csub(b[idx], Ax)));
+              }
+            }
+            __syncthreads();
+          }
+      return false;
     }
   }
   for (int sw = 0; sw < sweeps; ++sw)
@@ -1191,27 +1289,6 @@ __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const d
   return false;
 }
 
-// Q2 transfer weights in closed form (nodal interpolation between N_c and 2 N_c cells, DESIGN.md reading 12): the
-// same values as the host tables tP / tR (every product of them is exact in binary), without their loads.
-// Restriction row of coarse node I (fine offsets -3..3 around 2 I): vertex (even I) {-1/8, 0, 3/8, 1, 3/8, 0, -1/8},
-// midpoint (odd I) {0, 0, 3/4, 1, 3/4, 0, 0}.
-__device__ __forceinline__ void q2_rrow(int I, double* w) {
-  const bool mid = I & 1;
-  w[0] = w[6] = mid ? 0.0 : -0.125;
-  w[1] = w[5] = 0.0;
-  w[2] = w[4] = mid ? 0.75 : 0.375;
-  w[3] = 1.0;
-}
-// Prolongation of fine node f (interior): coarse nodes 2 (f >> 2) + {0, 1, 2}; f mod 4 = 0: {1, 0, 0}, 1: {3/8, 3/4,
-// -1/8}, 2: {0, 1, 0}, 3: {-1/8, 3/4, 3/8}
-__device__ __forceinline__ int q2_prow(int f, double* w) {
-  const int r = f & 3;
-  w[0] = r == 0 ? 1.0 : (r == 1 ? 0.375 : (r == 3 ? -0.125 : 0.0));
-  w[1] = (r & 1) ? 0.75 : (r == 2 ? 1.0 : 0.0);
-  w[2] = r == 1 ? -0.125 : (r == 3 ? 0.375 : 0.0);
-  return 2 * (f >> 2);
-}
-
 // level storage of one problem inside the CTA-resident MG
 struct MGLevels {
   const MGArgs& a;
@@ -1259,7 +1336,8 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
   double2* rl = S.R(l);
   const bool fused = cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl,
                                                        wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0,
-                                                       a.flat_max, wv ? rl : nullptr);
+                                                       a.flat_max, wv ? rl : nullptr, nullptr, 0,
+                                                       DIM == 3 && l < a.lsm && g.n1 >= a.zwave_min);
   pmark(2 * MG_MAXL - 2);
   const double* cvl = S.CV(l);
   if (fused) {
@@ -1394,6 +1472,9 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
   const Transfer t = a.t[l];
   double2* xl = S.X(l);
   const double2* xc = S.X(l + 1);
+  const bool wv = a.wave_h && l < a.lsm && g.n1 >= a.wave_min;
+  const bool fuse_prolong = TAB && ORD == 2 && DIM == 2 && !W && wv && a.post > 0;
+  if (!fuse_prolong) {
   cta_all_unknowns<DIM, ORD>(g.n1, tid, nth, [&](const int* c, int i) {
     int base[DIM];
     double w[DIM][NW];
@@ -1431,11 +1512,12 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
     xl[i] = cadd(xl[i], acc);
   });
   gsync<W>();
+  }
   const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
                                                    : ClassTab<DIM>::PER_LEVEL) : nullptr;
-  const bool wv = a.wave_h && l < a.lsm && g.n1 >= a.wave_min;
   cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl,
-                                    wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0, a.flat_max);
+                                    wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0, a.flat_max, nullptr,
+                                    fuse_prolong ? xc : nullptr, gc.n1, DIM == 3 && l < a.lsm && g.n1 >= a.zwave_min);
 }
 
 // threads per CTA of the CTA-resident MG; 3-D measured: 512 (spills at 128 registers) 205 ms vs 256 (no

@@ -319,8 +319,9 @@ template <int P, int Q>
 struct Pfa {
   static constexpr int HQ = (Q - 1) / 2;           // pairs t2, Q - t2
   static constexpr int NK2 = HQ + 1;               // k2 = 0..HQ
-  // k2 per block: stage A computes 4 k2 at a time (4 independent accumulator pairs per pass over the pairs)
-  static constexpr int KB = (NK2 + 3) / 4 * 4 <= 12 ? (NK2 + 3) / 4 * 4 : 8;
+  // k2 per block: stage A computes 4 k2 at a time (4 independent accumulator pairs per pass over the pairs); up to 4
+  // per warp in stage B
+  static constexpr int KB = (NK2 + 3) / 4 * 4 <= 4 * P ? (NK2 + 3) / 4 * 4 : 4 * P;
   static constexpr int NBLK = (NK2 + KB - 1) / KB;
   static constexpr int THREADS = 32 * P;
   // dynamic shared memory (double2 units): twiddles omega_Q^{k2 (j + 1)} [NK2][HQ], omega_P [P], frequency
@@ -388,6 +389,17 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_fwd_pfa(Geo G, const
   pfa_tables<P, Q>(G, tw, fc, tw2, twP, fcs);
   const bool valid = col < G.nblk;
   const bool msk = !valid || col_masked(G, col);
+  // destination of this series: Fv[k][h][comp][node] (velocity) or Fp[k][h][node]; element k at dst + k * dstride
+  double2* dst;
+  long dstride;
+  if (col < G.n_v) {
+    const long comp = col / G.n_s, node = col - comp * G.n_s;
+    dst = Fv + ((long)h * G.dim + comp) * G.n_s + node;
+    dstride = 2L * G.dim * G.n_s;
+  } else {
+    dst = Fp + (long)h * G.n_p + (col - G.n_v);
+    dstride = 2L * G.n_p;
+  }
   // stage A inputs of series (col, h), t1 = w: y[t2] = r[h][t(w, t2)][col]; pair sums / differences in registers
   const double* rc = r + (long)h * n * G.nblk + col;
   double ps[PF::HQ], pd[PF::HQ];
@@ -454,13 +466,7 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_fwd_pfa(Geo G, const
         other.y = __shfl_xor_sync(0xffffffffu, x.y, 16);
         if (!valid) continue;
         const double2 s0 = h ? other : x, s1 = h ? x : other;
-        const double2 out = tl_inv_half(G, fcs[k], col, s0, s1, stokes, h);
-        if (col < G.n_v) {
-          const long comp = col / G.n_s, node = col % G.n_s;
-          Fv[(((long)k * 2 + h) * G.dim + comp) * G.n_s + node] = out;
-        } else {
-          Fp[((long)k * 2 + h) * G.n_p + (col - G.n_v)] = out;
-        }
+        dst[k * dstride] = tl_inv_half(G, fcs[k], col, s0, s1, stokes, h);
       }
     }
     __syncthreads();
@@ -480,8 +486,8 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_inv_pfa(Geo G, InvSr
   double2* tw2 = pfa_sm;
   double2* twP = tw2 + PF::TW2;
   FreqConst* fcs = reinterpret_cast<FreqConst*>(twP + P);
-  double2 (*Hs)[P][32] = reinterpret_cast<double2 (*)[P][32]>(twP + P + 3 * G.n_f);   // gathered spectrum [k2][k1][s]
-  double2 (*Zs)[P][32] = Hs + PF::KB;                                                  // [k2][t1][s]
+  double2 (*Hs)[P][32] = reinterpret_cast<double2 (*)[P][32]>(twP + P + 3 * G.n_f);   // gathered spectrum [k2][k1][s],
+                                                                                       // then Z [k2][t1][s] in place
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int h = lane >> 4;
   const long col = (long)blockIdx.x * 16 + (lane & 15);
@@ -494,10 +500,12 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_inv_pfa(Geo G, InvSr
   for (int j = 0; j < PF::HQ; ++j) C[j] = Sn[j] = 0.0;
   __syncthreads();
   for (int blk = 0; blk < PF::NBLK; ++blk) {
-    // gather: Yh[k1][k2] for the block's k2 (T_r^{-1} applied, both halves read, own half kept)
+    // gather: Yh[k1][k2] for the block's k2 (T_r^{-1} applied, both halves read, own half kept); the P entries of
+    // an item are independent, so their loads are all in flight together
     for (int i = w; i < PF::KB; i += P) {
       const int k2g = blk * PF::KB + i;
       if (k2g > PF::HQ) break;
+      double2 v[P];
 #pragma unroll
       for (int k1 = 0; k1 < P; ++k1) {
         int k = (k1 * mp.QA + k2g * mp.PB) % n;
@@ -505,12 +513,14 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_inv_pfa(Geo G, InvSr
         if (cjg) k = n - k;
         double2 v0 = make_double2(0.0, 0.0), v1 = v0;
         if (!msk) slot_values(G, S, fcs[k], k, col, v0, v1);
-        const double2 v = h ? v1 : v0;
-        Hs[i][k1][lane] = cjg ? cj(v) : v;
+        v[k1] = h ? v1 : v0;
+        if (cjg) v[k1] = cj(v[k1]);
       }
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) Hs[i][k1][lane] = v[k1];
     }
     __syncthreads();
-    // stage B^-1: Z[t1] = sum_k1 Yh[k1] omega_P^{-k1 t1}
+    // stage B^-1: Z[t1] = sum_k1 Yh[k1] omega_P^{-k1 t1}, written over Yh (each lane owns its entries)
     for (int i = w; i < PF::KB; i += P) {
       const int k2g = blk * PF::KB + i;
       if (k2g > PF::HQ) break;
@@ -526,7 +536,7 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_inv_pfa(Geo G, InvSr
           x.x += hv[k1].x * wp.x - hv[k1].y * wp.y;
           x.y += hv[k1].y * wp.x + hv[k1].x * wp.y;
         }
-        Zs[i][t1][lane] = x;
+        Hs[i][t1][lane] = x;
       }
     }
     __syncthreads();
@@ -534,7 +544,7 @@ __global__ void __launch_bounds__(Pfa<P, Q>::THREADS) k_fft_inv_pfa(Geo G, InvSr
     for (int i = 0; i < PF::KB; ++i) {
       const int k2 = blk * PF::KB + i;
       if (k2 > PF::HQ) break;
-      const double2 zz = Zs[i][w][lane];
+      const double2 zz = Hs[i][w][lane];
       if (k2 == 0) {
         a0 = zz.x;
         continue;
@@ -1112,7 +1122,7 @@ static void fwd_pfa_t(const Ctx& c, const double* r, PfaMap mp, cudaStream_t s) 
 }
 template <int P, int Q>
 static void inv_pfa_t(const Ctx& c, const InvSrc& S, double* z, PfaMap mp, cudaStream_t s) {
-  const size_t sm = Pfa<P, Q>::smem(c.n_f, 2);
+  const size_t sm = Pfa<P, Q>::smem(c.n_f, 1);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fft_inv_pfa<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -307,7 +307,7 @@ def test_nonlinear_precond_parity(cfg):
     assert close(z, zo, PRECOND_TOL), (rel(z, zo), relmax(z, zo))
 
 
-@pytest.mark.parametrize("name", ["nl_stokes_small", "nl_oseen_small", "nl_c3", "nl_c5"])
+@pytest.mark.parametrize("name", ["nl_stokes_small", "nl_oseen_small", "nl_c3", "nl_c5", "nl_c5_head"])
 def test_fgmres_nonlinear_history_parity(name):
     """Algorithm 2 + FGMRES(10): outer iteration counts within +-1 and histories within 1e-8 of the oracle's
     (goldens written by tests/golden/gen_oracle_refs.py); for the full-size c3 (Oseen) and c5 (3-D) -- where
@@ -323,8 +323,12 @@ def test_fgmres_nonlinear_history_parity(name):
         r0 = b / torch.linalg.norm(b)
         ctx.precond_apply(r0)
         assert ctx.last_inner_iterations() == ref["inner_per_apply"][0]
-    x, info, hist, rc = ctx.gmres_solve(b, tol=1e-6, restart=10)
-    assert abs(info["iterations"] - ref["iterations"]) <= 1 and info["converged"] == 1
+    cap = ref.get("max_iters")
+    x, info, hist, rc = ctx.gmres_solve(b, tol=1e-6, restart=10, max_iters=cap or 500)
+    if cap:                     # truncated golden: the first `cap` iterations
+        assert info["iterations"] == ref["iterations"] == cap
+    else:
+        assert abs(info["iterations"] - ref["iterations"]) <= 1 and info["converged"] == 1
     n = min(len(hist), len(ref["hist"]))
     assert np.max(np.abs(np.array(hist[:n]) - np.array(ref["hist"][:n])) / np.array(ref["hist"][:n])) <= 1e-8
 
@@ -348,7 +352,7 @@ def test_arnoldi_hessenberg_parity(cfg):
     assert np.max(np.abs(ritz_g - ritz_o)) <= 1e-7 * np.max(np.abs(ritz_o))
 
 
-@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[1], SMALL[3]], ids=lambda c: c.name)
+@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[1], SMALL[3], SMALL[5], SMALL[6]], ids=lambda c: c.name)
 def test_band_wavefront_sweeps_match_oracle(cfg, monkeypatch):
     """The band-wavefront colour fusion (default only for n1 >= 257) forced on every small level: the same
     map as the per-colour sweeps (ring wrap, partial last band, odd/even n_b, Oseen operators)."""

@@ -8,4 +8,4 @@ ncu --set full --import-source on --clock-control none --kernel-name regex:k_fft
     -o gpurun_out/${tag}_fft_${cfg} -f python tools/ncu_target.py $cfg 1 > gpurun_out/${tag}_ncu_fft_${cfg}.log 2>&1
 ncu --set full --import-source on --clock-control none --kernel-name regex:k_mg_cta --launch-skip 1 --launch-count 1 \
     -o gpurun_out/${tag}_mg_${cfg} -f python tools/ncu_target.py $cfg 1 > gpurun_out/${tag}_ncu_mg_${cfg}.log 2>&1
-tail -2 gpurun_out/${tag}_ncu_fft_${cfg}.log gpurun_out/${tag}_ncu_mg_${cfg}.log
+tail -n 2 gpurun_out/${tag}_ncu_fft_${cfg}.log; tail -n 2 gpurun_out/${tag}_ncu_mg_${cfg}.log
