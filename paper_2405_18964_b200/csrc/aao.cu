@@ -900,12 +900,15 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
     // 8 bands of h rows.  (Staging b one step ahead by cp.async into 3 more slots per thread was measured slower:
     // c4_512 velocity MG 228 -> 236 ms -- the extra 24 KB of shared memory comes out of the L1 cache.)
     const size_t ring = (size_t)8 * h * n1 * sizeof(double2);
-    if (used + ring <= (size_t)MG_SMEM_MAX) {
+    const size_t mbars = 5 * sizeof(double2);   // 8 mbarriers (64 B) + phase word
+    if (used + ring + mbars <= (size_t)MG_SMEM_MAX) {
       a.wave_h = h;
       a.wave_min = c.wave_min;
       used = (used + 15) / 16 * 16;
       a.ring_off = (long)(used / sizeof(double2));
       used += ring;
+      a.mbar_off = (long)(used / sizeof(double2));
+      used += mbars;
     }
   }
   a.flat_max = 33;   // measured: 33 best (c2 precond 2.371 -> 2.249 ms)

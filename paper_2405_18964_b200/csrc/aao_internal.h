@@ -82,6 +82,7 @@ struct MGArgs {
   int wave_h, wave_min;     // band-wavefront sweeps (2-D Q2 real): band height (3 or 6), levels with n1 >= wave_min
   int zwave_min;            // 3-D Q2: levels with n1 >= zwave_min sweep as a z-band wavefront (global memory)
   long ring_off;            // ring buffer offset in dynamic smem (double2 units)
+  long mbar_off;            // 8 band-slot mbarriers + their phase word after the ring (double2 units)
   int flat_max;             // 2-D Q2 real: levels with n1 <= flat_max use merged branch-free colour visits
   unsigned long long* clk;  // profiling (AAO_MG_CLOCK): CTA 0 accumulates SM cycles per [level][down, up]
 };

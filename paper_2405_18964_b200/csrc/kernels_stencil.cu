@@ -930,6 +930,32 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_commit_all() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
+// TMA bulk copies (cp.async.bulk) and mbarriers for the band ring of q2_wave_pass
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* mb, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* mb) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mb)) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, unsigned parity) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(smem_u32(mb)), "r"(parity) : "memory");
+}
+
 // Q2 transfer weights in closed form (nodal interpolation between N_c and 2 N_c cells, reading 12): the
 // same values as the host tables tP / tR (every product of them is exact in binary), without their loads.
 // Restriction row of coarse node I (fine offsets -3..3 around 2 I): vertex (even I) {-1/8, 0, 3/8, 1, 3/8, 0, -1/8},
@@ -998,7 +1024,7 @@ template <int H, bool CONV = false>
 __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __restrict__ b, double2* ring, int n1,
                              bool reverse, double omega, int tid, int nth, const double* cv = nullptr,
                              double2 cc = make_double2(0.0, 0.0), double2* rout = nullptr,
-                             const double2* xcoarse = nullptr, int n1c = 0) {
+                             const double2* xcoarse = nullptr, int n1c = 0, unsigned long long* mbar = nullptr) {
   static_assert(H % 3 == 0, "band height must be a multiple of the 3 row classes");
   constexpr int RR = 8 * H;   // ring rows: 8 bands
   const int nb = (n1 + H - 1) / H;
@@ -1006,17 +1032,22 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
     j0 = band * H;
     cnt = (min(n1, j0 + H) - j0) * n1;
   };
-  // stream a band of the iterate into the ring; with xcoarse (first post-smoothing sweep) the coarse-grid
-  // correction x += P x_c (nodal interpolation, mg_up's arithmetic) is applied on the way in instead of in a
-  // separate pass over the level
-  auto load_async = [&](int band) {
+  // Band copies.  Plain sweeps stream a band of the iterate into the ring with one TMA bulk copy (cp.async.bulk,
+  // 3 H n1 complex values, contiguous in both places) completing on the slot's mbarrier, and write a final band back
+  // with one bulk store; the CTA's threads only wait on the mbarrier.  With xcoarse (first post-smoothing sweep) the
+  // coarse-grid correction x += P x_c (nodal interpolation, mg_up's arithmetic) is applied on the way in by the
+  // threads instead of in a separate pass over the level.
+  // mbarriers (8 slots) and their phase bits: after the finest level's ring (initialised at kernel start)
+  unsigned* phase_word = reinterpret_cast<unsigned*>(mbar + 8);
+  unsigned phase = *phase_word;          // bit s: parity of the next completion of slot s
+  const bool tma = xcoarse == nullptr;
+  auto load_band = [&](int band) {
     int j0, cnt;
     band_rows(band, j0, cnt);
     double2* dst = ring + (j0 % RR) * n1;
     const double2* src = x + (long)j0 * n1;
-    if (xcoarse == nullptr) {
-      for (int e = tid; e < cnt; e += nth) cp_async16(dst + e, src + e);
-      cp_commit_all();
+    if (tma) {
+      if (tid == 0) bulk_load(dst, src, (unsigned)cnt * sizeof(double2), mbar + band % 8);
       return;
     }
     for (int e = tid; e < cnt; e += nth) {
@@ -1038,15 +1069,29 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
       dst[e] = v;
     }
   };
-  auto writeback = [&](int band) {
+  auto wait_band = [&](int band) {      // TMA loads: wait for the slot's completion (all threads)
+    if (!tma) return;
+    const int sl = band % 8;
+    mbar_wait(mbar + sl, (phase >> sl) & 1u);
+    phase ^= 1u << sl;
+  };
+  auto store_band = [&](int band) {     // by thread 0, after a fence + barrier of all writers
+    int j0, cnt;
+    band_rows(band, j0, cnt);
+    bulk_store(x + (long)j0 * n1, ring + (j0 % RR) * n1, (unsigned)cnt * sizeof(double2));
+  };
+  auto copy_back = [&](int band) {      // write a band back by the threads (prolongation sweep)
     int j0, cnt;
     band_rows(band, j0, cnt);
     const double2* src = ring + (j0 % RR) * n1;
     double2* dst = x + (long)j0 * n1;
     for (int e = tid; e < cnt; e += nth) dst[e] = src[e];
   };
-  load_async(0);
-  if (nb > 1) load_async(1);
+  // generic writes of the iterate (previous passes, zeroing) before the async-proxy reads
+  fence_async_global();
+  __syncthreads();
+  load_band(0);
+  if (nb > 1) load_band(1);
   // Work items of x-colour step q (x residue i0 = i0s[rx]): t = p per + kk cx + m covers the three active bands
   // T - 2p (p = 0, 1, 2; row class cls = p, reversed 2 - p), rows band H + cls + 3 kk (kk < H / 3), columns
   // i0 + 3 m.  H is a multiple of 3, so a work item keeps its (p, row offset, column) from one band step to the next
@@ -1072,13 +1117,24 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
     }
   }
   for (int T = 0; T <= nb + 3; ++T) {
-    cp_wait_all();
+    // bands T - 5 .. T + 1 are touched in this step; band T + 1 (issued in step T - 1) must have landed
+    if (T == 0) wait_band(0);
+    if (T + 1 < nb) wait_band(T + 1);
+    if (tma) fence_async_smem();       // this thread's ring writes (step T - 1) -> visible to the bulk store
     __syncthreads();
-    if (T >= 6) {
-      writeback(T - 6);
-      __syncthreads();
+    if (tma) {
+      if (tid == 0) {
+        bulk_wait_read();               // the store of band T - 6 (issued in step T - 1) has read its slot
+        if (T + 2 < nb) load_band(T + 2);
+        if (T - 5 >= 0 && T - 5 < nb) store_band(T - 5);   // final since step T - 1; only read from now on
+      }
+    } else {
+      if (T >= 6) {
+        copy_back(T - 6);
+        __syncthreads();
+      }
+      if (T + 2 < nb) load_band(T + 2);
     }
-    if (T + 2 < nb) load_async(T + 2);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
 #pragma unroll
@@ -1139,8 +1195,19 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
       }
     }
   }
-  for (int band = max(0, nb - 2); band < nb; ++band)
-    if (band + 6 > nb + 3) writeback(band);
+  if (tma) {
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      if (nb - 1 > nb + 3 - 5) store_band(nb - 1);   // the last band (final after step nb + 3)
+      bulk_wait_all();
+      fence_async_global();
+      *phase_word = phase;
+    }
+  } else {
+    for (int band = max(0, nb - 2); band < nb; ++band)
+      if (band + 6 > nb + 3) copy_back(band);
+  }
   __syncthreads();
 }
 
@@ -1150,7 +1217,8 @@ __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const d
                                           const double2* b, int sweeps, bool reverse, double omega, int tid, int nth,
                                           const double* tabl, double2* ring = nullptr,
                                           int waveH = 0, int flat_max = 0, double2* rout = nullptr,
-                                          const double2* xcoarse = nullptr, int n1c = 0, bool zwave = false) {
+                                          const double2* xcoarse = nullptr, int n1c = 0, bool zwave = false,
+                                          unsigned long long* mbar = nullptr) {
   constexpr int C1 = ORD == 2 ? 3 : 2;
   constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
   if constexpr (TAB && ORD == 2 && DIM == 2 && !W) {
@@ -1160,9 +1228,9 @@ __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const d
         double2* rr = (sw == sweeps - 1 && !reverse) ? rout : nullptr;
         const double2* xcs = sw == 0 ? xcoarse : nullptr;
         if (waveH == 6)
-          q2_wave_pass<6, CONV>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cc, rr, xcs, n1c);
+          q2_wave_pass<6, CONV>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cc, rr, xcs, n1c, mbar);
         else
-          q2_wave_pass<3, CONV>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cc, rr, xcs, n1c);
+          q2_wave_pass<3, CONV>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cc, rr, xcs, n1c, mbar);
       }
       return rout != nullptr && sweeps > 0 && !reverse;
     }
@@ -1305,6 +1373,9 @@ struct MGLevels {
   }
   __device__ double2* R(int l) const { return a.rw[l] + (long)p * a.g[l].n; }
   __device__ const double* CV(int l) const { return a.op.conv_sel == 1 ? a.g[l].conv : a.g[l].convT; }
+  __device__ unsigned long long* MBAR() const {
+    return a.wave_h ? reinterpret_cast<unsigned long long*>(smem + a.mbar_off) : nullptr;
+  }
 };
 
 // down-leg of level l: (x_l = 0 for l > 0), pre-smoothing, residual, restriction to b_{l+1}
@@ -1337,7 +1408,7 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
   const bool fused = cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl,
                                                        wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0,
                                                        a.flat_max, wv ? rl : nullptr, nullptr, 0,
-                                                       DIM == 3 && l < a.lsm && g.n1 >= a.zwave_min);
+                                                       DIM == 3 && l < a.lsm && g.n1 >= a.zwave_min, S.MBAR());
   pmark(2 * MG_MAXL - 2);
   const double* cvl = S.CV(l);
   if (fused) {
@@ -1517,7 +1588,8 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
                                                    : ClassTab<DIM>::PER_LEVEL) : nullptr;
   cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl,
                                     wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0, a.flat_max, nullptr,
-                                    fuse_prolong ? xc : nullptr, gc.n1, DIM == 3 && l < a.lsm && g.n1 >= a.zwave_min);
+                                    fuse_prolong ? xc : nullptr, gc.n1, DIM == 3 && l < a.lsm && g.n1 >= a.zwave_min,
+                                    S.MBAR());
 }
 
 // threads per CTA of the CTA-resident MG; 3-D measured: 512 (spills at 128 registers) 205 ms vs 256 (no
@@ -1547,6 +1619,15 @@ __global__ void __launch_bounds__(mg_threads<DIM, TAB>(), 1) k_mg_cta(MGArgs a) 
                                reinterpret_cast<double2*>(ctab) + l * ClassTab<DIM>::NCL * ClassTab<DIM>::NT, tid, nth);
       else
         build_class_tab<DIM>(a.g[l], cf.a.x, cf.b.x, ctab + l * ClassTab<DIM>::PER_LEVEL, tid, nth);
+    }
+    __syncthreads();
+  }
+  if constexpr (TAB && ORD == 2 && DIM == 2) {
+    if (a.wave_h && tid == 0) {   // band-ring mbarriers (8 slots) and their phase word, after the largest ring
+      unsigned long long* mb = reinterpret_cast<unsigned long long*>(smem + a.mbar_off);
+      for (int sl = 0; sl < 8; ++sl) mbar_init(mb + sl, 1);
+      *reinterpret_cast<unsigned*>(mb + 8) = 0u;
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
   }
