@@ -117,24 +117,37 @@ void launch_multi_axpy(double* u, const double* const* V, const double* coef, in
 // step i, so every step costs one pass over the chunk and one grid barrier.  Block partials are
 // reduced in a fixed order by every block (deterministic, bitwise reproducible).
 #ifndef MGS_THREADS
-#define MGS_THREADS 1024
+#define MGS_THREADS 512
 #endif
 #ifndef MGS_PER_SM
 #define MGS_PER_SM 1
 #endif
+
+// Streaming version for vectors too large for the on-chip variant below: the update/dot pass works on double2
+// (n even: N = 2 n_b (n_v + n_p)) with four elements per thread in flight per round (12 independent 16-byte loads),
+// enough memory-level parallelism for one 1024-thread CTA per SM to stream at HBM rate.
+constexpr int MGS_U = 4;
 
 __global__ void __launch_bounds__(MGS_THREADS) k_mgs(double* __restrict__ w, const double* const* __restrict__ V,
                                                      int k, long n, double* __restrict__ H,
                                                      double* __restrict__ partial) {
   cg::grid_group grid = cg::this_grid();
   const int nb = gridDim.x;
-  const long chunk = (n + nb - 1) / nb;
-  const long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  const long chunk = ((n + nb - 1) / nb + 1) / 2 * 2;   // even: double2 aligned
+  const long lo = min(n, blockIdx.x * chunk), hi = min(n, lo + chunk);
   __shared__ double hs;
   // dot for step 0
   double acc = 0.0;
-  const double* v0 = V[0];
-  for (long j = lo + threadIdx.x; j < hi; j += blockDim.x) acc = fma(w[j], v0[j], acc);
+  {
+    const double2* v0 = reinterpret_cast<const double2*>(V[0] + lo);
+    const double2* w2 = reinterpret_cast<const double2*>(w + lo);
+    const long m = (hi - lo) / 2;
+    for (long e = threadIdx.x; e < m; e += blockDim.x) {
+      const double2 a = w2[e], b = __ldcg(v0 + e);
+      acc = fma(a.x, b.x, acc);
+      acc = fma(a.y, b.y, acc);
+    }
+  }
   acc = block_sum(acc);
   if (threadIdx.x == 0) partial[blockIdx.x] = acc;
   grid.sync();
@@ -150,20 +163,35 @@ __global__ void __launch_bounds__(MGS_THREADS) k_mgs(double* __restrict__ w, con
     }
     __syncthreads();
     const double h = hs;
-    const double* vi = V[i];
-    const double* vn = i < k ? V[i + 1] : nullptr;
+    const double2* vi = reinterpret_cast<const double2*>(V[i] + lo);
+    const double2* vn = reinterpret_cast<const double2*>((i < k ? V[i + 1] : w) + lo);
+    double2* w2 = reinterpret_cast<double2*>(w + lo);
+    const long m = (hi - lo) / 2;                 // double2 elements of this chunk
+    const long step = (long)blockDim.x * MGS_U;
     double a2 = 0.0;
-    if (vn) {
-      for (long j = lo + threadIdx.x; j < hi; j += blockDim.x) {
-        const double wj = fma(-h, vi[j], w[j]);
-        w[j] = wj;
-        a2 = fma(wj, vn[j], a2);
+    for (long base = threadIdx.x; base < m; base += step) {
+      double2 ww[MGS_U], vv[MGS_U], nn[MGS_U];
+#pragma unroll
+      for (int u = 0; u < MGS_U; ++u) {
+        const long e = base + (long)u * blockDim.x;
+        if (e < m) {
+          ww[u] = w2[e];
+          vv[u] = __ldcs(vi + e);
+          if (i < k) nn[u] = __ldcg(vn + e);
+        }
       }
-    } else {
-      for (long j = lo + threadIdx.x; j < hi; j += blockDim.x) {
-        const double wj = fma(-h, vi[j], w[j]);
-        w[j] = wj;
-        a2 = fma(wj, wj, a2);
+#pragma unroll
+      for (int u = 0; u < MGS_U; ++u) {
+        const long e = base + (long)u * blockDim.x;
+        if (e < m) {
+          double2 x;
+          x.x = fma(-h, vv[u].x, ww[u].x);
+          x.y = fma(-h, vv[u].y, ww[u].y);
+          w2[e] = x;
+          const double2 y = i < k ? nn[u] : x;
+          a2 = fma(x.x, y.x, a2);
+          a2 = fma(x.y, y.y, a2);
+        }
       }
     }
     a2 = block_sum(a2);
@@ -330,6 +358,7 @@ cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double*
     return cudaLaunchCooperativeKernel((void*)k_mgs_oc<MGS_OC_R2>, dim3(nb), dim3(MGS_OC_THREADS), args,
                                        (size_t)smem, s);
   }
+  if (n % 2 != 0) return cudaErrorInvalidValue;   // N = 2 n_b (n_v + n_p) is even (double2 passes)
   int nb = mgs_blocks();
   void* args[] = {&w, (void*)&V, &k, &n, &H, &partial};
   *scaled = 0;
