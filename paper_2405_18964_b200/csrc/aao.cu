@@ -1256,7 +1256,8 @@ void gmres_alloc(Ctx& c, int m) {
   c.gV = dalloc<double>(c, (size_t)(m + 1) * N);
   c.gz = dalloc<double>(c, N);
   c.gH = dalloc<double>(c, (size_t)(m + 2) * (m + 1));
-  c.gpart = dalloc<double>(c, std::max((long)dot_blocks(), (long)(m + 3) * mgs_blocks()));
+  c.gpart = dalloc<double>(c, std::max((long)dot_blocks(), (long)(2 * m + 4) * 4 * mgs_blocks()));
+  c.gG = dalloc<double>(c, (size_t)(m + 2) * (m + 2));
   c.gscal = dalloc<double>(c, 4 * (m + 2));
   std::vector<double*> ptr(m + 1);
   for (int i = 0; i <= m; ++i) ptr[i] = c.gV + (size_t)i * N;
@@ -1343,7 +1344,7 @@ aao_status gmres(Ctx& c, const double* b, double* x, const aao_krylov& kry, aao_
       if (c.timing) CK(cudaEventRecord(c.gt_ev[2], s));
       double* hcol = c.gH + (size_t)k * (m + 1);
       int w_scaled = 0;
-      CK(launch_mgs(w, (const double* const*)c.gVptr, k, N, hcol, c.gpart, s, &w_scaled));
+      CK(launch_mgs(w, (const double* const*)c.gVptr, k, N, hcol, c.gpart, c.gG, m + 2, s, &w_scaled));
       ++launch_counter();
       if (!w_scaled) {
         launch_scale_dev(w, w, hcol + k + 1, N, s);
@@ -1457,7 +1458,7 @@ int arnoldi(Ctx& c, const double* v0, int m, double* H, cudaStream_t s) {
     kkt_apply(c, c.gz, w, s);
     double* hcol = c.gH + (size_t)k * (m + 1);
     int w_scaled = 0;
-    CK(launch_mgs(w, (const double* const*)c.gVptr, k, N, hcol, c.gpart, s, &w_scaled));
+    CK(launch_mgs(w, (const double* const*)c.gVptr, k, N, hcol, c.gpart, c.gG, m + 2, s, &w_scaled));
     ++launch_counter();
     if (!w_scaled) {
       launch_scale_dev(w, w, hcol + k + 1, N, s);

@@ -157,7 +157,7 @@ struct Ctx {
   // GMRES workspace (allocated on first solve): basis V_0..V_m and one work vector (z / update)
   int gm_m = 0;
   double *gV = nullptr, *gz = nullptr;
-  double *gH = nullptr, *gpart = nullptr, *gscal = nullptr;
+  double *gH = nullptr, *gpart = nullptr, *gscal = nullptr, *gG = nullptr;
   double **gVptr = nullptr;
   double *stage_b = nullptr, *stage_x = nullptr;   // device staging of aao_gmres_solve_host
   double* hostH = nullptr;   // pinned, 2 x (m + 2): Hessenberg columns of iterations k, k+1
@@ -248,9 +248,11 @@ void launch_copy_sub(double* y, const double* b, const double* ax, long n, cudaS
 void launch_multi_axpy(double* u, const double* const* V, const double* coef, int k, long n, cudaStream_t s);
 int dot_blocks();
 int mgs_blocks();
-// whole MGS sweep (dots, updates, norm) in one cooperative launch; partial: [(k+2) * mgs_blocks()]
-// MGS of w against V[0..k] -> H[0..k+1]; sets *scaled = 1 if w was also overwritten by w / H[k+1]
-cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double* H, double* partial, cudaStream_t s,
-                       int* scaled);
+// whole MGS sweep (dots, updates, norm) in one cooperative launch; partial: [(2k+3) * 4 * mgs_blocks()]
+// MGS of w against V[0..k] -> H[0..k+1]; sets *scaled = 1 if w was also overwritten by w / H[k+1].
+// G (ld ldg, rows 0..k+1): Gram rows <v_i, v_j> (j < i) of the current cycle, written and read by the
+// inverse-compact-WY form used for vectors that do not fit on chip (row k+1 is written by step k).
+cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double* H, double* partial, double* G,
+                       int ldg, cudaStream_t s, int* scaled);
 
 }  // namespace aao

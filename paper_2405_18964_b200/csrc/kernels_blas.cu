@@ -206,6 +206,124 @@ __global__ void __launch_bounds__(MGS_THREADS) k_mgs(double* __restrict__ w, con
   }
 }
 
+// ---- MGS in its inverse-compact-WY form for vectors too large for the on-chip variant (c4 at n_t >= 32).
+// MGS computes h_i = <v_i, w^(i)>, w^(i+1) = w^(i) - h_i v_i (i = 0..k).  Since w^(i) = w - sum_{j<i} h_j v_j,
+//   h_i = s_i - sum_{j<i} <v_i, v_j> h_j,   s_i = <v_i, w>,
+// a forward substitution with the strictly lower Gram matrix of the basis (Swirydowicz et al., "Low
+// synchronization Gram-Schmidt and GMRES algorithms", 2020: the same loss of orthogonality as MGS).  The
+// Gram row of v_{k+1} is formed in the update pass that creates it, so one step is two passes over the
+// basis instead of k+1: pass 1 reads w and v_0..v_k once (all k+1 dots); pass 2 reads them again and
+// writes w_new = w - h_0 v_0 - ... - h_k v_k (the same per-element FMA order as MGS), accumulating
+// <w_new, v_j> (-> Gram row k+1) and ||w_new||^2.  HBM traffic per step (2k+5) vectors instead of
+// 4(k+1)+2.  Gram rows live in G (ld = ldg), row i valid for the current restart cycle once v_i exists.
+constexpr int MGSW_THREADS = 256;
+
+__device__ __forceinline__ double dot2(double2 a, double2 b) { return fma(a.x, b.x, a.y * b.y); }
+
+// Block sums of acc[i] for i < cnt and of acc[NA - 1] (when last), written to out[i] / out[NA - 1].
+template <int NA>
+__device__ __forceinline__ void block_sum_many(const double* acc, int cnt, bool last, double* red /* [nw][NA] */,
+                                               double* out /* [NA] */) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NA; ++i) {
+    if (i < cnt || (last && i == NA - 1)) {
+      const double v = warp_sum(acc[i]);
+      if (lane == 0) red[wid * NA + i] = v;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NA; i += blockDim.x) {
+    if (i < cnt || (last && i == NA - 1)) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += red[w * NA + i];
+      out[i] = s;
+    }
+  }
+  __syncthreads();
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(MGSW_THREADS, 2)
+    k_mgs_icwy(double* __restrict__ w, const double* const* __restrict__ V, int k, long n2,
+               double* __restrict__ H, double* __restrict__ partial, double* __restrict__ G, int ldg) {
+  constexpr int NA = KMAX + 1;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[(MGSW_THREADS / 32) * NA];
+  __shared__ double bs[NA], hs[KMAX];
+  __shared__ const double2* vp[KMAX];
+  const int nb = gridDim.x, T = blockDim.x, tid = threadIdx.x;
+  const long chunk = (n2 + nb - 1) / nb;
+  const long lo = min(n2, (long)blockIdx.x * chunk), cnt = min(n2, lo + chunk) - lo;
+  const int K1 = k + 1;
+  if (tid < K1) vp[tid] = reinterpret_cast<const double2*>(V[tid]) + lo;
+  double2* w2 = reinterpret_cast<double2*>(w) + lo;
+  __syncthreads();
+  // pass 1: s_i = <v_i, w>, i = 0..k
+  double acc[NA];
+#pragma unroll
+  for (int i = 0; i < NA; ++i) acc[i] = 0.0;
+  for (long e = tid; e < cnt; e += T) {
+    const double2 x = w2[e];
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i)
+      if (i < K1) acc[i] += dot2(x, __ldcs(vp[i] + e));
+  }
+  block_sum_many<NA>(acc, K1, false, red, bs);
+  for (int i = tid; i < K1; i += T) partial[(long)i * nb + blockIdx.x] = bs[i];
+  grid.sync();
+  // every block: s_i summed in a fixed order, then h_i = s_i - sum_{j<i} G_ij h_j
+  for (int i = tid; i < K1; i += T) {
+    double sm = 0.0;
+    for (int b = 0; b < nb; ++b) sm += partial[(long)i * nb + b];
+    bs[i] = sm;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = 0; i < K1; ++i) {
+      double h = bs[i];
+      for (int j = 0; j < i; ++j) h -= G[(long)i * ldg + j] * hs[j];
+      hs[i] = h;
+      if (blockIdx.x == 0) H[i] = h;
+    }
+  }
+  __syncthreads();
+  // pass 2: w_new = w - h_0 v_0 - ... - h_k v_k (MGS order), q_j = <w_new, v_j>, ||w_new||^2 (acc[KMAX])
+#pragma unroll
+  for (int i = 0; i < NA; ++i) acc[i] = 0.0;
+  for (long e = tid; e < cnt; e += T) {
+    double2 x = w2[e];
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) {
+      if (i < K1) {
+        const double2 v = __ldg(vp[i] + e);
+        x.x = fma(-hs[i], v.x, x.x);
+        x.y = fma(-hs[i], v.y, x.y);
+      }
+    }
+    w2[e] = x;
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i)
+      if (i < K1) acc[i] += dot2(x, __ldg(vp[i] + e));
+    acc[KMAX] += dot2(x, x);
+  }
+  block_sum_many<NA>(acc, K1, true, red, bs);
+  for (int i = tid; i < K1; i += T) partial[(long)(K1 + i) * nb + blockIdx.x] = bs[i];
+  if (tid == 0) partial[(long)(2 * K1) * nb + blockIdx.x] = bs[KMAX];
+  grid.sync();
+  if (blockIdx.x == 0) {
+    for (int i = tid; i <= K1; i += T) {
+      double sm = 0.0;
+      for (int b = 0; b < nb; ++b) sm += partial[(long)(K1 + i) * nb + b];
+      bs[i] = sm;
+    }
+    __syncthreads();
+    const double hn = sqrt(bs[K1]);
+    if (tid == 0) H[K1] = hn;
+    for (int j = tid; j < K1; j += T) G[(long)K1 * ldg + j] = hn > 0.0 ? bs[j] / hn : 0.0;
+  }
+}
+
 // ---- MGS with the new vector w held on chip (registers + shared memory) for all k+1 passes.
 // One 1024-thread CTA per SM owns a contiguous chunk of w (in double2 units): the first R2*1024
 // double2 in registers (slot r of thread t holds element r*1024+t, coalesced), the rest in
@@ -216,8 +334,6 @@ __global__ void __launch_bounds__(MGS_THREADS) k_mgs(double* __restrict__ w, con
 // element as k_mgs (h_i = <w, v_i>, w -= h_i v_i), different (fixed) reduction partition.
 constexpr int MGS_OC_THREADS = 1024;
 constexpr int MGS_OC_R2 = 4;
-
-__device__ __forceinline__ double dot2(double2 a, double2 b) { return fma(a.x, b.x, a.y * b.y); }
 
 template <int R2>
 __global__ void __launch_bounds__(MGS_OC_THREADS, 1)
@@ -340,8 +456,8 @@ static long mgs_oc_smem(long n, long* C2out) {
   return bytes;
 }
 
-cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double* H, double* partial, cudaStream_t s,
-                       int* scaled) {
+cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double* H, double* partial, double* G,
+                       int ldg, cudaStream_t s, int* scaled) {
   long C2 = 0;
   const long smem = mgs_oc_smem(n, &C2);
   if (smem >= 0) {
@@ -359,9 +475,20 @@ cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double*
                                        (size_t)smem, s);
   }
   if (n % 2 != 0) return cudaErrorInvalidValue;   // N = 2 n_b (n_v + n_p) is even (double2 passes)
+  *scaled = 0;
+  if (k < 32 && G) {   // inverse-compact-WY form: two passes over the basis per step
+    long n2 = n / 2;
+    void* args[] = {&w, (void*)&V, &k, &n2, &H, &partial, &G, &ldg};
+    void* fn = k < 8 ? (void*)k_mgs_icwy<8> : k < 16 ? (void*)k_mgs_icwy<16> : (void*)k_mgs_icwy<32>;
+    static int bpsm = 0;
+    if (bpsm == 0) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, k_mgs_icwy<32>, MGSW_THREADS, 0);
+      bpsm = std::max(1, std::min(bpsm, 4));
+    }
+    return cudaLaunchCooperativeKernel(fn, dim3(bpsm * mgs_blocks()), dim3(MGSW_THREADS), args, 0, s);
+  }
   int nb = mgs_blocks();
   void* args[] = {&w, (void*)&V, &k, &n, &H, &partial};
-  *scaled = 0;
   return cudaLaunchCooperativeKernel((void*)k_mgs, dim3(nb), dim3(MGS_THREADS), args, 0, s);
 }
 

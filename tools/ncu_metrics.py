@@ -15,7 +15,10 @@ STALLS = ["long_scoreboard", "barrier", "short_scoreboard", "mio_throttle", "lg_
 
 
 def main(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):   # already exported on the box (tools/ncu_full.sh)
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, u = rows[0], rows[1]
     for r in rows[2:]:

@@ -1,4 +1,5 @@
-"""ncu target: build one context and run `reps` preconditioner applications (and one kkt_apply).
+"""ncu target: build one context and run `reps` preconditioner applications (and one kkt_apply), or, with
+reps < 0, a GMRES(30) solve capped at -reps iterations (MGS, KKT and preconditioner launches of a real step).
 
 usage: python tools/ncu_target.py <config> [reps] [freq_chunk]
 """
@@ -16,10 +17,15 @@ name = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 cfg = synth.CONFIGS[name]
 ctx = Context.from_config(cfg, synth.wind(cfg), freq_chunk=int(sys.argv[3]) if len(sys.argv) > 3 else 0)
-r = torch.from_numpy(synth.probe_vector(cfg)).cuda()
-z = torch.empty_like(r)
-for _ in range(reps):
-    ctx.precond_apply(r, z)
-ctx.kkt_apply(r, z)
+if reps < 0:
+    b = ctx.build_rhs(synth.desired_state(cfg))
+    x, info, hist, rc = ctx.gmres_solve(b, tol=1e-6, restart=30, max_iters=-reps)
+    print("gmres", info["iterations"])
+else:
+    r = torch.from_numpy(synth.probe_vector(cfg)).cuda()
+    z = torch.empty_like(r)
+    for _ in range(reps):
+        ctx.precond_apply(r, z)
+    ctx.kkt_apply(r, z)
 torch.cuda.synchronize()
 print("done", name, ctx.device_bytes() / 1e9)
