@@ -886,27 +886,42 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
       a.lwarp = l;
       break;
     }
-  // band-wavefront sweeps (2-D Q2 real operators) on the levels with n1 >= wave_min (default 257): the
-  // iterate crosses HBM once per sweep instead of once per colour -- measured c4_64 precond 43.6 -> 35.2 ms,
-  // c4_128 87.8 -> 73.5 ms; slower where the level is L2-resident (c2, n1 = 129: 2.37 -> 2.73 ms) and with the
-  // stored per-node convection stencils (c3 255 -> 330 ms).  AAO_WAVE=0/1 forces it off/on for every eligible
-  // level >= AAO_WAVE_MIN (parity-tested).
+  // band-wavefront sweeps (2-D Q2) on the levels with n1 >= wave_min (default 257): the iterate crosses HBM once
+  // per sweep instead of once per colour, every tap is a shared-memory load (measured with the first, node-per-thread
+  // form: c4_64 precond 43.6 -> 35.2 ms, c4_128 87.8 -> 73.5 ms; slower with the stored per-node convection stencils,
+  // c3 255 -> 330 ms, so Oseen operators use it only when forced).  AAO_WAVE=0/1 forces it off/on for every eligible
+  // level >= AAO_WAVE_MIN (parity-tested).  Real operators sweep in triple form, one thread per node triple: the band
+  // height of a level is the largest H in {24, 12, 6, 3} whose H rows of triples fit the CTA's threads and whose
+  // 9-slot ring fits the shared memory left (513^2: 3, 257^2: 6, 129^2: 12, 65^2: 24).
   a.wave_h = 0;
+  for (int l = 0; l < MG_MAXL; ++l) a.wave_hl[l] = 0;
   const bool wave_on = c.wave_force >= 0 ? c.wave_force != 0 : a.g[0].n1 >= c.wave_min;
   const bool wave_conv = c.wave_force == 1;
   if (wave_on && c.dim == 2 && S.order == 2 && a.use_ctab && (op.conv_sel == 0 || wave_conv)) {
-    const int n1 = a.g[0].n1;
-    const int h = n1 <= 129 ? 6 : 3;
-    // 8 bands of h rows.  (Staging b one step ahead by cp.async into 3 more slots per thread was measured slower:
-    // c4_512 velocity MG 228 -> 236 ms -- the extra 24 KB of shared memory comes out of the L1 cache.)
-    const size_t ring = (size_t)8 * h * n1 * sizeof(double2);
-    const size_t mbars = 5 * sizeof(double2);   // 8 mbarriers (64 B) + phase word
-    if (used + ring + mbars <= (size_t)MG_SMEM_MAX) {
-      a.wave_h = h;
-      a.wave_min = c.wave_min;
-      used = (used + 15) / 16 * 16;
-      a.ring_off = (long)(used / sizeof(double2));
-      used += ring;
+    const size_t mbars = 5 * sizeof(double2);   // 9 mbarriers (72 B) + phase word
+    const size_t guard = 2 * MG_RING_GUARD * sizeof(double2);
+    used = (used + 15) / 16 * 16;
+    const size_t cap = (size_t)MG_SMEM_MAX > used + mbars + guard ? (size_t)MG_SMEM_MAX - used - mbars - guard : 0;
+    size_t ring = 0;
+    for (int l = 0; l < a.nlev - 1 && l < a.lsm; ++l) {
+      const int n1 = a.g[l].n1;
+      if (n1 < c.wave_min || n1 < 9) break;
+      int h = 0;
+      if (op.conv_sel != 0) {
+        h = n1 <= 129 ? 6 : 3;                       // node-per-thread form (q2_wave_pass)
+        if ((size_t)8 * h * n1 * sizeof(double2) > cap) h = 0;
+      } else {
+        const int ntr = (n1 - 2) / 3 + 1;
+        for (int cand = c.wave_hmax; cand >= 3 && !h; cand /= 2)
+          if (cand * ntr <= MG_TRI_THREADS && (size_t)MG_TRI_SLOTS * cand * n1 * sizeof(double2) <= cap) h = cand;
+      }
+      a.wave_hl[l] = h;
+      if (h) ring = std::max(ring, (size_t)(op.conv_sel != 0 ? 8 : MG_TRI_SLOTS) * h * n1 * sizeof(double2));
+    }
+    if (ring) {
+      a.wave_h = 1;
+      a.ring_off = (long)(used / sizeof(double2)) + MG_RING_GUARD;
+      used += ring + guard;
       a.mbar_off = (long)(used / sizeof(double2));
       used += mbars;
     }
@@ -922,6 +937,7 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
     if (!clk_dev) cudaMalloc(&clk_dev, 2 * MG_MAXL * sizeof(unsigned long long));
     cudaMemsetAsync(clk_dev, 0, 2 * MG_MAXL * sizeof(unsigned long long), s);
     a.clk = clk_dev;
+    a.clk_block = std::min(std::atoi(std::getenv("AAO_MG_CLOCK")), nprob - 1);
   }
   launch_mg_cta(a, nprob, used, s);
   ++launch_counter();
@@ -931,8 +947,9 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
     cudaStreamSynchronize(s);
     std::fprintf(stderr, "mg_clock order %d nprob %d lwarp %d:", S.order, nprob, a.lwarp);
     for (int l = 0; l < a.nlev - 1; ++l) std::fprintf(stderr, " L%d(n1=%d) %llu/%llu", l, a.g[l].n1, h[2 * l], h[2 * l + 1]);
-    std::fprintf(stderr, " bottom %llu | L0 down: sweeps %llu residual %llu restrict %llu\n", h[2 * MG_MAXL - 1],
-                 h[2 * MG_MAXL - 2], h[2 * MG_MAXL - 3], h[2 * MG_MAXL - 4]);
+    std::fprintf(stderr, " bottom %llu | L0 down: sweeps %llu residual %llu restrict %llu | tri steps: band wait %llu "
+                 "barrier %llu tma issue %llu update %llu residual %llu\n", h[2 * MG_MAXL - 1], h[2 * MG_MAXL - 2],
+                 h[2 * MG_MAXL - 3], h[2 * MG_MAXL - 4], h[16], h[17], h[18], h[19], h[14]);
   }
 }
 
@@ -1552,6 +1569,9 @@ aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
     ctx->c.wave_force = we ? std::atoi(we) : -1;
     const char* wm = std::getenv("AAO_WAVE_MIN");
     ctx->c.wave_min = wm ? std::atoi(wm) : 257;
+    const char* wh = std::getenv("AAO_WAVE_H");      // largest band height tried (24, 12, 6 or 3): tests force 3
+    const int whv = wh ? std::atoi(wh) : 24;
+    ctx->c.wave_hmax = (whv == 3 || whv == 6 || whv == 12) ? whv : 24;
     aao::setup(ctx->c, *cfg);
     for (auto& e : ctx->c.ev) cudaEventCreate(&e);
     cudaStreamCreateWithFlags(&ctx->c.s2, cudaStreamNonBlocking);

@@ -59,7 +59,10 @@ struct FreqConst {
 
 // Arguments of the CTA-resident multigrid solve (one CTA per problem, all levels and cycles).
 constexpr int MG_MAXL = 12;
-constexpr int MG_WAVE_THREADS = 512;   // threads per CTA of the 2-D Q2 class-stencil MG (band-wavefront sweeps)
+constexpr int MG_TRI_THREADS = 544;    // threads per CTA of the 2-D Q2 real class-stencil MG: one per triple of a
+                                       // band-wavefront step (3 rows x 171 triples on a 513^2 level), 120 registers
+constexpr int MG_RING_GUARD = 4;       // zeroed double2 entries before and after the band ring
+constexpr int MG_TRI_SLOTS = 9;        // band slots of the triple-form ring (8 for the node-per-thread Oseen form)
 constexpr int MG_SMEM_MAX = 232448;    // dynamic shared memory per CTA (227 KB opt-in on sm_100)
 struct MGArgs {
   int nlev, cycles, pre, post;
@@ -79,12 +82,14 @@ struct MGArgs {
   int lwarp;              // levels >= lwarp run inside one warp (tiny bottom of the V-cycle)
   int use_ctab;           // Q2 operators: per-level class stencils at the start of dynamic smem
   long sm_x[MG_MAXL], sm_b[MG_MAXL];
-  int wave_h, wave_min;     // band-wavefront sweeps (2-D Q2 real): band height (3 or 6), levels with n1 >= wave_min
+  int wave_h;               // band-wavefront sweeps (2-D Q2) on some level: the ring and its mbarriers exist
+  int wave_hl[MG_MAXL];     // per level: band height H (rows per band, a multiple of 3), 0 = colour-by-colour sweeps
   int zwave_min;            // 3-D Q2: levels with n1 >= zwave_min sweep as a z-band wavefront (global memory)
   long ring_off;            // ring buffer offset in dynamic smem (double2 units)
-  long mbar_off;            // 8 band-slot mbarriers + their phase word after the ring (double2 units)
+  long mbar_off;            // 9 band-slot mbarriers + their phase word after the ring (double2 units)
   int flat_max;             // 2-D Q2 real: levels with n1 <= flat_max use merged branch-free colour visits
-  unsigned long long* clk;  // profiling (AAO_MG_CLOCK): CTA 0 accumulates SM cycles per [level][down, up]
+  unsigned long long* clk;  // profiling (AAO_MG_CLOCK=<block>): that CTA accumulates SM cycles per [level][down, up]
+  int clk_block;
 };
 
 // a frequency vector: velocity part [k][half][comp][node] and pressure part [k][half][node] (complex)
@@ -175,6 +180,7 @@ struct Ctx {
   cudaStream_t s2 = nullptr;               // side stream: pressure solves overlap the velocity MG
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int wave_force = -1, wave_min = 257;   // band-wavefront sweeps: AAO_WAVE (-1 auto), AAO_WAVE_MIN
+  int wave_hmax = 24;                    // largest band height tried per level (AAO_WAVE_H)
   int mg_mode = 0;       // MG schedule: 0 CTA-resident (default), 1 per level / colour launches (AAO_MG_MODE=1)
   int freq_chunk = 0;    // frequencies per velocity-MG launch (aao_config.freq_chunk; workspace sized for it)
   bool phase_valid = false;   // ev[0..4] recorded by the last linear precond_apply (aao_last_phase_ms)

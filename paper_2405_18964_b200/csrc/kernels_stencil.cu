@@ -18,7 +18,6 @@ namespace aao {
 #ifndef MG_THREADS_TAB
 #define MG_THREADS_TAB 512
 #endif
-static_assert(MG_THREADS_TAB == MG_WAVE_THREADS, "wave staging slots are sized for MG_WAVE_THREADS");
 
 // ---------------------------------------------------------------- complex helpers
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -946,6 +945,7 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned 
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
@@ -978,27 +978,6 @@ __device__ __forceinline__ int q2_prow(int f, double* w) {
 }
 
 template <int RR, int PY>
-__device__ __forceinline__ double2 ring_eval(const double* T, const double2* ring, int r0, int i, int n1) {
-  constexpr int AY0 = PY ? 1 : 0, AY1 = PY ? 4 : 5;
-  const int xl = i >= 2 ? i - 2 : i, xr = i + 2 <= n1 - 1 ? i + 2 : i;
-  double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-  for (int ob = AY0; ob < AY1; ++ob) {
-    int r = r0 + ob - 2;
-    r += r < 0 ? RR : 0;
-    r -= r >= RR ? RR : 0;
-    const double2* row = ring + r * n1;
-    const double* t = T + ob * 5;
-    acc = cfma(t[0], row[xl], acc);
-    acc = cfma(t[1], row[i - 1], acc);
-    acc = cfma(t[2], row[i], acc);
-    acc = cfma(t[3], row[i + 1], acc);
-    acc = cfma(t[4], row[xr], acc);
-  }
-  return acc;
-}
-
-template <int RR, int PY>
 __device__ __forceinline__ double2 ring_eval_conv(const double2* T, const double* cvr, double2 cc, const double2* ring,
                                                   int r0, int i, int n1) {
   constexpr int AY0 = PY ? 1 : 0, AY1 = PY ? 4 : 5;
@@ -1020,7 +999,7 @@ __device__ __forceinline__ double2 ring_eval_conv(const double2* T, const double
   return cadd(acc, cmul(cc, nacc));
 }
 
-template <int H, bool CONV = false>
+template <int H>
 __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __restrict__ b, double2* ring, int n1,
                              bool reverse, double omega, int tid, int nth, const double* cv = nullptr,
                              double2 cc = make_double2(0.0, 0.0), double2* rout = nullptr,
@@ -1038,7 +1017,7 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
   // coarse-grid correction x += P x_c (nodal interpolation, mg_up's arithmetic) is applied on the way in by the
   // threads instead of in a separate pass over the level.
   // mbarriers (8 slots) and their phase bits: after the finest level's ring (initialised at kernel start)
-  unsigned* phase_word = reinterpret_cast<unsigned*>(mbar + 8);
+  unsigned* phase_word = reinterpret_cast<unsigned*>(mbar + MG_TRI_SLOTS);
   unsigned phase = *phase_word;          // bit s: parity of the next completion of slot s
   const bool tma = xcoarse == nullptr;
   auto load_band = [&](int band) {
@@ -1149,21 +1128,13 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
         const int r0 = j % RR;
         const int ccls = (i & 1) | ((j & 1) << 1);
         double2* xp = ring + r0 * n1 + i;
-        if constexpr (CONV) {
-          const double2* Tc = reinterpret_cast<const double2*>(tabl) + ccls * ClassTab<2>::NT;
-          const double* cvr = cv + ((long)j * n1 + i) * ClassTab<2>::NT;
-          const double2 Ax = (j & 1) ? ring_eval_conv<RR, 1>(Tc, cvr, cc, ring, r0, i, n1)
-                                     : ring_eval_conv<RR, 0>(Tc, cvr, cc, ring, r0, i, n1);
-          const double2 D = cadd(Tc[12], cscale(__ldg(cvr + 12), cc));
-          const double2 xo = *xp;
-          *xp = cadd(xo, cscale(omega, cdiv(csub(bb, Ax), D)));
-        } else {
-          const double* Tc = tabl + ccls * (ClassTab<2>::NT + 1);
-          const double invD = Tc[ClassTab<2>::NT];
-          const double2 Ax = (j & 1) ? ring_eval<RR, 1>(Tc, ring, r0, i, n1) : ring_eval<RR, 0>(Tc, ring, r0, i, n1);
-          const double2 xo = *xp;
-          *xp = make_double2(xo.x + omega * invD * (bb.x - Ax.x), xo.y + omega * invD * (bb.y - Ax.y));
-        }
+        const double2* Tc = reinterpret_cast<const double2*>(tabl) + ccls * ClassTab<2>::NT;
+        const double* cvr = cv + ((long)j * n1 + i) * ClassTab<2>::NT;
+        const double2 Ax = (j & 1) ? ring_eval_conv<RR, 1>(Tc, cvr, cc, ring, r0, i, n1)
+                                   : ring_eval_conv<RR, 0>(Tc, cvr, cc, ring, r0, i, n1);
+        const double2 D = cadd(Tc[12], cscale(__ldg(cvr + 12), cc));
+        const double2 xo = *xp;
+        *xp = cadd(xo, cscale(omega, cdiv(csub(bb, Ax), D)));
       }
       __syncthreads();
     }
@@ -1180,16 +1151,10 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
           const int r0 = j % RR;
           const double2 bb = b[(long)j * n1 + i];
           const int ccls = (i & 1) | ((j & 1) << 1);
-          double2 Ax;
-          if constexpr (CONV) {
-            const double2* Tc = reinterpret_cast<const double2*>(tabl) + ccls * ClassTab<2>::NT;
-            const double* cvr = cv + ((long)j * n1 + i) * ClassTab<2>::NT;
-            Ax = (j & 1) ? ring_eval_conv<RR, 1>(Tc, cvr, cc, ring, r0, i, n1)
-                         : ring_eval_conv<RR, 0>(Tc, cvr, cc, ring, r0, i, n1);
-          } else {
-            const double* Tc = tabl + ccls * (ClassTab<2>::NT + 1);
-            Ax = (j & 1) ? ring_eval<RR, 1>(Tc, ring, r0, i, n1) : ring_eval<RR, 0>(Tc, ring, r0, i, n1);
-          }
+          const double2* Tc = reinterpret_cast<const double2*>(tabl) + ccls * ClassTab<2>::NT;
+          const double* cvr = cv + ((long)j * n1 + i) * ClassTab<2>::NT;
+          const double2 Ax = (j & 1) ? ring_eval_conv<RR, 1>(Tc, cvr, cc, ring, r0, i, n1)
+                                     : ring_eval_conv<RR, 0>(Tc, cvr, cc, ring, r0, i, n1);
           rout[(long)j * n1 + i] = csub(bb, Ax);
         }
       }
@@ -1211,6 +1176,307 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
   __syncthreads();
 }
 
+// ---- band-wavefront sweeps in triple form (2-D Q2, real class stencils) ------------------------------------------
+// The same schedule of updates as q2_wave_pass (bands of H rows; a row of class c' in band B is updated at step
+// B + 2 c'; the three x-colours of a step run in order), reorganised so that the barrier-separated x-colour phases
+// carry almost no work.  A thread owns the three consecutive nodes (3m, 3m+1, 3m+2) of one active row: one node of
+// each x-colour.  Rows j +- 1, j +- 2 belong to other row classes and are not written during the step, and within
+// row j only the triple itself and the colour-0 / colour-1 nodes of the neighbouring triple (m + 1; m - 1 for the
+// reversed colour order) change before the triple's last update.  So every tap that cannot change is accumulated up
+// front in one phase with all loads independent -- 7 columns x 5 rows serve the three nodes, 35 shared-memory loads
+// instead of 3 x 25 -- and each x-colour phase only adds its one or two fresh values and updates its node.  The
+// reversed order is the mirror image: local column c stands for i0 + 4 - c, local tap oa for 4 - oa.
+// Columns -2, -1 (m = 0) and n1 .. n1 + 2 (last triple) fall into the neighbouring ring rows or the zeroed guard
+// around the ring; they only meet zero coefficients (midpoint rows have three taps) or inactive boundary nodes.
+template <bool REV, int PY, bool FULL>
+__device__ __forceinline__ void tri_accumulate(const double* __restrict__ Ta, const double* __restrict__ Tb,
+                                               const double2* ring, int r0, int RR, int n1, int cb, double2* acc,
+                                               double2* xo) {
+  constexpr int AY0 = PY ? 1 : 0, AY1 = PY ? 4 : 5;
+#pragma unroll
+  for (int ob = AY0; ob < AY1; ++ob) {
+    int r = r0 + ob - 2;
+    r += r < 0 ? RR : 0;
+    r -= r >= RR ? RR : 0;
+    const double2* row = ring + r * n1 + cb;
+    double ta[5], tb[5];
+#pragma unroll
+    for (int oa = 0; oa < 5; ++oa) {
+      ta[oa] = Ta[ob * 5 + (REV ? 4 - oa : oa)];
+      tb[oa] = Tb[ob * 5 + (REV ? 4 - oa : oa)];
+    }
+    if (FULL || ob != 2) {
+      double2 v[7];
+#pragma unroll
+      for (int c = 0; c < 7; ++c) v[c] = row[REV ? -c : c];
+#pragma unroll
+      for (int oa = 0; oa < 5; ++oa) {
+        acc[0] = cfma(ta[oa], v[oa], acc[0]);
+        acc[1] = cfma(tb[oa], v[1 + oa], acc[1]);
+        acc[2] = cfma(ta[oa], v[2 + oa], acc[2]);
+      }
+    } else {
+      // row j: node 0 (first colour) sees only old values; nodes 1 and 2 take their fresh taps in their own phase
+      double2 v[5];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) v[c] = row[REV ? -c : c];
+      xo[0] = v[2];
+      xo[1] = v[3];
+      xo[2] = v[4];
+#pragma unroll
+      for (int oa = 0; oa < 5; ++oa) acc[0] = cfma(ta[oa], v[oa], acc[0]);
+      acc[1] = cfma(tb[0], v[1], acc[1]);
+      acc[1] = cfma(tb[2], v[3], acc[1]);
+      acc[1] = cfma(tb[3], v[4], acc[1]);
+      acc[2] = cfma(ta[2], v[4], acc[2]);
+    }
+  }
+}
+
+// one band step of the triple-form sweep for this thread's item (see q2_tri_pass)
+template <bool REV>
+__device__ __forceinline__ void tri_step(const double* tabl, double2* ring, int n1, int RR, int j, int r0, int i0,
+                                         int px, bool on, const bool* act, double omega, double2* acc) {
+  const int cb = REV ? i0 + 4 : i0 - 2;
+  const int py = j & 1;
+  // class stencils of the x-parity of nodes 0 and 2 (Ta) and of node 1 (Tb); lanes alternate in parity, the two
+  // addresses of a warp fall into different banks (a select from two broadcast loads was measured no faster)
+  const double* Ta = tabl + (px | (py << 1)) * (ClassTab<2>::NT + 1);
+  const double* Tb = tabl + ((px ^ 1) | (py << 1)) * (ClassTab<2>::NT + 1);
+  double2 xo[3] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  double2* rowj = ring + r0 * n1 + cb;
+  double wa = 0.0, wb = 0.0, tb1 = 0.0, tb4 = 0.0, ta0 = 0.0, ta1 = 0.0, ta3 = 0.0, ta4 = 0.0;
+  if (on) {
+    if (py) tri_accumulate<REV, 1, false>(Ta, Tb, ring, r0, RR, n1, cb, acc, xo);
+    else tri_accumulate<REV, 0, false>(Ta, Tb, ring, r0, RR, n1, cb, acc, xo);
+    wa = omega * Ta[ClassTab<2>::NT];
+    wb = omega * Tb[ClassTab<2>::NT];
+    tb1 = Tb[10 + (REV ? 3 : 1)];
+    tb4 = Tb[10 + (REV ? 0 : 4)];
+    ta0 = Ta[10 + (REV ? 4 : 0)];
+    ta1 = Ta[10 + (REV ? 3 : 1)];
+    ta3 = Ta[10 + (REV ? 1 : 3)];
+    ta4 = Ta[10 + (REV ? 0 : 4)];
+  }
+  // first x-colour
+  double2 x0n = xo[0];
+  if (on && act[0]) {
+    x0n = make_double2(xo[0].x - wa * acc[0].x, xo[0].y - wa * acc[0].y);
+    rowj[REV ? -2 : 2] = x0n;
+  }
+  __syncthreads();
+  // second x-colour: fresh taps = own first node and the first node of the next triple
+  double2 x1n = xo[1];
+  double2 v5 = make_double2(0.0, 0.0);
+  if (on) {
+    v5 = rowj[REV ? -5 : 5];
+    if (act[1]) {
+      double2 a1 = cfma(tb1, x0n, acc[1]);
+      a1 = cfma(tb4, v5, a1);
+      x1n = make_double2(xo[1].x - wb * a1.x, xo[1].y - wb * a1.y);
+      rowj[REV ? -3 : 3] = x1n;
+    }
+  }
+  __syncthreads();
+  // third x-colour
+  if (on && act[2]) {
+    const double2 v6 = rowj[REV ? -6 : 6];
+    double2 a2 = cfma(ta0, x0n, acc[2]);
+    a2 = cfma(ta1, x1n, a2);
+    a2 = cfma(ta3, v5, a2);
+    a2 = cfma(ta4, v6, a2);
+    rowj[REV ? -4 : 4] = make_double2(xo[2].x - wa * a2.x, xo[2].y - wa * a2.y);
+  }
+}
+
+// Ring of MG_TRI_SLOTS = 9 band slots.  At step T the bands T - 4 .. T are updated (rows up to band T + 1 and down to
+// band T - 5 are read), band T + 1 has landed, band T + 2 is being loaded, band T - 5 (final since step T - 1) is
+// stored and, in the sweep that also produces the residual, r = b - A x of band T - 5 is formed from final values
+// (its stencils reach the last rows of band T - 6 and the first two rows -- row classes 0 and 1, final -- of band
+// T - 4): nothing this step writes is read by it, so it needs no barrier of its own.  The slot loaded at step T held
+// band T - 7, whose store was issued two steps earlier, so the copy thread never waits for the latest store to drain.
+__device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, const double2* __restrict__ b, double2* ring,
+                                            int n1, int H, bool reverse, double omega, int tid, int nth, double2* rout,
+                                            const double2* xcoarse, int n1c, unsigned long long* mbar,
+                                            unsigned long long* clk = nullptr) {
+  constexpr int NS = MG_TRI_SLOTS;
+  const int RR = NS * H;
+  const int nb = (n1 + H - 1) / H;
+  auto band_rows = [&](int band, int& j0, int& cnt) {
+    j0 = band * H;
+    cnt = (min(n1, j0 + H) - j0) * n1;
+  };
+  // band copies: TMA bulk copies on the slot mbarriers; with xcoarse (first post-smoothing sweep) the threads copy
+  // and add the coarse-grid correction x += P x_c on the way in (mg_up's arithmetic)
+  unsigned* phase_word = reinterpret_cast<unsigned*>(mbar + NS);
+  unsigned phase = *phase_word;
+  const bool tma = xcoarse == nullptr;
+  auto load_band = [&](int band) {
+    int j0, cnt;
+    band_rows(band, j0, cnt);
+    double2* dst = ring + (band % NS) * H * n1;
+    const double2* src = x + (long)j0 * n1;
+    if (tma) {
+      bulk_load(dst, src, (unsigned)cnt * sizeof(double2), mbar + band % NS);
+      return;
+    }
+    for (int e = tid; e < cnt; e += nth) {
+      const int jj = e / n1, j = j0 + jj, i = e - jj * n1;
+      double2 v = src[e];
+      if (j >= 1 && j <= n1 - 2 && i >= 1 && i <= n1 - 2) {
+        double wy[3], wx[3];
+        const int by = q2_prow(j, wy), bx = q2_prow(i, wx);
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int ob = 0; ob < 3; ++ob)
+#pragma unroll
+          for (int oa = 0; oa < 3; ++oa) {
+            const double ww = wy[ob] * wx[oa];
+            if (ww != 0.0) acc = cfma(ww, xcoarse[(by + ob) * n1c + bx + oa], acc);
+          }
+        v = cadd(v, acc);
+      }
+      dst[e] = v;
+    }
+  };
+  auto wait_band = [&](int band) {
+    if (!tma) return;
+    const int sl = band % NS;
+    mbar_wait(mbar + sl, (phase >> sl) & 1u);
+    phase ^= 1u << sl;
+  };
+  auto store_band = [&](int band) {
+    int j0, cnt;
+    band_rows(band, j0, cnt);
+    bulk_store(x + (long)j0 * n1, ring + (band % NS) * H * n1, (unsigned)cnt * sizeof(double2));
+  };
+  auto copy_back = [&](int band) {
+    int j0, cnt;
+    band_rows(band, j0, cnt);
+    const double2* src = ring + (band % NS) * H * n1;
+    double2* dst = x + (long)j0 * n1;
+    for (int e = tid; e < cnt; e += nth) dst[e] = src[e];
+  };
+  // this thread's item: row class slot p (band lag 2 p), row kk of that class within the band, triple m
+  const int ntr = (n1 - 2) / 3 + 1;
+  const int per = (H / 3) * ntr;
+  const bool has = tid < 3 * per;
+  // the copy thread: the last thread when it has no item of its own
+  const bool copier = tid == (nth - 1 >= 3 * per ? nth - 1 : 0);
+  fence_async_global();   // generic writes of the iterate (previous passes, zeroing) before the async-proxy reads
+  __syncthreads();
+  if (tma) {
+    if (copier) {
+      load_band(0);
+      if (nb > 1) load_band(1);
+    }
+  } else {
+    load_band(0);
+    if (nb > 1) load_band(1);
+  }
+  int p = 0, kk = 0, m = 0;
+  if (has) {
+    p = tid / per;
+    const int rem = tid - p * per;
+    kk = rem / ntr;
+    m = rem - kk * ntr;
+  }
+  const int rowoff = (reverse ? 2 - p : p) + 3 * kk;
+  const int i0 = 3 * m, px = m & 1;
+  int gc[3];     // global columns of the local nodes (update order)
+  bool act[3];
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    gc[n] = reverse ? i0 + 2 - n : i0 + n;
+    act[n] = gc[n] >= 1 && gc[n] <= n1 - 2;
+  }
+  const int rrow = p * (H / 3) + kk;   // residual item: row rrow of band T - 5, the same triple
+  const double2 zero = make_double2(0.0, 0.0);
+  double2 bn[3] = {zero, zero, zero};
+  if (has && p == 0 && rowoff >= 1 && rowoff <= n1 - 2) {   // step 0: band 0 for p = 0
+#pragma unroll
+    for (int n = 0; n < 3; ++n)
+      if (act[n]) bn[n] = b[(long)rowoff * n1 + gc[n]];
+  }
+  int slot = (NS - 2 * p) % NS;   // ring slot of this item's band T - 2 p at T = 0 (p <= 2)
+  unsigned long long pt = clk ? clock64() : 0ull;
+  auto pmark = [&](int sl) {
+    if (clk) {
+      const unsigned long long t1 = clock64();
+      clk[sl] += t1 - pt;
+      pt = t1;
+    }
+  };
+  for (int T = 0; T <= nb + 4; ++T) {
+    if (T == 0) wait_band(0);
+    if (T + 1 < nb) wait_band(T + 1);
+    pmark(16);
+    if (tma) fence_async_smem();   // this thread's ring writes (step T - 1) -> visible to the bulk store
+    __syncthreads();
+    pmark(17);
+    if (tma) {
+      if (copier) {
+        bulk_wait_read1();          // all but the latest store have read their slot: band T - 7's slot is free
+        if (T + 2 < nb) load_band(T + 2);
+        if (T - 5 >= 0 && T - 5 < nb) store_band(T - 5);
+      }
+    } else {
+      if (T - 6 >= 0 && T - 6 < nb) copy_back(T - 6);
+      if (T + 2 < nb) load_band(T + 2);
+    }
+    pmark(18);
+    const int band = T - 2 * p;
+    const int j = band * H + rowoff;
+    const bool on = has && band >= 0 && band < nb && j >= 1 && j <= n1 - 2;
+    const int r0 = slot * H + rowoff;
+    slot = slot == NS - 1 ? 0 : slot + 1;
+    double2 acc[3] = {make_double2(-bn[0].x, -bn[0].y), make_double2(-bn[1].x, -bn[1].y),
+                      make_double2(-bn[2].x, -bn[2].y)};
+    {   // right-hand side of the next step's row
+      const int j1 = j + H;
+      const bool on1 = has && band + 1 >= 0 && band + 1 < nb && j1 >= 1 && j1 <= n1 - 2;
+#pragma unroll
+      for (int n = 0; n < 3; ++n) bn[n] = (on1 && act[n]) ? b[(long)j1 * n1 + gc[n]] : zero;
+    }
+    if (reverse) tri_step<true>(tabl, ring, n1, RR, j, r0, i0, px, on, act, omega, acc);
+    else tri_step<false>(tabl, ring, n1, RR, j, r0, i0, px, on, act, omega, acc);
+    pmark(19);
+    // fused residual (last pre-smoothing sweep, forward order) of band T - 5
+    if (rout != nullptr) {
+      const int F = T - 5;
+      const int jr = F * H + rrow;
+      if (has && F >= 0 && F < nb && jr >= 1 && jr <= n1 - 2) {
+        double2 bb[3];
+#pragma unroll
+        for (int n = 0; n < 3; ++n) bb[n] = act[n] ? b[(long)jr * n1 + i0 + n] : zero;
+        double2 ra[3] = {zero, zero, zero};
+        const int rr0 = (F % NS) * H + rrow;
+        const int pyr = jr & 1;
+        const double* Ta = tabl + (px | (pyr << 1)) * (ClassTab<2>::NT + 1);
+        const double* Tb = tabl + ((px ^ 1) | (pyr << 1)) * (ClassTab<2>::NT + 1);
+        if (pyr) tri_accumulate<false, 1, true>(Ta, Tb, ring, rr0, RR, n1, i0 - 2, ra, nullptr);
+        else tri_accumulate<false, 0, true>(Ta, Tb, ring, rr0, RR, n1, i0 - 2, ra, nullptr);
+#pragma unroll
+        for (int n = 0; n < 3; ++n)
+          if (act[n]) rout[(long)jr * n1 + i0 + n] = csub(bb[n], ra[n]);
+      }
+      pmark(14);
+    }
+  }
+  if (tma) {
+    __syncthreads();
+    if (copier) {
+      bulk_wait_all();
+      fence_async_global();
+    }
+    if (tid == 0) *phase_word = phase;
+  } else {
+    __syncthreads();
+    for (int band = max(0, nb + 4 - 5); band < nb; ++band) copy_back(band);
+  }
+  __syncthreads();
+}
+
 // Returns true if the band-wavefront path also wrote the residual b - A x of the final iterate to rout.
 template <int DIM, int ORD, bool CONV, bool W, bool TAB>
 __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
@@ -1218,19 +1484,22 @@ __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const d
                                           const double* tabl, double2* ring = nullptr,
                                           int waveH = 0, int flat_max = 0, double2* rout = nullptr,
                                           const double2* xcoarse = nullptr, int n1c = 0, bool zwave = false,
-                                          unsigned long long* mbar = nullptr) {
+                                          unsigned long long* mbar = nullptr, unsigned long long* clk = nullptr) {
   constexpr int C1 = ORD == 2 ? 3 : 2;
   constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
   if constexpr (TAB && ORD == 2 && DIM == 2 && !W) {
     if (ring && waveH) {
-      const double2 cc = CONV ? cf.c : make_double2(0.0, 0.0);
       for (int sw = 0; sw < sweeps; ++sw) {
         double2* rr = (sw == sweeps - 1 && !reverse) ? rout : nullptr;
         const double2* xcs = sw == 0 ? xcoarse : nullptr;
-        if (waveH == 6)
-          q2_wave_pass<6, CONV>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cc, rr, xcs, n1c, mbar);
-        else
-          q2_wave_pass<3, CONV>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cc, rr, xcs, n1c, mbar);
+        if constexpr (CONV) {
+          if (waveH == 6)
+            q2_wave_pass<6>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cf.c, rr, xcs, n1c, mbar);
+          else
+            q2_wave_pass<3>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cf.c, rr, xcs, n1c, mbar);
+        } else {
+          q2_tri_pass(tabl, x, b, ring, g.n1, waveH, reverse, omega, tid, nth, rr, xcs, n1c, mbar, clk);
+        }
       }
       return rout != nullptr && sweeps > 0 && !reverse;
     }
@@ -1394,7 +1663,7 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
   const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
                                                        : ClassTab<DIM>::PER_LEVEL) : nullptr;
   // profiling (AAO_MG_CLOCK): split of the level-0 down-leg into sweeps / residual / restriction
-  const bool pclk = DIM == 2 && a.clk != nullptr && blockIdx.x == 0 && tid == 0 && l == 0;
+  const bool pclk = DIM == 2 && a.clk != nullptr && blockIdx.x == a.clk_block && tid == 0 && l == 0;
   unsigned long long pt = pclk ? clock64() : 0ull;
   auto pmark = [&](int slot) {
     if (pclk) {
@@ -1403,12 +1672,13 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
       pt = t1;
     }
   };
-  const bool wv = a.wave_h && l < a.lsm && g.n1 >= a.wave_min;
+  const bool wv = a.wave_hl[l] > 0;
   double2* rl = S.R(l);
   const bool fused = cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, bl, a.pre, false, a.omega, tid, nth, tabl,
-                                                       wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0,
+                                                       wv ? S.smem + a.ring_off : nullptr, a.wave_hl[l],
                                                        a.flat_max, wv ? rl : nullptr, nullptr, 0,
-                                                       DIM == 3 && l < a.lsm && g.n1 >= a.zwave_min, S.MBAR());
+                                                       DIM == 3 && l < a.lsm && g.n1 >= a.zwave_min, S.MBAR(),
+                                                       pclk ? a.clk : nullptr);
   pmark(2 * MG_MAXL - 2);
   const double* cvl = S.CV(l);
   if (fused) {
@@ -1543,7 +1813,7 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
   const Transfer t = a.t[l];
   double2* xl = S.X(l);
   const double2* xc = S.X(l + 1);
-  const bool wv = a.wave_h && l < a.lsm && g.n1 >= a.wave_min;
+  const bool wv = a.wave_hl[l] > 0;
   const bool fuse_prolong = TAB && ORD == 2 && DIM == 2 && !W && wv && a.post > 0;
   if (!fuse_prolong) {
   cta_all_unknowns<DIM, ORD>(g.n1, tid, nth, [&](const int* c, int i) {
@@ -1587,7 +1857,7 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
   const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
                                                    : ClassTab<DIM>::PER_LEVEL) : nullptr;
   cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl,
-                                    wv ? S.smem + a.ring_off : nullptr, wv ? a.wave_h : 0, a.flat_max, nullptr,
+                                    wv ? S.smem + a.ring_off : nullptr, a.wave_hl[l], a.flat_max, nullptr,
                                     fuse_prolong ? xc : nullptr, gc.n1, DIM == 3 && l < a.lsm && g.n1 >= a.zwave_min,
                                     S.MBAR());
 }
@@ -1597,13 +1867,14 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
 #ifndef MG_THREADS_3D
 #define MG_THREADS_3D 512
 #endif
-template <int DIM, bool TAB>
+template <int DIM, bool TAB, bool CONV>
 constexpr int mg_threads() {
-  return DIM == 3 ? MG_THREADS_3D : (TAB ? MG_THREADS_TAB : MG_THREADS);
+  // 2-D real class stencils: one thread per triple of the band-wavefront sweeps (3 x 171 triples on a 513^2 level)
+  return DIM == 3 ? MG_THREADS_3D : (TAB ? (CONV ? MG_THREADS_TAB : MG_TRI_THREADS) : MG_THREADS);
 }
 
 template <int DIM, int ORD, bool CONV, bool TAB>
-__global__ void __launch_bounds__(mg_threads<DIM, TAB>(), 1) k_mg_cta(MGArgs a) {
+__global__ void __launch_bounds__(mg_threads<DIM, TAB, CONV>(), 1) k_mg_cta(MGArgs a) {
   extern __shared__ double2 smem[];
   const int p = blockIdx.x;
   const int L = a.nlev;
@@ -1623,11 +1894,16 @@ __global__ void __launch_bounds__(mg_threads<DIM, TAB>(), 1) k_mg_cta(MGArgs a) 
     __syncthreads();
   }
   if constexpr (TAB && ORD == 2 && DIM == 2) {
-    if (a.wave_h && tid == 0) {   // band-ring mbarriers (8 slots) and their phase word, after the largest ring
-      unsigned long long* mb = reinterpret_cast<unsigned long long*>(smem + a.mbar_off);
-      for (int sl = 0; sl < 8; ++sl) mbar_init(mb + sl, 1);
-      *reinterpret_cast<unsigned*>(mb + 8) = 0u;
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (a.wave_h) {
+      // the ring and its guard columns start as zeros: the triple-form sweeps read up to three entries beyond a row
+      // (they only meet zero coefficients or inactive nodes, but must be finite)
+      for (long e = a.ring_off - MG_RING_GUARD + tid; e < a.mbar_off; e += nth) smem[e] = make_double2(0.0, 0.0);
+      if (tid == 0) {   // band-ring mbarriers (8 slots) and their phase word, after the ring
+        unsigned long long* mb = reinterpret_cast<unsigned long long*>(smem + a.mbar_off);
+        for (int sl = 0; sl < MG_TRI_SLOTS; ++sl) mbar_init(mb + sl, 1);
+        *reinterpret_cast<unsigned*>(mb + MG_TRI_SLOTS) = 0u;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
     }
     __syncthreads();
   }
@@ -1636,7 +1912,7 @@ __global__ void __launch_bounds__(mg_threads<DIM, TAB>(), 1) k_mg_cta(MGArgs a) 
   double2* x0 = S.X(0);
   for (int i = tid; i < (int)a.g[0].n; i += nth) x0[i] = make_double2(0.0, 0.0);
   __syncthreads();
-  const bool clk = a.clk != nullptr && blockIdx.x == 0 && tid == 0;
+  const bool clk = a.clk != nullptr && blockIdx.x == a.clk_block && tid == 0;
   unsigned long long t0 = clk ? clock64() : 0ull;
   auto mark = [&](int slot) {
     if (clk) {
@@ -1858,13 +2134,13 @@ static void mgcta_t(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
     attr = true;
   }
   if (a.op.conv_sel != 0 && ORD == 2 && a.use_ctab)
-    k_mg_cta<DIM, ORD, true, (ORD == 2)><<<nprob, mg_threads<DIM, true>(), smem, s>>>(a);
+    k_mg_cta<DIM, ORD, true, (ORD == 2)><<<nprob, mg_threads<DIM, true, true>(), smem, s>>>(a);
   else if (a.op.conv_sel != 0)
-    k_mg_cta<DIM, ORD, true, false><<<nprob, mg_threads<DIM, false>(), smem, s>>>(a);
+    k_mg_cta<DIM, ORD, true, false><<<nprob, mg_threads<DIM, false, true>(), smem, s>>>(a);
   else if (ORD == 2 && a.use_ctab)
-    k_mg_cta<DIM, ORD, false, (ORD == 2)><<<nprob, mg_threads<DIM, true>(), smem, s>>>(a);
+    k_mg_cta<DIM, ORD, false, (ORD == 2)><<<nprob, mg_threads<DIM, true, false>(), smem, s>>>(a);
   else
-    k_mg_cta<DIM, ORD, false, false><<<nprob, mg_threads<DIM, false>(), smem, s>>>(a);
+    k_mg_cta<DIM, ORD, false, false><<<nprob, mg_threads<DIM, false, false>(), smem, s>>>(a);
 }
 void launch_mg_cta(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
   SWITCH_DO(a.g[0], mgcta_t, a, nprob, smem, s);

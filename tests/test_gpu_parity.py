@@ -352,13 +352,16 @@ def test_arnoldi_hessenberg_parity(cfg):
     assert np.max(np.abs(ritz_g - ritz_o)) <= 1e-7 * np.max(np.abs(ritz_o))
 
 
+@pytest.mark.parametrize("hmax", ["3", "6", "24"])
 @pytest.mark.parametrize("cfg", [SMALL[0], SMALL[1], SMALL[3], SMALL[5], SMALL[6]], ids=lambda c: c.name)
-def test_band_wavefront_sweeps_match_oracle(cfg, monkeypatch):
+def test_band_wavefront_sweeps_match_oracle(cfg, hmax, monkeypatch):
     """The band-wavefront colour fusion (default only for n1 >= 257) forced on every small level: the same
-    map as the per-colour sweeps (ring wrap, partial last band, odd/even n_b, Oseen operators)."""
+    map as the per-colour sweeps (ring wrap and partial last band with 3-row bands, whole level in one or two
+    bands with 24-row bands, odd/even n_b, Oseen operators in the node-per-thread form)."""
     torch = _torch()
     monkeypatch.setenv("AAO_WAVE", "1")
     monkeypatch.setenv("AAO_WAVE_MIN", "9")
+    monkeypatch.setenv("AAO_WAVE_H", hmax)
     _, pc = oracle_for(cfg)
     ctx = gpu_ctx(cfg)
     r = synth.probe_vector(cfg)

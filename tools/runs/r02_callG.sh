@@ -1,0 +1,9 @@
+#!/bin/bash
+python -c "import __graft_entry__ as g; g.build()" > /tmp/build.log 2>&1 || { tail -20 /tmp/build.log; exit 1; }
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "wavefront or c4_64" 2>&1 | tail -4
+for blk in 0 64 127; do AAO_MG_CLOCK=$blk timeout 300 python tools/run_precond.py --config c4_64 --reps 1 2>&1 | grep "order 2" | tail -1; done
+nvidia-smi --query-gpu=clocks.sm,power.draw,clocks_event_reasons.sw_power_cap --format=csv,noheader -lms 100 > gpurun_out/smi_c4_64.log &
+SMI=$!
+for cfg in c4_32 c4_64 c4_512; do timeout 300 python tools/run_precond.py --config $cfg --reps 20; done
+kill $SMI
+sort gpurun_out/smi_c4_64.log | uniq -c | sort -rn | head -12
