@@ -243,8 +243,11 @@ __device__ __forceinline__ void block_sum_many(const double* acc, int cnt, bool 
   __syncthreads();
 }
 
+// KMAX = 32 runs one CTA per SM so that a thread can hold the 32 basis values of its element in registers between
+// the update and the Gram dots of pass 2 (with two CTAs per SM and 128 registers the second use re-read them through
+// L2: measured 2.9-3.4 TB/s against 5.8 TB/s for KMAX = 16 on c4 at n_t = 512).
 template <int KMAX>
-__global__ void __launch_bounds__(MGSW_THREADS, 2)
+__global__ void __launch_bounds__(MGSW_THREADS, KMAX > 16 ? 1 : 2)
     k_mgs_icwy(double* __restrict__ w, const double* const* __restrict__ V, int k, long n2,
                double* __restrict__ H, double* __restrict__ partial, double* __restrict__ G, int ldg) {
   constexpr int NA = KMAX + 1;
@@ -293,18 +296,20 @@ __global__ void __launch_bounds__(MGSW_THREADS, 2)
   for (int i = 0; i < NA; ++i) acc[i] = 0.0;
   for (long e = tid; e < cnt; e += T) {
     double2 x = w2[e];
+    double2 v[KMAX];
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) v[i] = i < K1 ? __ldcs(vp[i] + e) : make_double2(0.0, 0.0);
 #pragma unroll
     for (int i = 0; i < KMAX; ++i) {
       if (i < K1) {
-        const double2 v = __ldg(vp[i] + e);
-        x.x = fma(-hs[i], v.x, x.x);
-        x.y = fma(-hs[i], v.y, x.y);
+        x.x = fma(-hs[i], v[i].x, x.x);
+        x.y = fma(-hs[i], v[i].y, x.y);
       }
     }
     w2[e] = x;
 #pragma unroll
     for (int i = 0; i < KMAX; ++i)
-      if (i < K1) acc[i] += dot2(x, __ldg(vp[i] + e));
+      if (i < K1) acc[i] += dot2(x, v[i]);
     acc[KMAX] += dot2(x, x);
   }
   block_sum_many<NA>(acc, K1, true, red, bs);
@@ -480,11 +485,14 @@ cudaError_t launch_mgs(double* w, const double* const* V, int k, long n, double*
     long n2 = n / 2;
     void* args[] = {&w, (void*)&V, &k, &n2, &H, &partial, &G, &ldg};
     void* fn = k < 8 ? (void*)k_mgs_icwy<8> : k < 16 ? (void*)k_mgs_icwy<16> : (void*)k_mgs_icwy<32>;
-    static int bpsm = 0;
-    if (bpsm == 0) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, k_mgs_icwy<32>, MGSW_THREADS, 0);
-      bpsm = std::max(1, std::min(bpsm, 4));
+    static int bpsm16 = 0, bpsm32 = 0;
+    if (bpsm16 == 0) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm16, k_mgs_icwy<16>, MGSW_THREADS, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm32, k_mgs_icwy<32>, MGSW_THREADS, 0);
+      bpsm16 = std::max(1, std::min(bpsm16, 2));
+      bpsm32 = std::max(1, std::min(bpsm32, 1));
     }
+    const int bpsm = k < 16 ? bpsm16 : bpsm32;
     return cudaLaunchCooperativeKernel(fn, dim3(bpsm * mgs_blocks()), dim3(MGSW_THREADS), args, 0, s);
   }
   int nb = mgs_blocks();
