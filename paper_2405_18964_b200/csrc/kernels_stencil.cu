@@ -18,6 +18,13 @@ namespace aao {
 #ifndef MG_THREADS_TAB
 #define MG_THREADS_TAB 512
 #endif
+// 2-D Q1 (pressure) solves: threads per CTA and CTAs per SM of the CTA-resident MG and Chebyshev kernels
+#ifndef MG_THREADS_Q1
+#define MG_THREADS_Q1 512
+#endif
+#ifndef MG_MINB_Q1
+#define MG_MINB_Q1 1
+#endif
 
 // ---------------------------------------------------------------- complex helpers
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -1867,14 +1874,19 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
 #ifndef MG_THREADS_3D
 #define MG_THREADS_3D 512
 #endif
-template <int DIM, bool TAB, bool CONV>
+template <int DIM, bool TAB, bool CONV, int ORD = 2>
 constexpr int mg_threads() {
   // 2-D real class stencils: one thread per triple of the band-wavefront sweeps (3 x 171 triples on a 513^2 level)
-  return DIM == 3 ? MG_THREADS_3D : (TAB ? (CONV ? MG_THREADS_TAB : MG_TRI_THREADS) : MG_THREADS);
+  return DIM == 3 ? MG_THREADS_3D
+                  : (TAB ? (CONV ? MG_THREADS_TAB : MG_TRI_THREADS) : (ORD == 1 ? MG_THREADS_Q1 : MG_THREADS));
+}
+template <int DIM, int ORD>
+constexpr int mg_minb() {
+  return DIM == 2 && ORD == 1 ? MG_MINB_Q1 : 1;
 }
 
 template <int DIM, int ORD, bool CONV, bool TAB>
-__global__ void __launch_bounds__(mg_threads<DIM, TAB, CONV>(), 1) k_mg_cta(MGArgs a) {
+__global__ void __launch_bounds__(mg_threads<DIM, TAB, CONV, ORD>(), mg_minb<DIM, ORD>()) k_mg_cta(MGArgs a) {
   extern __shared__ double2 smem[];
   const int p = blockIdx.x;
   const int L = a.nlev;
@@ -1947,7 +1959,7 @@ __global__ void __launch_bounds__(mg_threads<DIM, TAB, CONV>(), 1) k_mg_cta(MGAr
 
 // Chebyshev semi-iteration on a mass matrix, one CTA per problem
 template <int DIM, int ORD>
-__global__ void __launch_bounds__(MG_THREADS, 1) k_cheb_cta(Grid g, View bv, View xv, double2* rw, double2* d0w, double2* d1w,
+__global__ void __launch_bounds__(mg_threads<DIM, false, false, ORD>(), mg_minb<DIM, ORD>()) k_cheb_cta(Grid g, View bv, View xv, double2* rw, double2* d0w, double2* d1w,
                                                    double theta, double sigma, double delta, int iters, double scale) {
   const int p = blockIdx.x;
   const double2* b = bv.p + voff(bv, p, g.n);
@@ -2136,11 +2148,11 @@ static void mgcta_t(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
   if (a.op.conv_sel != 0 && ORD == 2 && a.use_ctab)
     k_mg_cta<DIM, ORD, true, (ORD == 2)><<<nprob, mg_threads<DIM, true, true>(), smem, s>>>(a);
   else if (a.op.conv_sel != 0)
-    k_mg_cta<DIM, ORD, true, false><<<nprob, mg_threads<DIM, false, true>(), smem, s>>>(a);
+    k_mg_cta<DIM, ORD, true, false><<<nprob, mg_threads<DIM, false, true, ORD>(), smem, s>>>(a);
   else if (ORD == 2 && a.use_ctab)
     k_mg_cta<DIM, ORD, false, (ORD == 2)><<<nprob, mg_threads<DIM, true, false>(), smem, s>>>(a);
   else
-    k_mg_cta<DIM, ORD, false, false><<<nprob, mg_threads<DIM, false, false>(), smem, s>>>(a);
+    k_mg_cta<DIM, ORD, false, false><<<nprob, mg_threads<DIM, false, false, ORD>(), smem, s>>>(a);
 }
 void launch_mg_cta(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
   SWITCH_DO(a.g[0], mgcta_t, a, nprob, smem, s);
@@ -2149,7 +2161,8 @@ void launch_mg_cta(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
 template <int DIM, int ORD>
 static void chcta_t(const Grid& g, View b, View x, double2* r, double2* d0, double2* d1, double theta, double sigma,
                     double delta, int iters, double scale, int nprob, cudaStream_t s) {
-  k_cheb_cta<DIM, ORD><<<nprob, MG_THREADS, 0, s>>>(g, b, x, r, d0, d1, theta, sigma, delta, iters, scale);
+  k_cheb_cta<DIM, ORD><<<nprob, mg_threads<DIM, false, false, ORD>(), 0, s>>>(g, b, x, r, d0, d1, theta, sigma, delta,
+                                                                            iters, scale);
 }
 void launch_cheb_cta(const Grid& g, View b, View x, double2* r, double2* d0, double2* d1, double theta, double sigma,
                      double delta, int iters, double scale, int nprob, cudaStream_t s) {
