@@ -892,7 +892,7 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
   // c3 255 -> 330 ms, so Oseen operators use it only when forced).  AAO_WAVE=0/1 forces it off/on for every eligible
   // level >= AAO_WAVE_MIN (parity-tested).  Real operators sweep in triple form, one thread per node triple: the band
   // height of a level is the largest H in {24, 12, 6, 3} whose H rows of triples fit the CTA's threads and whose
-  // 9-slot ring fits the shared memory left (513^2: 3, 257^2: 6, 129^2: 12, 65^2: 24).
+  // 9-slot ring fits the shared memory left (513^2: 3, 257^2: 6, 129^2: 6, 65^2: 12, 33^2: 24); a row takes whole warps.
   a.wave_h = 0;
   for (int l = 0; l < MG_MAXL; ++l) a.wave_hl[l] = 0;
   const bool wave_on = c.wave_force >= 0 ? c.wave_force != 0 : a.g[0].n1 >= c.wave_min;
@@ -913,7 +913,9 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
       } else {
         const int ntr = (n1 - 2) / 3 + 1;
         for (int cand = c.wave_hmax; cand >= 3 && !h; cand /= 2)
-          if (cand * ntr <= MG_TRI_THREADS && (size_t)MG_TRI_SLOTS * cand * n1 * sizeof(double2) <= cap) h = cand;
+          if (cand * mg_tri_lanes_per_row(ntr) <= MG_TRI_THREADS &&
+              (size_t)MG_TRI_SLOTS * cand * n1 * sizeof(double2) <= cap)
+            h = cand;
       }
       a.wave_hl[l] = h;
       if (h) ring = std::max(ring, (size_t)(op.conv_sel != 0 ? 8 : MG_TRI_SLOTS) * h * n1 * sizeof(double2));

@@ -59,8 +59,16 @@ struct FreqConst {
 
 // Arguments of the CTA-resident multigrid solve (one CTA per problem, all levels and cycles).
 constexpr int MG_MAXL = 12;
-constexpr int MG_TRI_THREADS = 544;    // threads per CTA of the 2-D Q2 real class-stencil MG: one per triple of a
-                                       // band-wavefront step (3 rows x 171 triples on a 513^2 level), 120 registers
+constexpr int MG_TRI_THREADS = 576;    // threads per CTA of the 2-D Q2 real class-stencil MG: one per triple of a
+                                       // band-wavefront step, rows padded to whole warps (3 rows x 192 lanes for the
+                                       // 171 triples of a 513^2 level); 96 registers (as for any count in 513..640)
+// lanes a row of ntr triples takes in that mapping
+inline int mg_tri_lanes_per_row(int ntr) {
+  if (ntr >= 32) return (ntr + 31) / 32 * 32;
+  int l = 1;
+  while (l < ntr) l *= 2;
+  return l;
+}
 constexpr int MG_RING_GUARD = 4;       // zeroed double2 entries before and after the band ring
 constexpr int MG_TRI_SLOTS = 9;        // band slots of the triple-form ring (8 for the node-per-thread Oseen form)
 constexpr int MG_SMEM_MAX = 232448;    // dynamic shared memory per CTA (227 KB opt-in on sm_100)

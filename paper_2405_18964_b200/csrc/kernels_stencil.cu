@@ -1195,6 +1195,14 @@ __device__ void q2_wave_pass(const double* tabl, double2* x, const double2* __re
 // reversed order is the mirror image: local column c stands for i0 + 4 - c, local tap oa for 4 - oa.
 // Columns -2, -1 (m = 0) and n1 .. n1 + 2 (last triple) fall into the neighbouring ring rows or the zeroed guard
 // around the ring; they only meet zero coefficients (midpoint rows have three taps) or inactive boundary nodes.
+// lanes a row of ntr triples takes in the thread mapping of q2_tri_pass
+__host__ __device__ __forceinline__ int tri_lanes_per_row(int ntr) {
+  if (ntr >= 32) return (ntr + 31) / 32 * 32;
+  int l = 1;
+  while (l < ntr) l *= 2;
+  return l;
+}
+
 template <bool REV, int PY, bool FULL>
 __device__ __forceinline__ void tri_accumulate(const double* __restrict__ Ta, const double* __restrict__ Tb,
                                                const double2* ring, int r0, int RR, int n1, int cb, double2* acc,
@@ -1241,9 +1249,16 @@ __device__ __forceinline__ void tri_accumulate(const double* __restrict__ Ta, co
 }
 
 // one band step of the triple-form sweep for this thread's item (see q2_tri_pass)
+// x-colour phases synchronise only the threads of one row class (named barrier 1 + p, a whole number of warps):
+// updates of different row classes touch rows at least four apart and never exchange values within a step.
+__device__ __forceinline__ void class_sync(int bar_id, int bar_threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(bar_threads) : "memory");
+}
+
 template <bool REV>
 __device__ __forceinline__ void tri_step(const double* tabl, double2* ring, int n1, int RR, int j, int r0, int i0,
-                                         int px, bool on, const bool* act, double omega, double2* acc) {
+                                         int px, bool on, const bool* act, double omega, double2* acc, int bar_id,
+                                         int bar_threads) {
   const int cb = REV ? i0 + 4 : i0 - 2;
   const int py = j & 1;
   // class stencils of the x-parity of nodes 0 and 2 (Ta) and of node 1 (Tb); lanes alternate in parity, the two
@@ -1271,7 +1286,7 @@ __device__ __forceinline__ void tri_step(const double* tabl, double2* ring, int 
     x0n = make_double2(xo[0].x - wa * acc[0].x, xo[0].y - wa * acc[0].y);
     rowj[REV ? -2 : 2] = x0n;
   }
-  __syncthreads();
+  class_sync(bar_id, bar_threads);
   // second x-colour: fresh taps = own first node and the first node of the next triple
   double2 x1n = xo[1];
   double2 v5 = make_double2(0.0, 0.0);
@@ -1284,7 +1299,7 @@ __device__ __forceinline__ void tri_step(const double* tabl, double2* ring, int 
       rowj[REV ? -3 : 3] = x1n;
     }
   }
-  __syncthreads();
+  class_sync(bar_id, bar_threads);
   // third x-colour
   if (on && act[2]) {
     const double2 v6 = rowj[REV ? -6 : 6];
@@ -1364,12 +1379,15 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
     double2* dst = x + (long)j0 * n1;
     for (int e = tid; e < cnt; e += nth) dst[e] = src[e];
   };
-  // this thread's item: row class slot p (band lag 2 p), row kk of that class within the band, triple m
+  // this thread's item: row class slot p (band lag 2 p), row kk of that class within the band, triple m.  A row
+  // takes lpr lanes (tri_lanes_per_row: whole warps, or a power-of-two fraction of a warp on small levels), so the
+  // threads of a row class are whole warps: they synchronise among themselves, and on the big levels a warp works
+  // on one row (one row parity: no divergence between the 5-row and 3-row stencils).
   const int ntr = (n1 - 2) / 3 + 1;
-  const int per = (H / 3) * ntr;
-  const bool has = tid < 3 * per;
-  // the copy thread: the last thread when it has no item of its own
-  const bool copier = tid == (nth - 1 >= 3 * per ? nth - 1 : 0);
+  const int lpr = tri_lanes_per_row(ntr);
+  const int per = (H / 3) * lpr;            // threads of one row class
+  // the copy thread: the block's last thread (a spare lane: ntr < lpr on every level with n1 = 2^k + 1)
+  const bool copier = tid == nth - 1;
   fence_async_global();   // generic writes of the iterate (previous passes, zeroing) before the async-proxy reads
   __syncthreads();
   if (tma) {
@@ -1382,12 +1400,19 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
     if (nb > 1) load_band(1);
   }
   int p = 0, kk = 0, m = 0;
+  bool has = tid < 3 * per;
   if (has) {
     p = tid / per;
     const int rem = tid - p * per;
-    kk = rem / ntr;
-    m = rem - kk * ntr;
+    kk = rem / lpr;
+    m = rem - kk * lpr;
+    has = m < ntr;
   }
+  // barrier group of the x-colour phases: the row class (whole warps), or the whole block where a class is a
+  // fraction of a warp (small levels with forced 3- or 6-row bands)
+  const bool grouped = (per & 31) == 0;
+  const bool in_class = !grouped || tid < 3 * per;
+  const int bar_id = grouped ? 1 + p : 0, bar_threads = grouped ? per : nth;
   const int rowoff = (reverse ? 2 - p : p) + 3 * kk;
   const int i0 = 3 * m, px = m & 1;
   int gc[3];     // global columns of the local nodes (update order)
@@ -1445,8 +1470,10 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
 #pragma unroll
       for (int n = 0; n < 3; ++n) bn[n] = (on1 && act[n]) ? b[(long)j1 * n1 + gc[n]] : zero;
     }
-    if (reverse) tri_step<true>(tabl, ring, n1, RR, j, r0, i0, px, on, act, omega, acc);
-    else tri_step<false>(tabl, ring, n1, RR, j, r0, i0, px, on, act, omega, acc);
+    if (in_class) {
+      if (reverse) tri_step<true>(tabl, ring, n1, RR, j, r0, i0, px, on, act, omega, acc, bar_id, bar_threads);
+      else tri_step<false>(tabl, ring, n1, RR, j, r0, i0, px, on, act, omega, acc, bar_id, bar_threads);
+    }
     pmark(19);
     // fused residual (last pre-smoothing sweep, forward order) of band T - 5
     if (rout != nullptr) {
