@@ -1317,10 +1317,14 @@ __device__ __forceinline__ void tri_step(const double* tabl, double2* ring, int 
 // (its stencils reach the last rows of band T - 6 and the first two rows -- row classes 0 and 1, final -- of band
 // T - 4): nothing this step writes is read by it, so it needs no barrier of its own.  The slot loaded at step T held
 // band T - 7, whose store was issued two steps earlier, so the copy thread never waits for the latest store to drain.
+// N1C / HC: the level size and band height as compile-time constants for the two big levels of the BASELINE
+// meshes (513 / 3 and 257 / 6), 0 = the run-time values (every other level; same code).
+template <int N1C, int HC>
 __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, const double2* __restrict__ b, double2* ring,
-                                            int n1, int H, bool reverse, double omega, int tid, int nth, double2* rout,
+                                            int n1r, int Hr, bool reverse, double omega, int tid, int nth, double2* rout,
                                             const double2* xcoarse, int n1c, unsigned long long* mbar,
                                             unsigned long long* clk = nullptr) {
+  const int n1 = N1C ? N1C : n1r, H = HC ? HC : Hr;
   constexpr int NS = MG_TRI_SLOTS;
   const int RR = NS * H;
   const int nb = (n1 + H - 1) / H;
@@ -1428,9 +1432,10 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
   if (has && p == 0 && rowoff >= 1 && rowoff <= n1 - 2) {   // step 0: band 0 for p = 0
 #pragma unroll
     for (int n = 0; n < 3; ++n)
-      if (act[n]) bn[n] = b[(long)rowoff * n1 + gc[n]];
+      if (act[n]) bn[n] = b[rowoff * n1 + gc[n]];
   }
   int slot = (NS - 2 * p) % NS;   // ring slot of this item's band T - 2 p at T = 0 (p <= 2)
+#ifdef AAO_TRI_CLOCK   // per-phase cycle accounting of the steps (build with -DAAO_TRI_CLOCK, run with AAO_MG_CLOCK)
   unsigned long long pt = clk ? clock64() : 0ull;
   auto pmark = [&](int sl) {
     if (clk) {
@@ -1439,6 +1444,9 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
       pt = t1;
     }
   };
+#else
+  auto pmark = [](int) {};
+#endif
   for (int T = 0; T <= nb + 4; ++T) {
     if (T == 0) wait_band(0);
     if (T + 1 < nb) wait_band(T + 1);
@@ -1468,7 +1476,7 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
       const int j1 = j + H;
       const bool on1 = has && band + 1 >= 0 && band + 1 < nb && j1 >= 1 && j1 <= n1 - 2;
 #pragma unroll
-      for (int n = 0; n < 3; ++n) bn[n] = (on1 && act[n]) ? b[(long)j1 * n1 + gc[n]] : zero;
+      for (int n = 0; n < 3; ++n) bn[n] = (on1 && act[n]) ? b[j1 * n1 + gc[n]] : zero;
     }
     if (in_class) {
       if (reverse) tri_step<true>(tabl, ring, n1, RR, j, r0, i0, px, on, act, omega, acc, bar_id, bar_threads);
@@ -1482,7 +1490,7 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
       if (has && F >= 0 && F < nb && jr >= 1 && jr <= n1 - 2) {
         double2 bb[3];
 #pragma unroll
-        for (int n = 0; n < 3; ++n) bb[n] = act[n] ? b[(long)jr * n1 + i0 + n] : zero;
+        for (int n = 0; n < 3; ++n) bb[n] = act[n] ? b[jr * n1 + i0 + n] : zero;
         double2 ra[3] = {zero, zero, zero};
         const int rr0 = (F % NS) * H + rrow;
         const int pyr = jr & 1;
@@ -1492,7 +1500,7 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
         else tri_accumulate<false, 0, true>(Ta, Tb, ring, rr0, RR, n1, i0 - 2, ra, nullptr);
 #pragma unroll
         for (int n = 0; n < 3; ++n)
-          if (act[n]) rout[(long)jr * n1 + i0 + n] = csub(bb[n], ra[n]);
+          if (act[n]) rout[jr * n1 + i0 + n] = csub(bb[n], ra[n]);
       }
       pmark(14);
     }
@@ -1532,7 +1540,12 @@ __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const d
           else
             q2_wave_pass<3>(tabl, x, b, ring, g.n1, reverse, omega, tid, nth, cv, cf.c, rr, xcs, n1c, mbar);
         } else {
-          q2_tri_pass(tabl, x, b, ring, g.n1, waveH, reverse, omega, tid, nth, rr, xcs, n1c, mbar, clk);
+          if (g.n1 == 513 && waveH == 3)
+            q2_tri_pass<513, 3>(tabl, x, b, ring, 513, 3, reverse, omega, tid, nth, rr, xcs, n1c, mbar, clk);
+          else if (g.n1 == 257 && waveH == 6)
+            q2_tri_pass<257, 6>(tabl, x, b, ring, 257, 6, reverse, omega, tid, nth, rr, xcs, n1c, mbar, clk);
+          else
+            q2_tri_pass<0, 0>(tabl, x, b, ring, g.n1, waveH, reverse, omega, tid, nth, rr, xcs, n1c, mbar, clk);
         }
       }
       return rout != nullptr && sweeps > 0 && !reverse;
