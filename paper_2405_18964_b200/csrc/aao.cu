@@ -861,6 +861,9 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
     const size_t per = (size_t)(1 << c.dim) * (op.conv_sel == 0 ? (nt + 1) : 2 * nt);
     tab_bytes = (a.nlev - 1) * per * sizeof(double);
     tab_bytes = (tab_bytes + 15) / 16 * 16;
+  } else if (!no_ctab && S.order == 1 && c.dim == 2 && op.conv_sel == 0 && a.nlev >= 2) {
+    a.use_ctab = 2;   // 2-D Q1 real operators: position-class stencils (90 doubles per smoothing level)
+    tab_bytes = ((size_t)(a.nlev - 1) * 90 * sizeof(double) + 15) / 16 * 16;
   }
   // shared-memory residency of the coarse levels (coarsest first while x and b fit).  Measured: 2-D Q2 with the
   // merged small-level visits keeps no level in shared memory (the L1 cache serves every level better than a

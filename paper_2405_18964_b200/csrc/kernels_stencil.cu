@@ -810,6 +810,52 @@ __device__ __forceinline__ double2 class_eval_conv_flat2(const double2* tabl, co
   return cadd(A, cmul(cc, N));
 }
 
+// ---------------------------------------------------------------- class stencils (2-D Q1, real operators)
+// The Q1 pressure operators (Neumann K_p, M_p; every node an unknown except the pinned corner, whose iterate is an
+// exact zero) have one stencil per position class: first / interior / last node along each axis, 3 x 3 classes of
+// 9 taps + 1 / A_ii.  Taps that would leave the grid have zero coefficients and are read at a clamped index.  One
+// table per level in shared memory replaces the per-node 1-D row loads and the separate M and K sums of
+// apply_MKC_generic (the pressure MG was bound by the L1 data path: 12 table loads per node, lanes diverging).
+constexpr int Q1TAB = 90;   // doubles per level: 9 classes x (9 taps + 1 / diagonal)
+
+__device__ void build_class_tab_q1(const Grid& g, double ca, double cb, double* tab, int tid, int nth) {
+  const int n1 = g.n1;
+  for (int e = tid; e < 81; e += nth) {
+    const int cls = e / 9, tap = e % 9;
+    const int oa = tap % 3, ob = tap / 3;
+    const int cx = cls % 3, cy = cls / 3;
+    const int ix = cx == 0 ? 0 : (cx == 2 ? n1 - 1 : 1), iy = cy == 0 ? 0 : (cy == 2 ? n1 - 1 : 1);
+    const double mx = g.tM[ix * 3 + oa], kx = g.tK[ix * 3 + oa];
+    const double my = g.tM[iy * 3 + ob], ky = g.tK[iy * 3 + ob];
+    tab[cls * 10 + tap] = ca * (my * mx) + cb * (ky * mx + my * kx);
+  }
+  __syncthreads();
+  for (int cls = tid; cls < 9; cls += nth) tab[cls * 10 + 9] = 1.0 / tab[cls * 10 + 4];
+}
+
+// (A x)_i at node (i, j) of a 2-D Q1 level from its class stencil; 1 / A_ii in invD
+__device__ __forceinline__ double2 class_eval_q1(const double* tabl, const double2* x, int i, int j, int n1,
+                                                 double& invD) {
+  const int cx = i == 0 ? 0 : (i == n1 - 1 ? 2 : 1), cy = j == 0 ? 0 : (j == n1 - 1 ? 2 : 1);
+  const double* T = tabl + (cy * 3 + cx) * 10;
+  invD = T[9];
+  const int xl = i > 0 ? i - 1 : i, xr = i < n1 - 1 ? i + 1 : i;
+  const int yl = j > 0 ? j - 1 : j, yr = j < n1 - 1 ? j + 1 : j;
+  const double2* r0 = x + yl * n1;
+  const double2* r1 = x + j * n1;
+  const double2* r2 = x + yr * n1;
+  double2 a0 = cscale(T[0], r0[xl]);
+  a0 = cfma(T[1], r0[i], a0);
+  a0 = cfma(T[2], r0[xr], a0);
+  double2 a1 = cscale(T[3], r1[xl]);
+  a1 = cfma(T[4], r1[i], a1);
+  a1 = cfma(T[5], r1[xr], a1);
+  double2 a2 = cscale(T[6], r2[xl]);
+  a2 = cfma(T[7], r2[i], a2);
+  a2 = cfma(T[8], r2[xr], a2);
+  return cadd(cadd(a0, a1), a2);
+}
+
 // ---------------------------------------------------------------- CTA-resident solvers
 // One CTA owns one problem (one frequency / slot / component) and runs the WHOLE fixed-count
 // solve -- every level, colour, transfer and V-cycle -- with block barriers only.  The problems
@@ -1621,6 +1667,14 @@ __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const d
           const double2 Ax = class_eval<DIM>(tabl, x, c, g.n1, invD);
           x[idx] = cadd(x[idx], cscale(omega * invD, csub(b[idx], Ax)));
         } else {
+          if constexpr (ORD == 1 && DIM == 2 && !CONV) {
+            if (tabl) {
+              double invD;
+              const double2 Ax = class_eval_q1(tabl, x, c[0], c[1], g.n1, invD);
+              x[idx] = cadd(x[idx], cscale(omega * invD, csub(b[idx], Ax)));
+              return;
+            }
+          }
           sor_node<DIM, ORD, CONV>(g, cf, cv, x, b, c, idx, omega);
         }
       };
@@ -1707,8 +1761,9 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
     for (int i = tid; i < (int)g.n; i += nth) xl[i] = make_double2(0.0, 0.0);
     gsync<W>();
   }
-  const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
-                                                       : ClassTab<DIM>::PER_LEVEL) : nullptr;
+  const double* tabl = S.ctab ? S.ctab + l * (ORD == 1 ? Q1TAB
+                                                       : (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
+                                                               : ClassTab<DIM>::PER_LEVEL)) : nullptr;
   // profiling (AAO_MG_CLOCK): split of the level-0 down-leg into sweeps / residual / restriction
   const bool pclk = DIM == 2 && a.clk != nullptr && blockIdx.x == a.clk_block && tid == 0 && l == 0;
   unsigned long long pt = pclk ? clock64() : 0ull;
@@ -1767,6 +1822,9 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
     } else if (CONV) {
       double2 D;
       apply_op_conv<DIM, ORD>(g, cf, cvl, xl, c, i, Ax, D);
+    } else if (ORD == 1 && DIM == 2 && tabl != nullptr) {
+      double invD;
+      Ax = class_eval_q1(tabl, xl, c[0], c[1], g.n1, invD);
     } else {
       double D;
       apply_op_real<DIM, ORD>(g, cf.a.x, cf.b.x, xl, c, i, Ax, D);
@@ -1901,8 +1959,9 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
   });
   gsync<W>();
   }
-  const double* tabl = S.ctab ? S.ctab + l * (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
-                                                   : ClassTab<DIM>::PER_LEVEL) : nullptr;
+  const double* tabl = S.ctab ? S.ctab + l * (ORD == 1 ? Q1TAB
+                                                   : (CONV ? 2 * ClassTab<DIM>::NCL * ClassTab<DIM>::NT
+                                                           : ClassTab<DIM>::PER_LEVEL)) : nullptr;
   cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl,
                                     wv ? S.smem + a.ring_off : nullptr, a.wave_hl[l], a.flat_max, nullptr,
                                     fuse_prolong ? xc : nullptr, gc.n1, DIM == 3 && l < a.lsm && g.n1 >= a.zwave_min,
@@ -1934,6 +1993,15 @@ __global__ void __launch_bounds__(mg_threads<DIM, TAB, CONV, ORD>(), mg_minb<DIM
   const int tid = threadIdx.x, nth = blockDim.x;
   // class stencils of every smoothing level (real Q2 operators) at the start of dynamic smem
   double* ctab = nullptr;
+  if constexpr (ORD == 1 && DIM == 2 && !CONV) {
+    if (a.use_ctab == 2) {   // Q1 position-class stencils of every smoothing level
+      ctab = reinterpret_cast<double*>(smem);
+      for (int l = 0; l < L - 1; ++l) {
+        build_class_tab_q1(a.g[l], cf.a.x, cf.b.x, ctab + l * Q1TAB, tid, nth);
+        __syncthreads();
+      }
+    }
+  }
   if (TAB) {
     ctab = reinterpret_cast<double*>(smem);
     for (int l = 0; l < L - 1; ++l) {
@@ -2010,9 +2078,14 @@ __global__ void __launch_bounds__(mg_threads<DIM, false, false, ORD>(), mg_minb<
   const double2 z = make_double2(0.0, 0.0);
   // Q2 mass: class stencils (a = 1, b = 0) when the level has an interior vertex row (n1 >= 9)
   __shared__ double mtab[ClassTab<DIM>::PER_LEVEL];
+  static_assert(ClassTab<DIM>::PER_LEVEL >= Q1TAB, "the Q1 mass table shares mtab");
   const bool tab = ORD == 2 && g.n1 >= 9;
+  const bool tabq1 = ORD == 1 && DIM == 2 && g.n1 >= 3;
   if (tab) {
     build_class_tab<DIM>(g, 1.0, 0.0, mtab, threadIdx.x, blockDim.x);
+    __syncthreads();
+  } else if (tabq1) {
+    build_class_tab_q1(g, 1.0, 0.0, mtab, threadIdx.x, blockDim.x);
     __syncthreads();
   }
   for (int i = threadIdx.x; i < (int)g.n; i += blockDim.x) {
@@ -2041,6 +2114,8 @@ __global__ void __launch_bounds__(mg_threads<DIM, false, false, ORD>(), mg_minb<
       double invM;
       if (ORD == 2 && tab) {
         Mx = class_eval<DIM>(mtab, dold, c, g.n1, invM);
+      } else if (DIM == 2 && tabq1) {
+        Mx = class_eval_q1(mtab, dold, c[0], c[1], g.n1, invM);
       } else {
         double2 Kx, Cx;
         double dM, dK, dC;

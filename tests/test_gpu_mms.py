@@ -59,12 +59,14 @@ def _velocity_error(cfg, x):
 
 
 @pytest.mark.parametrize("nc,nt,tol,xtol,etol", [(4, 8, 1e-10, 1e-5, 1e-3), (8, 16, 1e-10, 1e-5, 1e-3),
-                                                    (16, 32, 1e-9, None, None)])
+                                                    (16, 32, 3e-9, None, None)])
 def test_manufactured_solution_gpu_gmres(nc, nt, tol, xtol, etol, monkeypatch):
     """GPU GMRES(30) with the linear preconditioner reaches the direct solution of the same discrete system;
     the system is ill-conditioned (nu = 1 on [-1,1]^2), so a residual of 1e-10 leaves ~1e-7 in x and the
-    16 x 16 x 32 case (GMRES(30) stagnates below 1e-9; the oracle's sparse direct solve takes minutes there)
-    is checked against the exact solution only."""
+    16 x 16 x 32 case (restarted GMRES(30) crawls there: 1e-7 after 3000 iterations, ~2e-9 after 12000, and how
+    far it gets within the cap moves with the rounding order of the preconditioner's stencil sums -- 3e-9 is
+    asked, the check it feeds needs the 1e-3 discretisation error; the oracle's sparse direct solve takes
+    minutes there) is checked against the exact solution only."""
     _torch()
     from oracle.manufactured import solve_manufactured
     from paper_2405_18964_b200 import Context
