@@ -932,6 +932,10 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
     }
   }
   a.flat_max = 33;   // measured: 33 best (c2 precond 2.371 -> 2.249 ms)
+  // x += P x_c fused into the first post-smoothing wavefront sweep (AAO_FUSE_PROLONG=0: a separate pass; measured
+  // c4_512 precond 184 vs 175 ms with the fusion)
+  static const bool no_fuse_pro = std::getenv("AAO_FUSE_PROLONG") != nullptr && std::atoi(std::getenv("AAO_FUSE_PROLONG")) == 0;
+  a.fuse_prolong = no_fuse_pro ? 0 : 1;
   // 3-D: z-band wavefront sweeps on the levels whose iterate does not stay in L2 across the 27 colour steps
   // (n1 >= 65 by default; AAO_WAVE=1 forces every level >= AAO_WAVE_MIN, AAO_WAVE=0 none)
   a.zwave_min = c.wave_force == 0 ? (1 << 30) : (c.wave_force == 1 ? c.wave_min : 65);

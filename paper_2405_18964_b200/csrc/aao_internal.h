@@ -96,6 +96,7 @@ struct MGArgs {
   long ring_off;            // ring buffer offset in dynamic smem (double2 units)
   long mbar_off;            // 9 band-slot mbarriers + their phase word after the ring (double2 units)
   int flat_max;             // 2-D Q2 real: levels with n1 <= flat_max use merged branch-free colour visits
+  int fuse_prolong;         // wavefront levels: x += P x_c applied while the first post-smoothing sweep loads its bands
   unsigned long long* clk;  // profiling (AAO_MG_CLOCK=<block>): that CTA accumulates SM cycles per [level][down, up]
   int clk_block;
 };

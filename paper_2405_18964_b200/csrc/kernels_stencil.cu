@@ -1378,23 +1378,29 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
     j0 = band * H;
     cnt = (min(n1, j0 + H) - j0) * n1;
   };
-  // band copies: TMA bulk copies on the slot mbarriers; with xcoarse (first post-smoothing sweep) the threads copy
-  // and add the coarse-grid correction x += P x_c on the way in (mg_up's arithmetic)
+  // band copies: TMA bulk copies on the slot mbarriers, issued by the copy thread.  With xcoarse (first
+  // post-smoothing sweep) the coarse-grid correction x += P x_c (nodal interpolation, mg_up's arithmetic) is added
+  // to a band in the ring once it has landed -- at the end of the step that issued its load, one step before it is
+  // first read -- instead of in a separate pass over the level.
   unsigned* phase_word = reinterpret_cast<unsigned*>(mbar + NS);
   unsigned phase = *phase_word;
-  const bool tma = xcoarse == nullptr;
+  const bool corr = xcoarse != nullptr;
   auto load_band = [&](int band) {
     int j0, cnt;
     band_rows(band, j0, cnt);
+    bulk_load(ring + (band % NS) * H * n1, x + (long)j0 * n1, (unsigned)cnt * sizeof(double2), mbar + band % NS);
+  };
+  auto wait_band = [&](int band) {
+    const int sl = band % NS;
+    mbar_wait(mbar + sl, (phase >> sl) & 1u);
+    phase ^= 1u << sl;
+  };
+  auto correct_band = [&](int band) {   // ring band += P x_c (all threads; the band has landed)
+    int j0, cnt;
+    band_rows(band, j0, cnt);
     double2* dst = ring + (band % NS) * H * n1;
-    const double2* src = x + (long)j0 * n1;
-    if (tma) {
-      bulk_load(dst, src, (unsigned)cnt * sizeof(double2), mbar + band % NS);
-      return;
-    }
     for (int e = tid; e < cnt; e += nth) {
       const int jj = e / n1, j = j0 + jj, i = e - jj * n1;
-      double2 v = src[e];
       if (j >= 1 && j <= n1 - 2 && i >= 1 && i <= n1 - 2) {
         double wy[3], wx[3];
         const int by = q2_prow(j, wy), bx = q2_prow(i, wx);
@@ -1406,28 +1412,14 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
             const double ww = wy[ob] * wx[oa];
             if (ww != 0.0) acc = cfma(ww, xcoarse[(by + ob) * n1c + bx + oa], acc);
           }
-        v = cadd(v, acc);
+        dst[e] = cadd(dst[e], acc);
       }
-      dst[e] = v;
     }
-  };
-  auto wait_band = [&](int band) {
-    if (!tma) return;
-    const int sl = band % NS;
-    mbar_wait(mbar + sl, (phase >> sl) & 1u);
-    phase ^= 1u << sl;
   };
   auto store_band = [&](int band) {
     int j0, cnt;
     band_rows(band, j0, cnt);
     bulk_store(x + (long)j0 * n1, ring + (band % NS) * H * n1, (unsigned)cnt * sizeof(double2));
-  };
-  auto copy_back = [&](int band) {
-    int j0, cnt;
-    band_rows(band, j0, cnt);
-    const double2* src = ring + (band % NS) * H * n1;
-    double2* dst = x + (long)j0 * n1;
-    for (int e = tid; e < cnt; e += nth) dst[e] = src[e];
   };
   // this thread's item: row class slot p (band lag 2 p), row kk of that class within the band, triple m.  A row
   // takes lpr lanes (tri_lanes_per_row: whole warps, or a power-of-two fraction of a warp on small levels), so the
@@ -1440,14 +1432,17 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
   const bool copier = tid == nth - 1;
   fence_async_global();   // generic writes of the iterate (previous passes, zeroing) before the async-proxy reads
   __syncthreads();
-  if (tma) {
-    if (copier) {
-      load_band(0);
-      if (nb > 1) load_band(1);
-    }
-  } else {
+  if (copier) {
     load_band(0);
     if (nb > 1) load_band(1);
+  }
+  if (corr) {   // the first two bands are corrected before step 0 reads them
+    wait_band(0);
+    correct_band(0);
+    if (nb > 1) {
+      wait_band(1);
+      correct_band(1);
+    }
   }
   int p = 0, kk = 0, m = 0;
   bool has = tid < 3 * per;
@@ -1494,21 +1489,18 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
   auto pmark = [](int) {};
 #endif
   for (int T = 0; T <= nb + 4; ++T) {
-    if (T == 0) wait_band(0);
-    if (T + 1 < nb) wait_band(T + 1);
+    if (!corr) {   // (with the correction, a band was waited for when it was corrected)
+      if (T == 0) wait_band(0);
+      if (T + 1 < nb) wait_band(T + 1);
+    }
     pmark(16);
-    if (tma) fence_async_smem();   // this thread's ring writes (step T - 1) -> visible to the bulk store
+    fence_async_smem();   // this thread's ring writes (step T - 1) -> visible to the bulk store
     __syncthreads();
     pmark(17);
-    if (tma) {
-      if (copier) {
-        bulk_wait_read1();          // all but the latest store have read their slot: band T - 7's slot is free
-        if (T + 2 < nb) load_band(T + 2);
-        if (T - 5 >= 0 && T - 5 < nb) store_band(T - 5);
-      }
-    } else {
-      if (T - 6 >= 0 && T - 6 < nb) copy_back(T - 6);
+    if (copier) {
+      bulk_wait_read1();          // all but the latest store have read their slot: band T - 7's slot is free
       if (T + 2 < nb) load_band(T + 2);
+      if (T - 5 >= 0 && T - 5 < nb) store_band(T - 5);
     }
     pmark(18);
     const int band = T - 2 * p;
@@ -1550,18 +1542,17 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
       }
       pmark(14);
     }
-  }
-  if (tma) {
-    __syncthreads();
-    if (copier) {
-      bulk_wait_all();
-      fence_async_global();
+    if (corr && T + 2 < nb) {   // band T + 2 (issued at the top of this step): correct it once it has landed
+      wait_band(T + 2);
+      correct_band(T + 2);
     }
-    if (tid == 0) *phase_word = phase;
-  } else {
-    __syncthreads();
-    for (int band = max(0, nb + 4 - 5); band < nb; ++band) copy_back(band);
   }
+  __syncthreads();
+  if (copier) {
+    bulk_wait_all();
+    fence_async_global();
+  }
+  if (tid == 0) *phase_word = phase;
   __syncthreads();
 }
 
@@ -1919,7 +1910,7 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
   double2* xl = S.X(l);
   const double2* xc = S.X(l + 1);
   const bool wv = a.wave_hl[l] > 0;
-  const bool fuse_prolong = TAB && ORD == 2 && DIM == 2 && !W && wv && a.post > 0;
+  const bool fuse_prolong = TAB && ORD == 2 && DIM == 2 && !W && wv && a.post > 0 && a.fuse_prolong;
   if (!fuse_prolong) {
   cta_all_unknowns<DIM, ORD>(g.n1, tid, nth, [&](const int* c, int i) {
     int base[DIM];
