@@ -889,7 +889,7 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
       a.lwarp = l;
       break;
     }
-  // band-wavefront sweeps (2-D Q2) on the levels with n1 >= wave_min (default 257): the iterate crosses HBM once
+  // band-wavefront sweeps (2-D Q2) on the levels with n1 >= wave_min (default 65): the iterate crosses HBM once
   // per sweep instead of once per colour, every tap is a shared-memory load (measured with the first, node-per-thread
   // form: c4_64 precond 43.6 -> 35.2 ms, c4_128 87.8 -> 73.5 ms; slower with the stored per-node convection stencils,
   // c3 255 -> 330 ms, so Oseen operators use it only when forced).  AAO_WAVE=0/1 forces it off/on for every eligible
@@ -898,7 +898,7 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
   // 9-slot ring fits the shared memory left (513^2: 3, 257^2: 6, 129^2: 6, 65^2: 12, 33^2: 24); a row takes whole warps.
   a.wave_h = 0;
   for (int l = 0; l < MG_MAXL; ++l) a.wave_hl[l] = 0;
-  const bool wave_on = c.wave_force >= 0 ? c.wave_force != 0 : a.g[0].n1 >= c.wave_min;
+  const bool wave_on = c.wave_force >= 0 ? c.wave_force != 0 : (op.conv_sel == 0 && a.g[0].n1 >= c.wave_min);
   const bool wave_conv = c.wave_force == 1;
   if (wave_on && c.dim == 2 && S.order == 2 && a.use_ctab && (op.conv_sel == 0 || wave_conv)) {
     const size_t mbars = 5 * sizeof(double2);   // 9 mbarriers (72 B) + phase word
@@ -1577,7 +1577,8 @@ aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
     const char* we = std::getenv("AAO_WAVE");
     ctx->c.wave_force = we ? std::atoi(we) : -1;
     const char* wm = std::getenv("AAO_WAVE_MIN");
-    ctx->c.wave_min = wm ? std::atoi(wm) : 257;
+    ctx->c.wave_min = wm ? std::atoi(wm) : 65;   // measured (triple form): c4_512 precond 175.9 (257) / 170.1 (129) /
+                                                 // 169.3 ms (65); c2 2.07 / 1.92 / 1.84 ms
     const char* wh = std::getenv("AAO_WAVE_H");      // largest band height tried (24, 12, 6 or 3): tests force 3
     const int whv = wh ? std::atoi(wh) : 24;
     ctx->c.wave_hmax = (whv == 3 || whv == 6 || whv == 12) ? whv : 24;

@@ -188,7 +188,7 @@ struct Ctx {
   // live timing of the dominant kernel class (finest-level multicolour SOR sweeps)
   cudaStream_t s2 = nullptr;               // side stream: pressure solves overlap the velocity MG
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  int wave_force = -1, wave_min = 257;   // band-wavefront sweeps: AAO_WAVE (-1 auto), AAO_WAVE_MIN
+  int wave_force = -1, wave_min = 65;   // band-wavefront sweeps: AAO_WAVE (-1 auto), AAO_WAVE_MIN
   int wave_hmax = 24;                    // largest band height tried per level (AAO_WAVE_H)
   int mg_mode = 0;       // MG schedule: 0 CTA-resident (default), 1 per level / colour launches (AAO_MG_MODE=1)
   int freq_chunk = 0;    // frequencies per velocity-MG launch (aao_config.freq_chunk; workspace sized for it)
