@@ -1023,16 +1023,21 @@ void stokes_blocks(Ctx& c, FVec in, double2* outV, double2* outPA, double2* outP
   OpSel opW{c.coefW, 2 * dim, 0};
   // pressure slots on the side stream (independent of the velocity slots): K_p^{-1} by MG and
   // M_p^{-1} by Chebyshev, combined later
-  cudaStream_t sp = c.s2;
+  // (the two pressure solves are independent of each other too: on separate streams the partial last wave of one
+  // -- 512 problems on 148 SMs at c4_512 -- is filled by the other)
+  cudaStream_t sp = c.s2, sq = c.s3;
   cudaEventRecord(c.ev_fork, s);
   cudaStreamWaitEvent(sp, c.ev_fork, 0);
+  cudaStreamWaitEvent(sq, c.ev_fork, 0);
   OpSel opKp{c.coefKp, 1 << 30, 0};
   mg_solve(c, c.pres, opKp, c.invKp, 1 << 30, contig(outPA, gp.n), contig(in.p, gp.n), 2 * n_f, sp);
-  cheb_solve(c, gp, contig(in.p, gp.n), contig(outPB, gp.n), 2 * n_f, 1.0, sp);
+  cheb_solve(c, gp, contig(in.p, gp.n), contig(outPB, gp.n), 2 * n_f, 1.0, sq);
   cudaEventRecord(c.ev_join, sp);
+  cudaEventRecord(c.ev_join2, sq);
   mg_solve(c, c.vel, opW, c.invW, 2 * dim, contig(outV, gv.n), contig(in.v, gv.n), n_f * 2 * dim, s);
   if (c.timing) cudaEventRecord(c.ev[2], s);
   cudaStreamWaitEvent(s, c.ev_join, 0);
+  cudaStreamWaitEvent(s, c.ev_join2, 0);
 }
 
 void precond_stokes(Ctx& c, cudaStream_t s) { stokes_blocks(c, FVec{c.Fv, c.Fp}, c.Xv, c.XpA, c.XpB, s); }
@@ -1585,6 +1590,8 @@ aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
     aao::setup(ctx->c, *cfg);
     for (auto& e : ctx->c.ev) cudaEventCreate(&e);
     cudaStreamCreateWithFlags(&ctx->c.s2, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&ctx->c.s3, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ctx->c.ev_join2, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->c.ev_fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->c.ev_join, cudaEventDisableTiming);
   } catch (const CudaError& e) {
@@ -1609,6 +1616,8 @@ void aao_destroy(aao_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->c.prof_ev) cudaEventDestroy(e);
   if (ctx->c.s2) cudaStreamDestroy(ctx->c.s2);
+  if (ctx->c.s3) cudaStreamDestroy(ctx->c.s3);
+  if (ctx->c.ev_join2) cudaEventDestroy(ctx->c.ev_join2);
   if (ctx->c.ev_fork) cudaEventDestroy(ctx->c.ev_fork);
   if (ctx->c.ev_join) cudaEventDestroy(ctx->c.ev_join);
   delete ctx;

@@ -186,8 +186,8 @@ struct Ctx {
   cudaEvent_t ev[5] = {};
   double phase_ms[4] = {0, 0, 0, 0};
   // live timing of the dominant kernel class (finest-level multicolour SOR sweeps)
-  cudaStream_t s2 = nullptr;               // side stream: pressure solves overlap the velocity MG
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t s2 = nullptr, s3 = nullptr; // side streams: the two pressure solves overlap the velocity MG
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
   int wave_force = -1, wave_min = 65;   // band-wavefront sweeps: AAO_WAVE (-1 auto), AAO_WAVE_MIN
   int wave_hmax = 24;                    // largest band height tried per level (AAO_WAVE_H)
   int mg_mode = 0;       // MG schedule: 0 CTA-resident (default), 1 per level / colour launches (AAO_MG_MODE=1)
