@@ -1021,21 +1021,31 @@ void stokes_blocks(Ctx& c, FVec in, double2* outV, double2* outPA, double2* outP
   const Grid& gp = c.pres.grids[0];
   // x1 = MG(W; s1), x2 = MG(W; s2) per velocity component
   OpSel opW{c.coefW, 2 * dim, 0};
-  // pressure slots on the side stream (independent of the velocity slots): K_p^{-1} by MG and
-  // M_p^{-1} by Chebyshev, combined later
-  // (the two pressure solves are independent of each other too: on separate streams the partial last wave of one
-  // -- 512 problems on 148 SMs at c4_512 -- is filled by the other)
+  // The pressure slots (independent of the velocity slots) -- K_p^{-1} by MG and M_p^{-1} by Chebyshev, combined
+  // later -- run on two side streams, concurrently with each other (each fills the partial last wave of
+  // the other: 512 problems on 148 SMs at c4_512).  When the velocity solve is chunked into several full-width
+  // launches they start after it: interleaved with it, their short CTAs take the SMs that free up at every
+  // launch boundary and every velocity launch then waits for them (measured c4_512: 20.8 ms per launch with the
+  // same total as 15.9 ms per launch alone + the pressure solves at full width).  A single velocity launch that
+  // leaves SMs idle (small configs) still overlaps with them.
   cudaStream_t sp = c.s2, sq = c.s3;
-  cudaEventRecord(c.ev_fork, s);
-  cudaStreamWaitEvent(sp, c.ev_fork, 0);
-  cudaStreamWaitEvent(sq, c.ev_fork, 0);
   OpSel opKp{c.coefKp, 1 << 30, 0};
-  mg_solve(c, c.pres, opKp, c.invKp, 1 << 30, contig(outPA, gp.n), contig(in.p, gp.n), 2 * n_f, sp);
-  cheb_solve(c, gp, contig(in.p, gp.n), contig(outPB, gp.n), 2 * n_f, 1.0, sq);
-  cudaEventRecord(c.ev_join, sp);
-  cudaEventRecord(c.ev_join2, sq);
-  mg_solve(c, c.vel, opW, c.invW, 2 * dim, contig(outV, gv.n), contig(in.v, gv.n), n_f * 2 * dim, s);
+  const int nprob_v = n_f * 2 * dim;
+  static const int after_env = std::getenv("AAO_PRESSURE_AFTER") ? std::atoi(std::getenv("AAO_PRESSURE_AFTER")) : -1;
+  const bool after = after_env >= 0 ? after_env != 0 : nprob_v > c.vel.nprob_max;
+  auto pressure = [&]() {
+    cudaEventRecord(c.ev_fork, s);
+    cudaStreamWaitEvent(sp, c.ev_fork, 0);
+    cudaStreamWaitEvent(sq, c.ev_fork, 0);
+    mg_solve(c, c.pres, opKp, c.invKp, 1 << 30, contig(outPA, gp.n), contig(in.p, gp.n), 2 * n_f, sp);
+    cheb_solve(c, gp, contig(in.p, gp.n), contig(outPB, gp.n), 2 * n_f, 1.0, sq);
+    cudaEventRecord(c.ev_join, sp);
+    cudaEventRecord(c.ev_join2, sq);
+  };
+  if (!after) pressure();
+  mg_solve(c, c.vel, opW, c.invW, 2 * dim, contig(outV, gv.n), contig(in.v, gv.n), nprob_v, s);
   if (c.timing) cudaEventRecord(c.ev[2], s);
+  if (after) pressure();
   cudaStreamWaitEvent(s, c.ev_join, 0);
   cudaStreamWaitEvent(s, c.ev_join2, 0);
 }
@@ -1591,6 +1601,7 @@ aao_status aao_create(const aao_config* cfg, aao_ctx** out) {
     for (auto& e : ctx->c.ev) cudaEventCreate(&e);
     cudaStreamCreateWithFlags(&ctx->c.s2, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&ctx->c.s3, cudaStreamNonBlocking);
+
     cudaEventCreateWithFlags(&ctx->c.ev_join2, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->c.ev_fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->c.ev_join, cudaEventDisableTiming);
