@@ -93,6 +93,7 @@ struct MGArgs {
   int wave_h;               // band-wavefront sweeps (2-D Q2) on some level: the ring and its mbarriers exist
   int wave_hl[MG_MAXL];     // per level: band height H (rows per band, a multiple of 3), 0 = colour-by-colour sweeps
   int zwave_min;            // 3-D Q2: levels with n1 >= zwave_min sweep as a z-band wavefront (global memory)
+  long zstage_off;          // 3-D Q2 real: per-warp line stages of the line-form wavefront (double2 units), -1 = none
   long ring_off;            // ring buffer offset in dynamic smem (double2 units)
   long mbar_off;            // 9 band-slot mbarriers + their phase word after the ring (double2 units)
   int flat_max;             // 2-D Q2 real: levels with n1 <= flat_max use merged branch-free colour visits

@@ -1556,6 +1556,194 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
   __syncthreads();
 }
 
+// ---- z-band wavefront sweeps in line form (3-D Q2, real class stencils) -------------------------------------------
+// The schedule of the 3-D z-band wavefront (planes in bands of 3, band B updates its plane of z-class c' at step
+// B + 2 c', the 9 xy-colours of a step in order), with the work of a step given to warps line by line: a warp owns
+// one x-line (y = j, z = k) of the current y-class and each lane the triple (3m, 3m+1, 3m+2) of it, as in the 2-D
+// triple form.  The up to 25 neighbouring lines (j + dy, k + dz) are not written while the line is updated; the
+// warp copies each of them once, coalesced, into a small shared-memory stage and every lane takes its 7 columns
+// from there (the per-node form re-read them from L1 with stride-3 lane addresses: 3 x 125 taps per triple, twelve
+// cache lines per warp load).  The x-colours of a line are ordered inside the warp -- the two fresh neighbour
+// values come by shuffle -- so a step needs one block barrier per y-class instead of one per xy-colour.
+// Lines of one y-class are three apart and the three active planes five apart: no line read here is being written.
+constexpr int ZL_PAD = 4;   // zeroed entries before and after a staged line
+
+template <bool REV, int PY, int PZ>
+__device__ __forceinline__ void zline_accumulate(const double* __restrict__ Ta, const double* __restrict__ Tb,
+                                                 const double2* x, int n1, int j, int k, int cb, bool has, int lane,
+                                                 double2* stage, int& buf, double2* acc, double2* xo,
+                                                 double2& v5old, double2& v6old) {
+  constexpr int AY0 = PY ? 1 : 0, NY = PY ? 3 : 5;
+  constexpr int AZ0 = PZ ? 1 : 0, NZ = PZ ? 3 : 5;
+  constexpr int NL = NY * NZ;
+  const int SL = n1 + 2 * ZL_PAD;
+  // the next two neighbouring lines are in flight (registers) while the current one is processed from the stage
+  auto lptr = [&](int t) {
+    const int oc = AZ0 + t / NY, ob = AY0 + t % NY;
+    return x + ((long)(k + oc - 2) * n1 + (j + ob - 2)) * n1;
+  };
+  const bool l2 = lane + 64 < n1, l1 = lane + 32 < n1, l0 = lane < n1;
+  const double2 zero = make_double2(0.0, 0.0);
+  double2 ra[3], rb[3];
+  {
+    const double2* L = lptr(0);
+    ra[0] = l0 ? L[lane] : zero;
+    ra[1] = l1 ? L[lane + 32] : zero;
+    ra[2] = l2 ? L[lane + 64] : zero;
+    const double2* M = lptr(1);
+    rb[0] = l0 ? M[lane] : zero;
+    rb[1] = l1 ? M[lane + 32] : zero;
+    rb[2] = l2 ? M[lane + 64] : zero;
+  }
+#pragma unroll 1
+  for (int t = 0; t < NL; ++t) {
+    const int oc = AZ0 + t / NY, ob = AY0 + t % NY;
+    double2* st = stage + buf * SL + ZL_PAD;
+    if (l0) st[lane] = ra[0];
+    if (l1) st[lane + 32] = ra[1];
+    if (l2) st[lane + 64] = ra[2];
+    __syncwarp();
+    buf ^= 1;
+    ra[0] = rb[0];
+    ra[1] = rb[1];
+    ra[2] = rb[2];
+    if (t + 2 < NL) {
+      const double2* M = lptr(t + 2);
+      rb[0] = l0 ? M[lane] : zero;
+      rb[1] = l1 ? M[lane + 32] : zero;
+      rb[2] = l2 ? M[lane + 64] : zero;
+    }
+    if (!has) continue;
+    const double2* row = st + cb;
+    const double* pa = Ta + (oc * 5 + ob) * 5;
+    const double* pb = Tb + (oc * 5 + ob) * 5;
+    double ta[5], tb[5];
+#pragma unroll
+    for (int oa = 0; oa < 5; ++oa) {
+      ta[oa] = pa[REV ? 4 - oa : oa];
+      tb[oa] = pb[REV ? 4 - oa : oa];
+    }
+    double2 v[7];
+#pragma unroll
+    for (int c = 0; c < 7; ++c) v[c] = row[REV ? -c : c];
+    if (oc != 2 || ob != 2) {
+#pragma unroll
+      for (int oa = 0; oa < 5; ++oa) {
+        acc[0] = cfma(ta[oa], v[oa], acc[0]);
+        acc[1] = cfma(tb[oa], v[1 + oa], acc[1]);
+        acc[2] = cfma(ta[oa], v[2 + oa], acc[2]);
+      }
+    } else {   // the line itself: node 0 (first colour) sees only old values; nodes 1, 2 take their fresh taps later
+      xo[0] = v[2];
+      xo[1] = v[3];
+      xo[2] = v[4];
+      v5old = v[5];
+      v6old = v[6];
+#pragma unroll
+      for (int oa = 0; oa < 5; ++oa) acc[0] = cfma(ta[oa], v[oa], acc[0]);
+      acc[1] = cfma(tb[0], v[1], acc[1]);
+      acc[1] = cfma(tb[2], v[3], acc[1]);
+      acc[1] = cfma(tb[3], v[4], acc[1]);
+      acc[2] = cfma(ta[2], v[4], acc[2]);
+    }
+  }
+}
+
+template <bool REV>
+__device__ __forceinline__ void zline_update(const double* tabl, double2* x, const double2* __restrict__ b, int n1,
+                                             int j, int k, int m, int ntr, int lane, double omega, double2* stage,
+                                             int& buf) {
+  const bool has = m < ntr;
+  const int i0 = 3 * m, px = m & 1, py = j & 1, pz = k & 1;
+  const int cb = REV ? i0 + 4 : i0 - 2;
+  int gc[3];
+  bool act[3];
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    gc[n] = REV ? i0 + 2 - n : i0 + n;
+    act[n] = has && gc[n] >= 1 && gc[n] <= n1 - 2;
+  }
+  const long line = ((long)k * n1 + j) * n1;
+  const double* Ta = tabl + (px | (py << 1) | (pz << 2)) * (ClassTab<3>::NT + 1);
+  const double* Tb = tabl + ((px ^ 1) | (py << 1) | (pz << 2)) * (ClassTab<3>::NT + 1);
+  const double2 zero = make_double2(0.0, 0.0);
+  double2 acc[3], xo[3] = {zero, zero, zero}, v5old = zero, v6old = zero;
+#pragma unroll
+  for (int n = 0; n < 3; ++n) {
+    const double2 bb = act[n] ? b[line + gc[n]] : zero;
+    acc[n] = make_double2(-bb.x, -bb.y);
+  }
+  switch (py | (pz << 1)) {
+    case 0: zline_accumulate<REV, 0, 0>(Ta, Tb, x, n1, j, k, cb, has, lane, stage, buf, acc, xo, v5old, v6old); break;
+    case 1: zline_accumulate<REV, 1, 0>(Ta, Tb, x, n1, j, k, cb, has, lane, stage, buf, acc, xo, v5old, v6old); break;
+    case 2: zline_accumulate<REV, 0, 1>(Ta, Tb, x, n1, j, k, cb, has, lane, stage, buf, acc, xo, v5old, v6old); break;
+    default: zline_accumulate<REV, 1, 1>(Ta, Tb, x, n1, j, k, cb, has, lane, stage, buf, acc, xo, v5old, v6old); break;
+  }
+  const double wa = omega * Ta[ClassTab<3>::NT], wb = omega * Tb[ClassTab<3>::NT];
+  const double* ra = Ta + 62 - 2;   // the centre row (oc = ob = 2) of the two stencils
+  const double* rb = Tb + 62 - 2;
+  const double tb1 = rb[REV ? 3 : 1], tb4 = rb[REV ? 0 : 4];
+  const double ta0 = ra[REV ? 4 : 0], ta1 = ra[REV ? 3 : 1], ta3 = ra[REV ? 1 : 3], ta4 = ra[REV ? 0 : 4];
+  // the triple that holds local columns 5 and 6: m + 1 (m - 1 in the mirrored frame of the reversed order)
+  const int nbr = REV ? lane - 1 : lane + 1;
+  const bool nbr_ok = has && nbr >= 0 && nbr < ntr;
+  const int src = nbr_ok ? nbr : lane;
+  // first x-colour
+  double2 x0n = xo[0];
+  if (act[0]) x0n = make_double2(xo[0].x - wa * acc[0].x, xo[0].y - wa * acc[0].y);
+  // second x-colour: fresh taps = own first node and the first node of the neighbouring triple
+  double2 v5 = make_double2(__shfl_sync(0xffffffffu, x0n.x, src), __shfl_sync(0xffffffffu, x0n.y, src));
+  if (!nbr_ok) v5 = v5old;
+  double2 x1n = xo[1];
+  if (act[1]) {
+    double2 a1 = cfma(tb1, x0n, acc[1]);
+    a1 = cfma(tb4, v5, a1);
+    x1n = make_double2(xo[1].x - wb * a1.x, xo[1].y - wb * a1.y);
+  }
+  // third x-colour
+  double2 v6 = make_double2(__shfl_sync(0xffffffffu, x1n.x, src), __shfl_sync(0xffffffffu, x1n.y, src));
+  if (!nbr_ok) v6 = v6old;
+  if (act[0]) x[line + gc[0]] = x0n;
+  if (act[1]) x[line + gc[1]] = x1n;
+  if (act[2]) {
+    double2 a2 = cfma(ta0, x0n, acc[2]);
+    a2 = cfma(ta1, x1n, a2);
+    a2 = cfma(ta3, v5, a2);
+    a2 = cfma(ta4, v6, a2);
+    x[line + gc[2]] = make_double2(xo[2].x - wa * a2.x, xo[2].y - wa * a2.y);
+  }
+}
+
+// one sweep (all 27 colours in order, reversed if `reverse`) of a 3-D level with (n1 - 2) / 3 + 1 <= 32 triples per line
+__device__ __noinline__ void q2_zline_sweep(const double* tabl, double2* x, const double2* __restrict__ b, int n1,
+                                            bool reverse, double omega, int tid, int nth, double2* stage_all) {
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nth >> 5;
+  const int ntr = (n1 - 2) / 3 + 1;
+  const int SL = n1 + 2 * ZL_PAD;
+  double2* stage = stage_all + warp * 2 * SL;
+  for (int e = lane; e < 2 * SL; e += 32) stage[e] = make_double2(0.0, 0.0);   // pads stay zero
+  __syncwarp();
+  int buf = 0;
+  const int nbz = (n1 + 2) / 3;
+  for (int T = 0; T <= nbz + 3; ++T)
+    for (int q = 0; q < 3; ++q) {
+      const int cy = reverse ? 2 - q : q;
+      const int j0 = cy ? cy : 3;
+      const int nj = j0 > n1 - 2 ? 0 : (n1 - 2 - j0) / 3 + 1;
+      for (int ln = warp; ln < 3 * nj; ln += nwarp) {
+        const int pp = ln / nj, mj = ln - pp * nj;
+        const int band = T - 2 * pp;
+        if (band < 0 || band >= nbz) continue;
+        const int k = 3 * band + (reverse ? 2 - pp : pp);
+        if (k < 1 || k > n1 - 2) continue;
+        const int j = j0 + 3 * mj;
+        if (reverse) zline_update<true>(tabl, x, b, n1, j, k, lane, ntr, lane, omega, stage, buf);
+        else zline_update<false>(tabl, x, b, n1, j, k, lane, ntr, lane, omega, stage, buf);
+      }
+      __syncthreads();
+    }
+}
+
 // Returns true if the band-wavefront path also wrote the residual b - A x of the final iterate to rout.
 template <int DIM, int ORD, bool CONV, bool W, bool TAB>
 __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const double* cv, double2* x,
@@ -1563,7 +1751,8 @@ __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const d
                                           const double* tabl, double2* ring = nullptr,
                                           int waveH = 0, int flat_max = 0, double2* rout = nullptr,
                                           const double2* xcoarse = nullptr, int n1c = 0, bool zwave = false,
-                                          unsigned long long* mbar = nullptr, unsigned long long* clk = nullptr) {
+                                          unsigned long long* mbar = nullptr, unsigned long long* clk = nullptr,
+                                          double2* zstage = nullptr) {
   constexpr int C1 = ORD == 2 ? 3 : 2;
   constexpr int NC = DIM == 2 ? C1 * C1 : C1 * C1 * C1;
   if constexpr (TAB && ORD == 2 && DIM == 2 && !W) {
@@ -1586,6 +1775,12 @@ __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const d
         }
       }
       return rout != nullptr && sweeps > 0 && !reverse;
+    }
+  }
+  if constexpr (DIM == 3 && ORD == 2 && TAB && !W && !CONV) {
+    if (zwave && zstage != nullptr && (g.n1 - 2) / 3 + 1 <= 32) {
+      for (int sw = 0; sw < sweeps; ++sw) q2_zline_sweep(tabl, x, b, g.n1, reverse, omega, tid, nth, zstage);
+      return false;
     }
   }
   if constexpr (DIM == 3 && ORD == 2 && TAB && !W) {
@@ -1734,6 +1929,7 @@ struct MGLevels {
   }
   __device__ double2* R(int l) const { return a.rw[l] + (long)p * a.g[l].n; }
   __device__ const double* CV(int l) const { return a.op.conv_sel == 1 ? a.g[l].conv : a.g[l].convT; }
+  __device__ double2* ZSTAGE() const { return a.zstage_off >= 0 ? smem + a.zstage_off : nullptr; }
   __device__ unsigned long long* MBAR() const {
     return a.wave_h ? reinterpret_cast<unsigned long long*>(smem + a.mbar_off) : nullptr;
   }
@@ -1771,7 +1967,7 @@ __device__ void mg_down(const MGLevels& S, const Coef& cf, int l, int tid, int n
                                                        wv ? S.smem + a.ring_off : nullptr, a.wave_hl[l],
                                                        a.flat_max, wv ? rl : nullptr, nullptr, 0,
                                                        DIM == 3 && l < a.lsm && g.n1 >= a.zwave_min, S.MBAR(),
-                                                       pclk ? a.clk : nullptr);
+                                                       pclk ? a.clk : nullptr, S.ZSTAGE());
   pmark(2 * MG_MAXL - 2);
   const double* cvl = S.CV(l);
   if (fused) {
@@ -1956,7 +2152,7 @@ __device__ void mg_up(const MGLevels& S, const Coef& cf, int l, int tid, int nth
   cta_sweep<DIM, ORD, CONV, W, TAB>(g, cf, S.CV(l), xl, S.B(l), a.post, true, a.omega, tid, nth, tabl,
                                     wv ? S.smem + a.ring_off : nullptr, a.wave_hl[l], a.flat_max, nullptr,
                                     fuse_prolong ? xc : nullptr, gc.n1, DIM == 3 && l < a.lsm && g.n1 >= a.zwave_min,
-                                    S.MBAR());
+                                    S.MBAR(), nullptr, S.ZSTAGE());
 }
 
 // threads per CTA of the CTA-resident MG; 3-D measured: 512 (spills at 128 registers) 205 ms vs 256 (no
