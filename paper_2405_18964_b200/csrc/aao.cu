@@ -939,12 +939,12 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
   // 3-D: z-band wavefront sweeps on the levels whose iterate does not stay in L2 across the 27 colour steps
   // (n1 >= 65 by default; AAO_WAVE=1 forces every level >= AAO_WAVE_MIN, AAO_WAVE=0 none)
   a.zwave_min = c.wave_force == 0 ? (1 << 30) : (c.wave_force == 1 ? c.wave_min : 65);
-  // line form of the z-band wavefront (real operators): two staged lines of n1 + 8 entries per warp of the CTA
+  // line form of the z-band wavefront (real operators): a ring of staged lines of n1 + 8 entries per warp of the CTA
   a.zstage_off = -1;
   static const bool no_zline = std::getenv("AAO_NO_ZLINE") != nullptr;
   if (c.dim == 3 && S.order == 2 && a.use_ctab == 1 && op.conv_sel == 0 && !no_zline) {
     used = (used + 15) / 16 * 16;
-    const size_t st = (size_t)16 * 2 * (a.g[0].n1 + 8) * sizeof(double2);   // 512 threads = 16 warps
+    const size_t st = (size_t)16 * MG_ZL_STAGES * (a.g[0].n1 + 8) * sizeof(double2);   // 512 threads = 16 warps
     if (used + st <= (size_t)MG_SMEM_MAX) {
       a.zstage_off = (long)(used / sizeof(double2));
       used += st;

@@ -70,6 +70,7 @@ inline int mg_tri_lanes_per_row(int ntr) {
   return l;
 }
 constexpr int MG_RING_GUARD = 4;       // zeroed double2 entries before and after the band ring
+constexpr int MG_ZL_STAGES = 6;        // 3-D line-form sweeps: staged lines per warp (= ZL_STAGES of kernels_stencil.cu)
 constexpr int MG_TRI_SLOTS = 9;        // band slots of the triple-form ring (8 for the node-per-thread Oseen form)
 constexpr int MG_SMEM_MAX = 232448;    // dynamic shared memory per CTA (227 KB opt-in on sm_100)
 struct MGArgs {

@@ -1567,6 +1567,9 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
 // values come by shuffle -- so a step needs one block barrier per y-class instead of one per xy-colour.
 // Lines of one y-class are three apart and the three active planes five apart: no line read here is being written.
 constexpr int ZL_PAD = 4;   // zeroed entries before and after a staged line
+#ifndef ZL_STAGES
+#define ZL_STAGES MG_ZL_STAGES   // staged lines per warp (ring of cp.async copies)
+#endif
 
 template <bool REV, int PY, int PZ>
 __device__ __forceinline__ void zline_accumulate(const double* __restrict__ Ta, const double* __restrict__ Tb,
@@ -1576,44 +1579,30 @@ __device__ __forceinline__ void zline_accumulate(const double* __restrict__ Ta, 
   constexpr int AY0 = PY ? 1 : 0, NY = PY ? 3 : 5;
   constexpr int AZ0 = PZ ? 1 : 0, NZ = PZ ? 3 : 5;
   constexpr int NL = NY * NZ;
+  constexpr int D = ZL_STAGES;
   const int SL = n1 + 2 * ZL_PAD;
-  // the next two neighbouring lines are in flight (registers) while the current one is processed from the stage
-  auto lptr = [&](int t) {
+  // the neighbouring lines stream through a ring of D stages per warp: line t + D - 1 is issued (cp.async, 16 bytes
+  // per lane and copy) while line t is processed, so D - 1 lines are in flight per warp
+  auto issue = [&](int t, int slot) {
     const int oc = AZ0 + t / NY, ob = AY0 + t % NY;
-    return x + ((long)(k + oc - 2) * n1 + (j + ob - 2)) * n1;
+    const double2* L = x + ((long)(k + oc - 2) * n1 + (j + ob - 2)) * n1;
+    double2* st = stage + slot * SL + ZL_PAD;
+    for (int e = lane; e < n1; e += 32) cp_async16(st + e, L + e);
   };
-  const bool l2 = lane + 64 < n1, l1 = lane + 32 < n1, l0 = lane < n1;
-  const double2 zero = make_double2(0.0, 0.0);
-  double2 ra[3], rb[3];
-  {
-    const double2* L = lptr(0);
-    ra[0] = l0 ? L[lane] : zero;
-    ra[1] = l1 ? L[lane + 32] : zero;
-    ra[2] = l2 ? L[lane + 64] : zero;
-    const double2* M = lptr(1);
-    rb[0] = l0 ? M[lane] : zero;
-    rb[1] = l1 ? M[lane + 32] : zero;
-    rb[2] = l2 ? M[lane + 64] : zero;
+#pragma unroll
+  for (int t = 0; t < D - 1; ++t) {
+    if (t < NL) issue(t, (buf + t) % D);
+    cp_commit_all();
   }
 #pragma unroll 1
   for (int t = 0; t < NL; ++t) {
     const int oc = AZ0 + t / NY, ob = AY0 + t % NY;
-    double2* st = stage + buf * SL + ZL_PAD;
-    if (l0) st[lane] = ra[0];
-    if (l1) st[lane + 32] = ra[1];
-    if (l2) st[lane + 64] = ra[2];
+    if (t + D - 1 < NL) issue(t + D - 1, (buf + t + D - 1) % D);
+    cp_commit_all();
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(D - 1));
     __syncwarp();
-    buf ^= 1;
-    ra[0] = rb[0];
-    ra[1] = rb[1];
-    ra[2] = rb[2];
-    if (t + 2 < NL) {
-      const double2* M = lptr(t + 2);
-      rb[0] = l0 ? M[lane] : zero;
-      rb[1] = l1 ? M[lane + 32] : zero;
-      rb[2] = l2 ? M[lane + 64] : zero;
-    }
-    if (!has) continue;
+    const double2* st = stage + ((buf + t) % D) * SL + ZL_PAD;
+    if (has) {
     const double2* row = st + cb;
     const double* pa = Ta + (oc * 5 + ob) * 5;
     const double* pb = Tb + (oc * 5 + ob) * 5;
@@ -1646,7 +1635,10 @@ __device__ __forceinline__ void zline_accumulate(const double* __restrict__ Ta, 
       acc[1] = cfma(tb[3], v[4], acc[1]);
       acc[2] = cfma(ta[2], v[4], acc[2]);
     }
+    }
+    __syncwarp();   // every lane is done with this stage before a later issue reuses it
   }
+  buf = (buf + NL) % D;
 }
 
 template <bool REV>
@@ -1720,8 +1712,8 @@ __device__ __noinline__ void q2_zline_sweep(const double* tabl, double2* x, cons
   const int lane = tid & 31, warp = tid >> 5, nwarp = nth >> 5;
   const int ntr = (n1 - 2) / 3 + 1;
   const int SL = n1 + 2 * ZL_PAD;
-  double2* stage = stage_all + warp * 2 * SL;
-  for (int e = lane; e < 2 * SL; e += 32) stage[e] = make_double2(0.0, 0.0);   // pads stay zero
+  double2* stage = stage_all + warp * ZL_STAGES * SL;
+  for (int e = lane; e < ZL_STAGES * SL; e += 32) stage[e] = make_double2(0.0, 0.0);   // pads stay zero
   __syncwarp();
   int buf = 0;
   const int nbz = (n1 + 2) / 3;
