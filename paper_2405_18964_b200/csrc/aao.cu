@@ -931,6 +931,37 @@ void launch_cta_levels(Ctx& c, MGSpace& S, const OpSel& op, const double2* inv, 
       used += mbars;
     }
   }
+  // 2-D Q1 real operators (pressure MG): pair-form wavefront sweeps on the levels with n1 >= wave_min_q1; band
+  // height = the largest even H <= 8 whose rows of pairs (padded to whole warps; two rows per thread when 4 | H) fit
+  // the CTA's 512 threads
+  static const int wave_q1 = std::getenv("AAO_WAVE_Q1") ? std::atoi(std::getenv("AAO_WAVE_Q1")) : 1;
+  if (wave_q1 && c.wave_force != 0 && c.dim == 2 && S.order == 1 && a.use_ctab == 2 && op.conv_sel == 0) {
+    const int wmin = c.wave_force == 1 ? std::max(c.wave_min, 5) : 129;
+    const size_t mbars = 5 * sizeof(double2), guard = 2 * MG_RING_GUARD * sizeof(double2);
+    used = (used + 15) / 16 * 16;
+    const size_t cap = (size_t)MG_SMEM_MAX > used + mbars + guard ? (size_t)MG_SMEM_MAX - used - mbars - guard : 0;
+    size_t ring = 0;
+    for (int l = 0; l < a.nlev - 1 && l < a.lsm && l < a.lwarp; ++l) {
+      const int n1 = a.g[l].n1;
+      if (n1 < wmin) break;
+      const int lpr = mg_tri_lanes_per_row((n1 + 1) / 2);
+      int h = 0;
+      // (a thread takes two rows of its class when H is a multiple of 4: H / U rows of lanes)
+      for (int cand = std::min(8, c.wave_hmax >= 6 ? 8 : 2); cand >= 2 && !h; cand -= 2)
+        if ((cand % 4 == 0 ? cand / 2 : cand) * lpr <= 512 &&
+            (size_t)MG_TRI_SLOTS * cand * n1 * sizeof(double2) <= cap)
+          h = cand;
+      a.wave_hl[l] = h;
+      if (h) ring = std::max(ring, (size_t)MG_TRI_SLOTS * h * n1 * sizeof(double2));
+    }
+    if (ring) {
+      a.wave_h = 1;
+      a.ring_off = (long)(used / sizeof(double2)) + MG_RING_GUARD;
+      used += ring + guard;
+      a.mbar_off = (long)(used / sizeof(double2));
+      used += mbars;
+    }
+  }
   a.flat_max = 33;   // measured: 33 best (c2 precond 2.371 -> 2.249 ms)
   // x += P x_c fused into the first post-smoothing wavefront sweep (AAO_FUSE_PROLONG=0: a separate pass; measured
   // c4_512 precond 184 vs 175 ms with the fusion)

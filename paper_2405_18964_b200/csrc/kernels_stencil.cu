@@ -1556,6 +1556,182 @@ __device__ __forceinline__ void q2_tri_pass(const double* tabl, double2* x, cons
   __syncthreads();
 }
 
+// ---- band-wavefront sweeps in pair form (2-D Q1, real position-class stencils: the pressure MG) --------------------
+// The Q1 analogue of q2_tri_pass.  Colours (i mod 2) + 2 (j mod 2); bands of H rows (H even); the rows of class c'
+// (j mod 2, mirrored for the reversed order) of band B are updated at step B + 2 c' (a row's neighbours j +- 1 of the
+// other class may sit in the next or previous band: the lag of two steps orders them as the colour steps do).  A
+// thread owns the pair (2m, 2m + 1) of one active row: its first node sees only old values (rows j +- 1 are not
+// written during the step), its second needs the fresh first node and the fresh first node of the next pair.
+// Ring of MG_TRI_SLOTS band slots filled and drained by TMA bulk copies as in q2_tri_pass: at step T band T + 1 has
+// landed, band T + 2 is loading, band T - 3 (final since step T - 1) is stored.  Taps that leave the grid have zero
+// coefficients in the position classes and read finite ring or guard entries.
+__device__ __forceinline__ void q1_pair_pass(const double* tabl, double2* x, const double2* __restrict__ b, double2* ring,
+                                             int n1, int H, bool reverse, double omega, int tid, int nth,
+                                             unsigned long long* mbar) {
+  constexpr int NS = MG_TRI_SLOTS;
+  const int RR = NS * H;
+  const int nb = (n1 + H - 1) / H;
+  auto band_rows = [&](int band, int& j0, int& cnt) {
+    j0 = band * H;
+    cnt = (min(n1, j0 + H) - j0) * n1;
+  };
+  unsigned* phase_word = reinterpret_cast<unsigned*>(mbar + NS);
+  unsigned phase = *phase_word;
+  auto load_band = [&](int band) {
+    int j0, cnt;
+    band_rows(band, j0, cnt);
+    bulk_load(ring + (band % NS) * H * n1, x + (long)j0 * n1, (unsigned)cnt * sizeof(double2), mbar + band % NS);
+  };
+  auto wait_band = [&](int band) {
+    const int sl = band % NS;
+    mbar_wait(mbar + sl, (phase >> sl) & 1u);
+    phase ^= 1u << sl;
+  };
+  auto store_band = [&](int band) {
+    int j0, cnt;
+    band_rows(band, j0, cnt);
+    bulk_store(x + (long)j0 * n1, ring + (band % NS) * H * n1, (unsigned)cnt * sizeof(double2));
+  };
+  const int np = (n1 + 1) / 2;                 // pairs per row
+  const int lpr = tri_lanes_per_row(np);
+  // a thread owns its pair in U rows of its class (U = 2 when H is a multiple of 4: half the band steps for the
+  // same per-step overhead -- wait, fence, barriers -- which dominates a step of so little arithmetic)
+  constexpr int UMAX = 2;
+  const int U = (H & 3) == 0 ? 2 : 1;
+  const int per = (H / 2 / U) * lpr;           // threads of one row class
+  const bool copier = tid == nth - 1;
+  fence_async_global();
+  __syncthreads();
+  if (copier) {
+    load_band(0);
+    if (nb > 1) load_band(1);
+  }
+  int p = 0, kk = 0, m = 0;
+  bool has = tid < 2 * per;
+  if (has) {
+    p = tid / per;
+    const int rem = tid - p * per;
+    kk = rem / lpr;
+    m = rem - kk * lpr;
+    has = m < np;
+  }
+  const bool grouped = (per & 31) == 0;
+  const bool in_class = !grouped || tid < 2 * per;
+  const int bar_id = grouped ? 1 + p : 0, bar_threads = grouped ? per : nth;
+  const int rowoff0 = (reverse ? 1 - p : p) + 2 * kk * U;   // row u of this thread: rowoff0 + 2 u
+  // local frame: column c = 0..3 stands for 2m - 1 + c (2m + 2 - c for the reversed order); nodes at c = 1, 2
+  const int cb = reverse ? 2 * m + 2 : 2 * m - 1;
+  const int sgn = reverse ? -1 : 1;
+  const int g0 = reverse ? 2 * m + 1 : 2 * m, g1 = reverse ? 2 * m : 2 * m + 1;
+  const int cx0 = g0 == 0 ? 0 : (g0 == n1 - 1 ? 2 : 1), cx1 = g1 == 0 ? 0 : (g1 == n1 - 1 ? 2 : 1);
+  const bool in0 = has && g0 <= n1 - 1, in1 = has && g1 <= n1 - 1;
+  const double2 zero = make_double2(0.0, 0.0);
+  double2 bn0[UMAX] = {zero, zero}, bn1[UMAX] = {zero, zero};
+#pragma unroll
+  for (int u = 0; u < UMAX; ++u) {   // step 0: band 0 for p = 0
+    const int jr = rowoff0 + 2 * u;
+    if (u < U && p == 0 && jr <= n1 - 1) {
+      if (in0) bn0[u] = b[jr * n1 + g0];
+      if (in1) bn1[u] = b[jr * n1 + g1];
+    }
+  }
+  int slot = (NS - 2 * p) % NS;
+  for (int T = 0; T <= nb + 2; ++T) {
+    if (T == 0) wait_band(0);
+    if (T + 1 < nb) wait_band(T + 1);
+    fence_async_smem();
+    __syncthreads();
+    if (copier) {
+      bulk_wait_read1();
+      if (T + 2 < nb) load_band(T + 2);
+      if (T - 3 >= 0 && T - 3 < nb) store_band(T - 3);
+    }
+    const int band = T - 2 * p;
+    const bool bandon = has && band >= 0 && band < nb;
+    const bool band1on = band + 1 >= 0 && band + 1 < nb;
+    const int rs = slot * H;
+    slot = slot == NS - 1 ? 0 : slot + 1;
+    double2 acc0[UMAX], acc1[UMAX], xo0[UMAX], xo1[UMAX], x0n[UMAX];
+    double t10[UMAX], t12[UMAX], w0[UMAX], w1[UMAX];
+    bool act0[UMAX], act1[UMAX];
+#pragma unroll
+    for (int u = 0; u < UMAX; ++u) {
+      acc0[u] = make_double2(-bn0[u].x, -bn0[u].y);
+      acc1[u] = make_double2(-bn1[u].x, -bn1[u].y);
+      const int j1 = (band + 1) * H + rowoff0 + 2 * u;
+      const bool on1 = u < U && band1on && j1 >= 0 && j1 <= n1 - 1;
+      bn0[u] = (on1 && in0) ? b[j1 * n1 + g0] : zero;
+      bn1[u] = (on1 && in1) ? b[j1 * n1 + g1] : zero;
+    }
+    if (!in_class) continue;
+#pragma unroll
+    for (int u = 0; u < UMAX; ++u) {
+      const int ro = rowoff0 + 2 * u;
+      const int j = band * H + ro;
+      const bool on = u < U && bandon && j >= 0 && j <= n1 - 1;
+      const int r0 = rs + ro;
+      const int cy = j == 0 ? 0 : (j == n1 - 1 ? 2 : 1);
+      const double* T0 = tabl + (cy * 3 + cx0) * 10;
+      const double* T1 = tabl + (cy * 3 + cx1) * 10;
+      act0[u] = on && in0 && !(j == 0 && g0 == 0);   // (pinned corner)
+      act1[u] = on && in1 && !(j == 0 && g1 == 0);
+      xo0[u] = xo1[u] = zero;
+      t10[u] = t12[u] = w0[u] = w1[u] = 0.0;
+      if (on) {
+#pragma unroll
+        for (int ob = 0; ob < 3; ++ob) {
+          int r = r0 + ob - 1;
+          r += r < 0 ? RR : 0;
+          r -= r >= RR ? RR : 0;
+          const double2* row = ring + r * n1 + cb;
+          const double2 v0 = row[0], v1 = row[sgn], v2 = row[2 * sgn], v3 = row[3 * sgn];
+          const double a0 = T0[ob * 3 + (reverse ? 2 : 0)], a1 = T0[ob * 3 + 1], a2 = T0[ob * 3 + (reverse ? 0 : 2)];
+          const double c0 = T1[ob * 3 + (reverse ? 2 : 0)], c1 = T1[ob * 3 + 1], c2 = T1[ob * 3 + (reverse ? 0 : 2)];
+          acc0[u] = cfma(a0, v0, acc0[u]);
+          acc0[u] = cfma(a1, v1, acc0[u]);
+          acc0[u] = cfma(a2, v2, acc0[u]);
+          if (ob != 1) {
+            acc1[u] = cfma(c0, v1, acc1[u]);
+            acc1[u] = cfma(c1, v2, acc1[u]);
+            acc1[u] = cfma(c2, v3, acc1[u]);
+          } else {   // row j: the second node takes its two fresh taps after the first colour
+            xo0[u] = v1;
+            xo1[u] = v2;
+            acc1[u] = cfma(c1, v2, acc1[u]);
+            t10[u] = c0;
+            t12[u] = c2;
+          }
+        }
+        w0[u] = omega * T0[9];
+        w1[u] = omega * T1[9];
+      }
+      x0n[u] = xo0[u];
+      if (act0[u]) {
+        x0n[u] = make_double2(xo0[u].x - w0[u] * acc0[u].x, xo0[u].y - w0[u] * acc0[u].y);
+        ring[r0 * n1 + cb + sgn] = x0n[u];
+      }
+    }
+    class_sync(bar_id, bar_threads);
+#pragma unroll
+    for (int u = 0; u < UMAX; ++u) {
+      if (act1[u]) {
+        double2* rowj = ring + (rs + rowoff0 + 2 * u) * n1 + cb;
+        const double2 v3 = rowj[3 * sgn];
+        double2 a = cfma(t10[u], x0n[u], acc1[u]);
+        a = cfma(t12[u], v3, a);
+        rowj[2 * sgn] = make_double2(xo1[u].x - w1[u] * a.x, xo1[u].y - w1[u] * a.y);
+      }
+    }
+  }
+  __syncthreads();
+  if (copier) {
+    bulk_wait_all();
+    fence_async_global();
+  }
+  if (tid == 0) *phase_word = phase;
+  __syncthreads();
+}
+
 // ---- z-band wavefront sweeps in line form (3-D Q2, real class stencils) -------------------------------------------
 // The schedule of the 3-D z-band wavefront (planes in bands of 3, band B updates its plane of z-class c' at step
 // B + 2 c', the 9 xy-colours of a step in order), with the work of a step given to warps line by line: a warp owns
@@ -1767,6 +1943,12 @@ __device__ __forceinline__ bool cta_sweep(const Grid& g, const Coef& cf, const d
         }
       }
       return rout != nullptr && sweeps > 0 && !reverse;
+    }
+  }
+  if constexpr (DIM == 2 && ORD == 1 && !CONV && !W) {
+    if (ring && waveH && tabl) {
+      for (int sw = 0; sw < sweeps; ++sw) q1_pair_pass(tabl, x, b, ring, g.n1, waveH, reverse, omega, tid, nth, mbar);
+      return false;
     }
   }
   if constexpr (DIM == 3 && ORD == 2 && TAB && !W && !CONV) {
@@ -2179,6 +2361,18 @@ __global__ void __launch_bounds__(mg_threads<DIM, TAB, CONV, ORD>(), mg_minb<DIM
         build_class_tab_q1(a.g[l], cf.a.x, cf.b.x, ctab + l * Q1TAB, tid, nth);
         __syncthreads();
       }
+    }
+  }
+  if constexpr (ORD == 1 && DIM == 2 && !CONV) {
+    if (a.wave_h) {   // pair-form wavefront sweeps: zeroed ring with guards, band-slot mbarriers
+      for (long e = a.ring_off - MG_RING_GUARD + tid; e < a.mbar_off; e += nth) smem[e] = make_double2(0.0, 0.0);
+      if (tid == 0) {
+        unsigned long long* mb = reinterpret_cast<unsigned long long*>(smem + a.mbar_off);
+        for (int sl = 0; sl < MG_TRI_SLOTS; ++sl) mbar_init(mb + sl, 1);
+        *reinterpret_cast<unsigned*>(mb + MG_TRI_SLOTS) = 0u;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      __syncthreads();
     }
   }
   if (TAB) {
