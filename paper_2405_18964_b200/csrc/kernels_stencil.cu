@@ -25,6 +25,21 @@ namespace aao {
 #ifndef MG_MINB_Q1
 #define MG_MINB_Q1 1
 #endif
+// M_p Chebyshev of the 2-D Q1 space: pure streaming (five vectors per step), so several smaller CTAs per SM
+#ifndef CHEB_THREADS_Q1
+#define CHEB_THREADS_Q1 512
+#endif
+#ifndef CHEB_MINB_Q1
+#define CHEB_MINB_Q1 2   // measured c4_512: pressure solves 27.1 (512 x 1) / 24.35 (512 x 2) / 25.8 ms (256 x 3, 256 x 4)
+#endif
+template <int DIM, int ORD>
+constexpr int cheb_threads() {
+  return DIM == 2 && ORD == 1 ? CHEB_THREADS_Q1 : MG_THREADS;
+}
+template <int DIM, int ORD>
+constexpr int cheb_minb() {
+  return DIM == 2 && ORD == 1 ? CHEB_MINB_Q1 : 1;
+}
 
 // ---------------------------------------------------------------- complex helpers
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -2440,7 +2455,7 @@ __global__ void __launch_bounds__(mg_threads<DIM, TAB, CONV, ORD>(), mg_minb<DIM
 
 // Chebyshev semi-iteration on a mass matrix, one CTA per problem
 template <int DIM, int ORD>
-__global__ void __launch_bounds__(mg_threads<DIM, false, false, ORD>(), mg_minb<DIM, ORD>()) k_cheb_cta(Grid g, View bv, View xv, double2* rw, double2* d0w, double2* d1w,
+__global__ void __launch_bounds__(cheb_threads<DIM, ORD>(), cheb_minb<DIM, ORD>()) k_cheb_cta(Grid g, View bv, View xv, double2* rw, double2* d0w, double2* d1w,
                                                    double theta, double sigma, double delta, int iters, double scale) {
   const int p = blockIdx.x;
   const double2* b = bv.p + voff(bv, p, g.n);
@@ -2649,8 +2664,8 @@ void launch_mg_cta(const MGArgs& a, int nprob, size_t smem, cudaStream_t s) {
 template <int DIM, int ORD>
 static void chcta_t(const Grid& g, View b, View x, double2* r, double2* d0, double2* d1, double theta, double sigma,
                     double delta, int iters, double scale, int nprob, cudaStream_t s) {
-  k_cheb_cta<DIM, ORD><<<nprob, mg_threads<DIM, false, false, ORD>(), 0, s>>>(g, b, x, r, d0, d1, theta, sigma, delta,
-                                                                            iters, scale);
+  k_cheb_cta<DIM, ORD><<<nprob, cheb_threads<DIM, ORD>(), 0, s>>>(g, b, x, r, d0, d1, theta, sigma, delta, iters,
+                                                                  scale);
 }
 void launch_cheb_cta(const Grid& g, View b, View x, double2* r, double2* d0, double2* d1, double theta, double sigma,
                      double delta, int iters, double scale, int nprob, cudaStream_t s) {
